@@ -1,0 +1,199 @@
+/*
+ * rkmf_b200 — C ABI of the B200-native restarted randomized-Arnoldi f(A)b
+ * hot path (arXiv 2503.22631; reference artifact `rkmf`, /root/reference/proj).
+ *
+ * Plain pointers and sizes only: no torch or CUDA types in the signatures
+ * (a cudaStream_t is passed as void*). Every entry point returns a status
+ * code that mirrors the reference's exception hierarchy
+ * (proj/include/rkmf/types.hpp:25-48); the message of the last failure is
+ * available from rkmf_last_error(). The C++ wrapper include/rkmf_b200.hpp
+ * rethrows the reference exception types with the same message prefixes.
+ *
+ * Device pointers ("d_" prefix) must be cudaMalloc'ed on the context's device.
+ * Host pointers ("h_" prefix) are plain host memory (pinned or pageable).
+ * Calls are synchronous with respect to the host unless stated otherwise:
+ * like the reference, one solve runs at a time per context; distinct
+ * contexts are independent (proj/src/restart.cpp:267-299).
+ */
+#ifndef RKMF_B200_H
+#define RKMF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: types.hpp:25-48 (Error / ShapeError / ParameterError /
+ *      NumericalError) plus device-side failures ---- */
+#define RKMF_OK 0
+#define RKMF_PARAMETER_ERROR 1 /* rkmf::ParameterError */
+#define RKMF_SHAPE_ERROR 2     /* rkmf::ShapeError */
+#define RKMF_NUMERICAL_ERROR 3 /* rkmf::NumericalError */
+#define RKMF_DEVICE_ERROR 4    /* CUDA / NCCL failure (rkmf::Error) */
+#define RKMF_INTERNAL_ERROR 5  /* rkmf::Error */
+
+/* ---- function kinds: densefun.hpp:20 FunctionSpec::Kind. EXP_NEG is the
+ *      reference's ExpNeg(t): f(z) = exp(-t z). INV_SQRT (f(z) = z^{-1/2}) is
+ *      an extension required by BASELINE cfg3; the reference has no such kind. */
+#define RKMF_FN_EXP_NEG 0
+#define RKMF_FN_INV_SQRT 4
+
+/* ---- dense-f evaluation strategy (rkmf_restart_options.dense_f) ---- */
+#define RKMF_DENSE_AUTO 0       /* FULL for EXP_NEG, QUADRATURE for INV_SQRT */
+#define RKMF_DENSE_FULL 1       /* f(R_accum) in full every cycle, restart.cpp:72-78 */
+#define RKMF_DENSE_QUADRATURE 2 /* restart quadrature, O(N_q m^2) per cycle */
+
+typedef struct rkmf_context rkmf_context;
+typedef struct rkmf_matrix rkmf_matrix; /* device CSR, sparse.hpp:16-24 */
+typedef struct rkmf_sketch rkmf_sketch; /* device SketchOperator, sketch.hpp:16-24 */
+
+/* Replaces restart::RestartOptions (restart.hpp:20-26). Defaults via
+ * rkmf_restart_options_default(): m_r=20, tol=1e-10, k_max=100,
+ * budget_total_m=4000, divergence_factor=1e6. */
+typedef struct {
+  int64_t m_r;
+  double tol; /* absolute: stop when ||y_k|| <= tol (restart.cpp:113) */
+  int64_t k_max;
+  int64_t budget_total_m;
+  double divergence_factor;
+  int32_t dense_f;        /* RKMF_DENSE_* */
+  int32_t quad_nodes;     /* quadrature nodes (0 = default 512) */
+} rkmf_restart_options;
+
+/* Replaces restart::CycleRecord (restart.hpp:28-40). kappa_W and
+ * leftmost_ritz_re are per-cycle diagnostics of the reference
+ * (restart.cpp:101,103) that are not on the device hot path: NaN. Times are
+ * device times from CUDA events. */
+typedef struct {
+  int64_t cycle;
+  int64_t total_m;
+  int64_t total_matvecs;
+  double update_norm;
+  double error_vs_reference; /* NaN when no reference vector was given */
+  double kappa_W;
+  double leftmost_ritz_re;
+  double alpha_dev;
+  double elapsed_ms;
+  double build_ms;
+  double funm_ms;
+  double start_norm;
+  double subdiag;
+} rkmf_cycle_record;
+
+/* Replaces restart::RestartResult (restart.hpp:56-65) minus f_hat (written
+ * to the caller's buffer) and R_accum (rkmf_last_r_accum). Counters are
+ * PerfCounters (types.hpp:57-75). */
+typedef struct {
+  int64_t converged;
+  int64_t cycles;
+  int64_t total_m;
+  double alpha;
+  int64_t matvecs;
+  int64_t dot_n;
+  int64_t dot_d;
+  int64_t basis_updates;
+  int64_t peak_basis_cols;
+  int64_t n_records;
+  double solve_ms; /* device time of the whole solve (CUDA events) */
+} rkmf_restart_result;
+
+/* ---- context ---- */
+int rkmf_context_create(int device, rkmf_context** out);
+int rkmf_context_destroy(rkmf_context* ctx);
+const char* rkmf_last_error(const rkmf_context* ctx);
+/* Launch all work on this cudaStream_t (NULL = the context's own stream). */
+int rkmf_context_set_stream(rkmf_context* ctx, void* cuda_stream);
+void rkmf_restart_options_default(rkmf_restart_options* opts);
+/* Number of this library's kernels launched so far on the context. */
+int64_t rkmf_context_launch_count(const rkmf_context* ctx);
+
+/* Per-kernel-class device timing: CUDA events around every launch of the
+ * solve (off by default; adds ~1 us gaps, so keep it out of headline runs).
+ * Classes: 0 spmv_sketch (K2), 1 rgs_step (K3), 2 basis_update (K4),
+ * 3 dense f (K6), 4 final_update (K5), 5 start sketch + init (K7). */
+#define RKMF_KCLASS_COUNT 6
+int rkmf_context_kernel_timing(rkmf_context* ctx, int enable);
+/* ms[6] accumulated device milliseconds, launches[6] counts; reset != 0 clears. */
+int rkmf_context_kernel_times(rkmf_context* ctx, double* ms, int64_t* launches, int reset);
+
+/* ---- CSR matrices (sparse.hpp:16-24). Columns int32; row pointers int64 on
+ *      the host side; stored on device as int32 when nnz < 2^31. The matrix is
+ *      validated on creation (sparse.cpp:61-81) instead of every cycle as the
+ *      reference does (basis.cpp:15); norm1 (sparse.cpp:97-102) is cached. ---- */
+int rkmf_matrix_create_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
+                            const int64_t* h_row_ptr, const int32_t* h_col_idx,
+                            const double* h_values, rkmf_matrix** out);
+/* Device arrays are copied (the caller keeps ownership of its buffers). */
+int rkmf_matrix_create_device(rkmf_context* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                              const int64_t* d_row_ptr, const int32_t* d_col_idx,
+                              const double* d_values, rkmf_matrix** out);
+int rkmf_matrix_destroy(rkmf_matrix* A);
+int rkmf_matrix_info(const rkmf_matrix* A, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
+                     double* norm1);
+
+/* ---- sketch operator: make_sketch (sketch.cpp:13-49), generated on device,
+ *      bit-identical to the reference's SplitMix64/Floyd definition ---- */
+int rkmf_sketch_create(rkmf_context* ctx, int64_t d, int64_t n, int64_t zeta, uint64_t seed,
+                       rkmf_sketch** out);
+int rkmf_sketch_destroy(rkmf_sketch* S);
+/* SketchOperator::scale (default 1/sqrt(zeta)); settable as the reference's
+ * tests do (test_sketch.cpp:162-173). */
+int rkmf_sketch_set_scale(rkmf_sketch* S, double scale);
+/* Copies rows (n*zeta int64) and signs (n*zeta int8) to the host. */
+int rkmf_sketch_export(rkmf_context* ctx, const rkmf_sketch* S, int64_t* h_rows, int8_t* h_signs,
+                       double* h_scale);
+
+/* ---- single operations on device vectors ---- */
+/* y = A x  (sparse.cpp:83-95) */
+int rkmf_spmv(rkmf_context* ctx, const rkmf_matrix* A, const double* d_x, double* d_y);
+/* y = S x  (sketch.cpp:51-63) */
+int rkmf_sketch_apply(rkmf_context* ctx, const rkmf_sketch* S, const double* d_x, double* d_y);
+/* z = A x and p = S z in one pass (the fused K2 kernel) */
+int rkmf_spmv_sketch(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
+                     const double* d_x, double* d_z, double* d_p);
+
+/* ---- one randomized Arnoldi decomposition: basis.cpp:92-142 ----
+ * d_W: n x (m+1) column-major with leading dimension ldw >= n (device);
+ * d_U: d x (m+1) column-major (device); h_Rbar: (m+1) x m column-major (host).
+ * *mk = m, or the kept size k+1 after a breakdown (*breakdown_at = k+1,
+ * else 0). counters[5] = {matvecs, dot_n, dot_d, basis_updates, peak_basis_cols}. */
+int rkmf_randomized_arnoldi(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
+                            const double* d_b, int64_t m, double* d_W, int64_t ldw, double* d_U,
+                            double* h_Rbar, double* start_norm, int64_t* mk,
+                            int64_t* breakdown_at, int64_t* counters);
+
+/* ---- the drop-in boundary: restart::restarted_krylov (restart.hpp:74-79,
+ *      restart.cpp:27-122) with S != nullptr (randomized builder).
+ * b and f_out are host or device pointers (b_on_device / f_on_device).
+ * reference (optional, same residency as b) fills error_vs_reference.
+ * records: caller array of records_cap entries (may be NULL). ---- */
+int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
+                          const double* b, int b_on_device, int32_t fn_kind, double fn_t,
+                          const rkmf_restart_options* opts, double* f_out, int f_on_device,
+                          const double* reference, rkmf_restart_result* result,
+                          rkmf_cycle_record* records, int64_t records_cap);
+
+/* R_accum of the last solve on this context (total_m x total_m, column-major,
+ * host); n_cap is the caller's capacity in rows. */
+int rkmf_last_r_accum(rkmf_context* ctx, double* h_R, int64_t n_cap, int64_t* total_m);
+
+/* ---- synthetic inputs for the BASELINE configs (host, deterministic) ----
+ * Node ordering (ix*ny+iy)*nz+iz as problems.cpp:30-32. Two-call pattern:
+ * call with NULL arrays to get n and nnz, then with buffers. */
+int rkmf_gen_laplacian(int32_t dim, int64_t N, int64_t* n, int64_t* nnz, int64_t* h_row_ptr,
+                       int32_t* h_col_idx, double* h_values);
+int rkmf_gen_q1_hex(int64_t N, int32_t lognormal, uint64_t coef_seed, int32_t dirichlet,
+                    int64_t* n, int64_t* nnz, int64_t* h_row_ptr, int32_t* h_col_idx,
+                    double* h_values);
+int rkmf_gen_convdiff_upwind(int64_t N, double peclet, double vx, double vy, double vz,
+                             int64_t* n, int64_t* nnz, int64_t* h_row_ptr, int32_t* h_col_idx,
+                             double* h_values);
+/* b[i] = first N(0,1) draw of SplitMix64(derive(seed, i)) (rng.hpp:47-59). */
+int rkmf_gen_gaussian(uint64_t seed, int64_t n, double* h_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RKMF_B200_H */

@@ -1,0 +1,568 @@
+"""rkmf_b200 — B200-native restarted randomized-Arnoldi f(A)b (arXiv 2503.22631).
+
+Python mirror of the reference artifact's solver interface
+(/root/reference/proj/include/rkmf/restart.hpp, sketch.hpp, basis.hpp,
+densefun.hpp) over the C ABI in include/rkmf_b200.h. The compute path is the
+hand-written sm_100a library ``_lib/librkmf_b200.so``; there is no CPU
+fallback: if the library or a CUDA device is missing, calls raise.
+
+Reference name map (reference -> here):
+    restart::restarted_krylov        -> restarted_krylov
+    restart::RestartOptions          -> RestartOptions
+    restart::RestartResult           -> RestartResult
+    restart::CycleRecord             -> CycleRecord
+    sketch::make_sketch              -> make_sketch   (device-generated, bit-exact)
+    sketch::sketch_apply(S, vec)     -> sketch_apply
+    sparse::spmv                     -> spmv
+    basis::randomized_arnoldi        -> randomized_arnoldi
+    densefun::FunctionSpec::exp_neg  -> FunctionSpec.exp_neg
+    (new) z^{-1/2}                   -> FunctionSpec.inv_sqrt
+    rkmf::{Error, ShapeError, ParameterError, NumericalError} -> same names
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "librkmf_b200.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+RKMF_OK = 0
+FN_EXP_NEG = 0
+FN_INV_SQRT = 4
+DENSE_AUTO, DENSE_FULL, DENSE_QUADRATURE = 0, 1, 2
+
+
+# ---- error hierarchy: types.hpp:25-48 ----
+class Error(RuntimeError):
+    """rkmf::Error"""
+
+
+class ShapeError(Error):
+    """rkmf::ShapeError"""
+
+
+class ParameterError(Error):
+    """rkmf::ParameterError"""
+
+
+class ParseError(Error):
+    """rkmf::ParseError"""
+
+
+class NumericalError(Error):
+    """rkmf::NumericalError"""
+
+
+class DeviceError(Error):
+    """CUDA / NCCL failure inside the device library."""
+
+
+_CODE = {1: ParameterError, 2: ShapeError, 3: NumericalError, 4: DeviceError, 5: Error}
+
+
+class RestartOptionsC(C.Structure):
+    _fields_ = [("m_r", C.c_int64), ("tol", C.c_double), ("k_max", C.c_int64),
+                ("budget_total_m", C.c_int64), ("divergence_factor", C.c_double),
+                ("dense_f", C.c_int32), ("quad_nodes", C.c_int32)]
+
+
+class CycleRecordC(C.Structure):
+    _fields_ = [("cycle", C.c_int64), ("total_m", C.c_int64), ("total_matvecs", C.c_int64),
+                ("update_norm", C.c_double), ("error_vs_reference", C.c_double),
+                ("kappa_W", C.c_double), ("leftmost_ritz_re", C.c_double),
+                ("alpha_dev", C.c_double), ("elapsed_ms", C.c_double), ("build_ms", C.c_double),
+                ("funm_ms", C.c_double), ("start_norm", C.c_double), ("subdiag", C.c_double)]
+
+
+class RestartResultC(C.Structure):
+    _fields_ = [("converged", C.c_int64), ("cycles", C.c_int64), ("total_m", C.c_int64),
+                ("alpha", C.c_double), ("matvecs", C.c_int64), ("dot_n", C.c_int64),
+                ("dot_d", C.c_int64), ("basis_updates", C.c_int64),
+                ("peak_basis_cols", C.c_int64), ("n_records", C.c_int64),
+                ("solve_ms", C.c_double)]
+
+
+# Every symbol declared in include/rkmf_b200.h: (name, restype, argtypes)
+_P, _I64, _U64, _D, _I32 = C.c_void_p, C.c_int64, C.c_uint64, C.c_double, C.c_int32
+_PP = C.POINTER(C.c_void_p)
+SYMBOLS = [
+    ("rkmf_context_create", C.c_int, [C.c_int, _PP]),
+    ("rkmf_context_destroy", C.c_int, [_P]),
+    ("rkmf_last_error", C.c_char_p, [_P]),
+    ("rkmf_context_set_stream", C.c_int, [_P, _P]),
+    ("rkmf_restart_options_default", None, [_P]),
+    ("rkmf_context_launch_count", C.c_int64, [_P]),
+    ("rkmf_context_kernel_timing", C.c_int, [_P, C.c_int]),
+    ("rkmf_context_kernel_times", C.c_int, [_P, _P, _P, C.c_int]),
+    ("rkmf_matrix_create_host", C.c_int, [_P, _I64, _I64, _P, _P, _P, _PP]),
+    ("rkmf_matrix_create_device", C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _PP]),
+    ("rkmf_matrix_destroy", C.c_int, [_P]),
+    ("rkmf_matrix_info", C.c_int, [_P, _P, _P, _P, _P]),
+    ("rkmf_sketch_create", C.c_int, [_P, _I64, _I64, _I64, _U64, _PP]),
+    ("rkmf_sketch_destroy", C.c_int, [_P]),
+    ("rkmf_sketch_set_scale", C.c_int, [_P, _D]),
+    ("rkmf_sketch_export", C.c_int, [_P, _P, _P, _P, _P]),
+    ("rkmf_spmv", C.c_int, [_P, _P, _P, _P]),
+    ("rkmf_sketch_apply", C.c_int, [_P, _P, _P, _P]),
+    ("rkmf_spmv_sketch", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("rkmf_randomized_arnoldi", C.c_int,
+     [_P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
+    ("rkmf_restarted_krylov", C.c_int,
+     [_P, _P, _P, _P, C.c_int, _I32, _D, _P, _P, C.c_int, _P, _P, _P, _I64]),
+    ("rkmf_last_r_accum", C.c_int, [_P, _P, _I64, _P]),
+    ("rkmf_gen_laplacian", C.c_int, [_I32, _I64, _P, _P, _P, _P, _P]),
+    ("rkmf_gen_q1_hex", C.c_int, [_I64, _I32, _U64, _I32, _P, _P, _P, _P, _P]),
+    ("rkmf_gen_convdiff_upwind", C.c_int, [_I64, _D, _D, _D, _D, _P, _P, _P, _P, _P]),
+    ("rkmf_gen_gaussian", C.c_int, [_U64, _I64, _P]),
+]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the sm_100a library in-tree (nvcc -gencode arch=compute_100a,code=sm_100a)."""
+    jobs = str(max(1, min(8, os.cpu_count() or 1)))
+    if force:
+        subprocess.run(["make", "-s", "-C", CSRC, "clean"], check=True)
+    subprocess.run(["make", "-s", "-j", jobs, "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load the device library; raises if it is missing (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"rkmf_b200 CUDA library not built: {LIB_PATH} "
+                              "(run paper_2503_22631_b200.build() or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SYMBOLS:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a) -> Optional[int]:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return int(a.data_ptr())  # torch tensor
+
+
+def _is_torch(a) -> bool:
+    return hasattr(a, "data_ptr") and hasattr(a, "is_cuda")
+
+
+class Context:
+    """One device + stream (rkmf_context). Solves on one context are serialised."""
+
+    _default = {}
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        code = lib().rkmf_context_create(device, C.byref(h))
+        if code != RKMF_OK:
+            raise _CODE.get(code, Error)(f"rkmf_context_create failed (code {code}): "
+                                         "no CUDA device? (there is no CPU fallback)")
+        self.h = h
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    def check(self, code: int):
+        if code != RKMF_OK:
+            msg = lib().rkmf_last_error(self.h).decode()
+            raise _CODE.get(code, Error)(msg)
+
+    def set_stream(self, stream) -> None:
+        """Launch on a torch.cuda.Stream / raw cudaStream_t (None = own stream)."""
+        raw = None if stream is None else getattr(stream, "cuda_stream", stream)
+        self.check(lib().rkmf_context_set_stream(self.h, raw))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().rkmf_context_launch_count(self.h))
+
+    KERNEL_CLASSES = ("spmv_sketch", "rgs_step", "basis_update", "dense_f", "final_update",
+                      "start_sketch_init")
+
+    def kernel_timing(self, enable: bool) -> None:
+        """Events around every solve launch (diagnostic runs only)."""
+        self.check(lib().rkmf_context_kernel_timing(self.h, int(enable)))
+
+    def kernel_times(self, reset: bool = True) -> dict:
+        ms = np.zeros(6)
+        cnt = np.zeros(6, np.int64)
+        self.check(lib().rkmf_context_kernel_times(self.h, _ptr(ms), _ptr(cnt), int(reset)))
+        return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(self.KERNEL_CLASSES)}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().rkmf_context_destroy(self.h)
+        except Exception:
+            pass
+
+
+class SparseMatrix:
+    """Device CSR (sparse.hpp:16-24): int32 columns, fp64 values."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+        nr, nc, nz, n1 = C.c_int64(), C.c_int64(), C.c_int64(), C.c_double()
+        lib().rkmf_matrix_info(handle, C.byref(nr), C.byref(nc), C.byref(nz), C.byref(n1))
+        self.n_rows, self.n_cols, self.nnz, self.norm1 = nr.value, nc.value, nz.value, n1.value
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.n_cols)
+
+    @classmethod
+    def from_csr(cls, row_ptr, col_idx, values, n_cols: Optional[int] = None,
+                 ctx: Optional[Context] = None) -> "SparseMatrix":
+        ctx = ctx or Context.default()
+        if _is_torch(row_ptr) and row_ptr.is_cuda:
+            import torch
+            rp = row_ptr.to(torch.int64).contiguous()
+            ci = col_idx.to(torch.int32).contiguous()
+            v = values.to(torch.float64).contiguous()
+            n = rp.numel() - 1
+            h = C.c_void_p()
+            ctx.check(lib().rkmf_matrix_create_device(ctx.h, n, n if n_cols is None else n_cols,
+                                                      v.numel(), rp.data_ptr(), ci.data_ptr(),
+                                                      v.data_ptr(), C.byref(h)))
+            return cls(ctx, h)
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        ci = np.ascontiguousarray(col_idx, np.int32)
+        v = np.ascontiguousarray(values, np.float64)
+        n = len(rp) - 1
+        h = C.c_void_p()
+        ctx.check(lib().rkmf_matrix_create_host(ctx.h, n, n if n_cols is None else n_cols,
+                                                _ptr(rp), _ptr(ci), _ptr(v), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_scipy(cls, A, ctx: Optional[Context] = None) -> "SparseMatrix":
+        A = A.tocsr()
+        A.sort_indices()
+        return cls.from_csr(A.indptr, A.indices, A.data, A.shape[1], ctx)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().rkmf_matrix_destroy(self.h)
+        except Exception:
+            pass
+
+
+class SketchOperator:
+    """Device sparse-sign embedding S in R^{d x n} (sketch.hpp:16-24)."""
+
+    def __init__(self, ctx: Context, handle, d, n, zeta, seed):
+        self.ctx, self.h, self.d, self.n, self.zeta, self.seed = ctx, handle, d, n, zeta, seed
+        self._scale = 1.0 / math.sqrt(zeta)
+
+    @property
+    def scale(self) -> float:
+        return self._scale
+
+    @scale.setter
+    def scale(self, value: float) -> None:
+        lib().rkmf_sketch_set_scale(self.h, float(value))
+        self._scale = float(value)
+
+    def export(self):
+        """(rows int64[n*zeta], signs int8[n*zeta], scale) on the host."""
+        rows = np.empty(self.n * self.zeta, np.int64)
+        signs = np.empty(self.n * self.zeta, np.int8)
+        sc = C.c_double()
+        self.ctx.check(lib().rkmf_sketch_export(self.ctx.h, self.h, _ptr(rows), _ptr(signs),
+                                                C.byref(sc)))
+        return rows, signs, sc.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().rkmf_sketch_destroy(self.h)
+        except Exception:
+            pass
+
+
+def make_sketch(d: int, n: int, zeta: int, seed: int, ctx: Optional[Context] = None) -> SketchOperator:
+    """sketch::make_sketch (sketch.cpp:13-49), generated on the device."""
+    ctx = ctx or Context.default()
+    h = C.c_void_p()
+    ctx.check(lib().rkmf_sketch_create(ctx.h, d, n, zeta, C.c_uint64(seed), C.byref(h)))
+    return SketchOperator(ctx, h, d, n, zeta, seed)
+
+
+def _dev(x, ctx: Context):
+    import torch
+    if _is_torch(x) and x.is_cuda:
+        return x.to(torch.float64).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x, np.float64)).to(f"cuda:{ctx.device}")
+
+
+def spmv(A: SparseMatrix, x):
+    """z = A x (sparse.cpp:83-95); returns a CUDA tensor."""
+    import torch
+    xd = _dev(x, A.ctx)
+    if xd.numel() != A.n_cols:
+        raise ShapeError("shape: spmv expects len(x) == n_cols")
+    y = torch.empty(A.n_rows, dtype=torch.float64, device=xd.device)
+    A.ctx.check(lib().rkmf_spmv(A.ctx.h, A.h, xd.data_ptr(), y.data_ptr()))
+    return y
+
+
+def sketch_apply(S: SketchOperator, x):
+    """y = S x (sketch.cpp:51-63); returns a CUDA tensor."""
+    import torch
+    xd = _dev(x, S.ctx)
+    if xd.numel() != S.n:
+        raise ShapeError("shape: sketch_apply expects len(x) == n")
+    y = torch.empty(S.d, dtype=torch.float64, device=xd.device)
+    S.ctx.check(lib().rkmf_sketch_apply(S.ctx.h, S.h, xd.data_ptr(), y.data_ptr()))
+    return y
+
+
+def spmv_sketch(A: SparseMatrix, S: SketchOperator, x):
+    """(A x, S A x) from the fused kernel."""
+    import torch
+    xd = _dev(x, A.ctx)
+    z = torch.empty(A.n_rows, dtype=torch.float64, device=xd.device)
+    p = torch.empty(S.d, dtype=torch.float64, device=xd.device)
+    A.ctx.check(lib().rkmf_spmv_sketch(A.ctx.h, A.h, S.h, xd.data_ptr(), z.data_ptr(),
+                                       p.data_ptr()))
+    return z, p
+
+
+@dataclass
+class KrylovDecomposition:
+    """basis::KrylovDecomposition (basis.hpp:22-41), sketched-orthonormal kind."""
+    W: object  # CUDA tensor n x cols
+    U: object  # CUDA tensor d x cols
+    Rbar: np.ndarray
+    start_norm: float
+    breakdown_at: Optional[int]
+    counters: dict
+
+    def m(self) -> int:
+        return self.Rbar.shape[1]
+
+    def Rm(self) -> np.ndarray:
+        return self.Rbar[: self.m(), :]
+
+    def subdiag(self) -> float:
+        return float(self.Rbar[self.m(), self.m() - 1]) if self.Rbar.shape[0] > self.m() else 0.0
+
+
+def randomized_arnoldi(A: SparseMatrix, S: SketchOperator, b, m: int) -> KrylovDecomposition:
+    """basis::randomized_arnoldi (basis.cpp:92-142) on the device."""
+    import torch
+    bd = _dev(b, A.ctx)
+    n = A.n_rows
+    if bd.numel() != n:
+        raise ShapeError("arnoldi: start vector length mismatch")
+    W = torch.zeros((m + 1, n), dtype=torch.float64, device=bd.device)  # column-major n x (m+1)
+    U = torch.zeros((m + 1, S.d), dtype=torch.float64, device=bd.device)
+    R = np.zeros((m, m + 1))  # column-major (m+1) x m
+    sn, mk, bk = C.c_double(), C.c_int64(), C.c_int64()
+    ctr = np.zeros(5, np.int64)
+    A.ctx.check(lib().rkmf_randomized_arnoldi(A.ctx.h, A.h, S.h, bd.data_ptr(), m, W.data_ptr(),
+                                              n, U.data_ptr(), _ptr(R), C.byref(sn), C.byref(mk),
+                                              C.byref(bk), _ptr(ctr)))
+    k = mk.value
+    cols = k + 1 if bk.value == 0 else k
+    Rbar = R.T[: (k + 1 if bk.value == 0 else k), :k].copy()
+    return KrylovDecomposition(W=W[:cols].T, U=U[:cols].T, Rbar=Rbar, start_norm=sn.value,
+                               breakdown_at=bk.value or None,
+                               counters=dict(zip(["matvecs", "dot_n", "dot_d", "basis_updates",
+                                                  "peak_basis_cols"], ctr.tolist())))
+
+
+@dataclass
+class FunctionSpec:
+    """densefun::FunctionSpec (densefun.hpp:19-32): ExpNeg(t) and the new InvSqrt."""
+    kind: int = FN_EXP_NEG
+    t: float = 1.0
+
+    @staticmethod
+    def exp_neg(t: float) -> "FunctionSpec":
+        if not (t >= 0.0):
+            raise ParameterError("FunctionSpec: t must be >= 0")
+        return FunctionSpec(FN_EXP_NEG, float(t))
+
+    @staticmethod
+    def inv_sqrt() -> "FunctionSpec":
+        return FunctionSpec(FN_INV_SQRT, 1.0)
+
+
+@dataclass
+class RestartOptions:
+    """restart::RestartOptions (restart.hpp:20-26) + device dense-f choice."""
+    m_r: int = 20
+    tol: float = 1e-10
+    k_max: int = 100
+    budget_total_m: int = 4000
+    divergence_factor: float = 1e6
+    dense_f: str = "auto"  # auto | full | quadrature
+    quad_nodes: int = 0
+
+    def to_c(self) -> RestartOptionsC:
+        mode = {"auto": DENSE_AUTO, "full": DENSE_FULL, "quadrature": DENSE_QUADRATURE}[self.dense_f]
+        return RestartOptionsC(int(self.m_r), float(self.tol), int(self.k_max),
+                               int(self.budget_total_m), float(self.divergence_factor), mode,
+                               int(self.quad_nodes))
+
+
+@dataclass
+class CycleRecord:
+    """restart::CycleRecord (restart.hpp:28-40); times are device times."""
+    cycle: int
+    total_m: int
+    total_matvecs: int
+    update_norm: float
+    error_vs_reference: Optional[float]
+    kappa_W: float
+    leftmost_ritz_re: float
+    alpha_dev: float
+    elapsed_ms: float
+    build_ms: float
+    funm_ms: float
+    start_norm: float
+    subdiag: float
+
+
+@dataclass
+class RestartResult:
+    """restart::RestartResult (restart.hpp:56-65)."""
+    f_hat: object
+    history: List[CycleRecord]
+    converged: bool
+    alpha: float
+    cycles: int
+    total_m: int
+    counters: dict
+    solve_ms: float
+    _ctx: Context = field(repr=False, default=None)
+    _R: Optional[np.ndarray] = field(repr=False, default=None)
+
+    @property
+    def R_accum(self) -> np.ndarray:
+        if self._R is None:
+            M = self.total_m
+            R = np.zeros((M, M), order="F")
+            tm = C.c_int64()
+            self._ctx.check(lib().rkmf_last_r_accum(self._ctx.h, _ptr(R), M, C.byref(tm)))
+            self._R = R if tm.value == M else None
+        return self._R
+
+
+def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions = None,
+                     S: SketchOperator = None, reference=None) -> RestartResult:
+    """restart::restarted_krylov (restart.hpp:74-79) with the randomized builder.
+
+    b may be a numpy array (host: the host<->device copies are part of the call)
+    or a CUDA tensor (device-resident); f_hat comes back in the same residency.
+    """
+    opts = opts or RestartOptions()
+    ctx = A.ctx
+    if S is None:
+        raise ParameterError("rkmf_b200: the classical builder (S == nullptr) is not on the "
+                             "device path")
+    on_dev = _is_torch(b) and b.is_cuda
+    n = A.n_rows
+    if on_dev:
+        import torch
+        bb = b.to(torch.float64).contiguous()
+        fout = torch.empty(n, dtype=torch.float64, device=bb.device)
+        ref = None if reference is None else _dev(reference, ctx)
+        bptr, fptr = bb.data_ptr(), fout.data_ptr()
+    else:
+        bb = np.ascontiguousarray(b, np.float64)
+        fout = np.zeros(n)
+        ref = None if reference is None else np.ascontiguousarray(reference, np.float64)
+        bptr, fptr = _ptr(bb), _ptr(fout)
+    if len(bb) != n:
+        raise ShapeError("arnoldi: start vector length mismatch")
+    res = RestartResultC()
+    cap = int(opts.k_max) + 1
+    recs = (CycleRecordC * cap)()
+    oc = opts.to_c()
+    ctx.check(lib().rkmf_restarted_krylov(ctx.h, A.h, S.h, bptr, 1 if on_dev else 0, f.kind,
+                                          f.t, C.byref(oc), fptr, 1 if on_dev else 0,
+                                          _ptr(ref), C.byref(res), C.cast(recs, C.c_void_p),
+                                          cap))
+    hist = []
+    for i in range(res.n_records):
+        r = recs[i]
+        d = {k: getattr(r, k) for k, _ in CycleRecordC._fields_}
+        if math.isnan(d["error_vs_reference"]):
+            d["error_vs_reference"] = None
+        hist.append(CycleRecord(**d))
+    return RestartResult(f_hat=fout, history=hist, converged=bool(res.converged), alpha=res.alpha,
+                         cycles=res.cycles, total_m=res.total_m,
+                         counters=dict(matvecs=res.matvecs, dot_n=res.dot_n, dot_d=res.dot_d,
+                                       basis_updates=res.basis_updates,
+                                       peak_basis_cols=res.peak_basis_cols),
+                         solve_ms=res.solve_ms, _ctx=ctx)
+
+
+# ---- synthetic inputs (host; need only the shared library, not a GPU) ----
+def _gen(fn, *args):
+    n, nnz = C.c_int64(), C.c_int64()
+    code = fn(*args, C.byref(n), C.byref(nnz), None, None, None)
+    if code != RKMF_OK:
+        raise ParameterError("generator: invalid parameters")
+    rp = np.empty(n.value + 1, np.int64)
+    ci = np.empty(nnz.value, np.int32)
+    v = np.empty(nnz.value, np.float64)
+    fn(*args, C.byref(n), C.byref(nnz), _ptr(rp), _ptr(ci), _ptr(v))
+    return rp, ci, v
+
+
+def gen_laplacian(dim: int, N: int):
+    """2D 5-point / 3D 7-point Dirichlet Laplacian scaled by h^-2 (CSR arrays)."""
+    return _gen(lib().rkmf_gen_laplacian, dim, N)
+
+
+def gen_q1_hex(N: int, lognormal: bool = False, coef_seed: int = 1, dirichlet: bool = False):
+    """Q1 hexahedral 27-point stiffness matrix on an N^3 node grid (CSR arrays)."""
+    return _gen(lib().rkmf_gen_q1_hex, N, int(lognormal), C.c_uint64(coef_seed), int(dirichlet))
+
+
+def gen_convdiff_upwind(N: int, peclet: float = 10.0, v=(1.0, 0.5, 0.25)):
+    """3D upwind convection-diffusion, 7-point (CSR arrays)."""
+    return _gen(lib().rkmf_gen_convdiff_upwind, N, float(peclet), float(v[0]), float(v[1]),
+                float(v[2]))
+
+
+def gen_gaussian(seed: int, n: int) -> np.ndarray:
+    """b[i] = N(0,1) draw of SplitMix64(derive(seed, i)) (rng.hpp:47-59)."""
+    out = np.empty(n)
+    lib().rkmf_gen_gaussian(C.c_uint64(seed), n, _ptr(out))
+    return out
+
+
+__all__ = ["Context", "SparseMatrix", "SketchOperator", "make_sketch", "spmv", "sketch_apply",
+           "spmv_sketch", "randomized_arnoldi", "KrylovDecomposition", "FunctionSpec",
+           "RestartOptions", "RestartResult", "CycleRecord", "restarted_krylov", "gen_laplacian",
+           "gen_q1_hex", "gen_convdiff_upwind", "gen_gaussian", "Error", "ShapeError",
+           "ParameterError", "ParseError", "NumericalError", "DeviceError", "build", "lib",
+           "SYMBOLS"]

@@ -1,0 +1,122 @@
+"""The five BASELINE.json configurations as seeded synthetic problems.
+
+Each config fixes the matrix generator, the function f, m, the sketch size
+d = s, zeta = 8 and the relative tolerance. Shared by tests and bench.py so the
+device path and the CPU oracle always see the same CSR, b, S and t.
+
+Conventions (documented in DESIGN.md):
+  * b[i] = N(0,1) from SplitMix64(derive(b_seed, i)) (rng.hpp:47-59), b_seed = 1.
+  * S = make_sketch(d, n, 8, sketch_seed = 1) (sketch.cpp:13-49).
+  * tol_abs = tol_rel * ||b||_2 (the reference's own convention,
+    proj/tests/acceptance.cpp:358).
+  * t = c / ||A||_2; ||A||_2 analytic for the Dirichlet Laplacians, else a
+    fixed-seed, fixed-iteration power iteration (on A^T A when nonsymmetric),
+    as the reference's acceptance test does (acceptance.cpp:429-437).
+  * k_max = floor(budget_total_m / m) with the reference's budget 4000.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import gen_convdiff_upwind, gen_gaussian, gen_laplacian, gen_q1_hex
+
+CONFIGS = {
+    "cfg1": dict(kind="lap2d", N=256, fn="exp_neg", c=100.0, m=30, d=120, zeta=8, tol_rel=1e-8),
+    "cfg2": dict(kind="lap3d", N=128, fn="exp_neg", c=500.0, m=50, d=200, zeta=8, tol_rel=1e-8),
+    "cfg3": dict(kind="q1", N=200, lognormal=True, dirichlet=True, fn="inv_sqrt", m=40, d=160,
+                 zeta=8, tol_rel=1e-7),
+    "cfg4": dict(kind="convdiff", N=256, peclet=10.0, v=(1.0, 0.5, 0.25), fn="exp_neg", c=200.0,
+                 m=30, d=120, zeta=8, tol_rel=1e-8),
+    "cfg5": dict(kind="q1", N=512, lognormal=False, dirichlet=False, fn="exp_neg", c=300.0, m=50,
+                 d=200, zeta=8, tol_rel=1e-8),
+}
+BUDGET_TOTAL_M = 4000
+B_SEED, SKETCH_SEED, COEF_SEED = 1, 1, 1
+
+
+@dataclass
+class Problem:
+    name: str
+    n: int
+    nnz: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    b: np.ndarray
+    fn: str
+    t: float
+    m: int
+    d: int
+    zeta: int
+    tol: float  # absolute
+    k_max: int
+    norm2: float
+
+    def scipy(self):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.values, self.col_idx, self.row_ptr), shape=(self.n, self.n))
+
+
+def lap_lambda_max(dim: int, N: int) -> float:
+    h = 1.0 / (N + 1)
+    return (4.0 * dim / (h * h)) * math.sin(N * math.pi / (2 * N + 2)) ** 2
+
+
+def power_norm2(rp, ci, v, n, symmetric: bool, iters: int = 60, seed: int = 7) -> float:
+    """Deterministic power iteration for ||A||_2 (host, scipy)."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix((v, ci, rp), shape=(n, n))
+    x = gen_gaussian(seed, n)
+    x /= np.linalg.norm(x)
+    lam = 0.0
+    for _ in range(iters):
+        y = A @ x if symmetric else A.T @ (A @ x)
+        lam = float(np.linalg.norm(y))
+        x = y / lam
+    return lam if symmetric else math.sqrt(lam)
+
+
+def build(name: str, N: Optional[int] = None, with_b: bool = True) -> Problem:
+    """Build config `name`; N overrides the grid size (scaled-down parity cases)."""
+    cfg = dict(CONFIGS[name])
+    N = int(N or cfg["N"])
+    kind = cfg["kind"]
+    if kind == "lap2d":
+        rp, ci, v = gen_laplacian(2, N)
+        norm2 = lap_lambda_max(2, N)
+    elif kind == "lap3d":
+        rp, ci, v = gen_laplacian(3, N)
+        norm2 = lap_lambda_max(3, N)
+    elif kind == "q1":
+        rp, ci, v = gen_q1_hex(N, cfg["lognormal"], COEF_SEED, cfg["dirichlet"])
+        norm2 = power_norm2(rp, ci, v, len(rp) - 1, True) if cfg["fn"] == "exp_neg" else 0.0
+    elif kind == "convdiff":
+        rp, ci, v = gen_convdiff_upwind(N, cfg["peclet"], cfg["v"])
+        norm2 = power_norm2(rp, ci, v, len(rp) - 1, False)
+    else:
+        raise ValueError(kind)
+    n = len(rp) - 1
+    b = gen_gaussian(B_SEED, n) if with_b else None
+    t = cfg["c"] / norm2 if cfg["fn"] == "exp_neg" else 1.0
+    tol = cfg["tol_rel"] * (float(np.linalg.norm(b)) if with_b else math.sqrt(n))
+    return Problem(name=name, n=n, nnz=int(rp[-1]), row_ptr=rp, col_idx=ci, values=v, b=b,
+                   fn=cfg["fn"], t=t, m=cfg["m"], d=cfg["d"], zeta=cfg["zeta"], tol=tol,
+                   k_max=BUDGET_TOTAL_M // cfg["m"], norm2=norm2)
+
+
+def algorithmic_bytes_per_cycle(n: int, nnz: int, m: int, rp_bytes: int = 4) -> int:
+    """B_cycle = sum_k B_step(k) + 8n + 16n + 8n(m+2).
+
+    B_step(k) = 12 nnz + rp (n+1) + 8n (x) + 8n (z write) + 8n (k+1) (W read)
+                + 8n (z read) + 8n (w_{k+1} write).
+    Sketch metadata excluded (regenerable from the seed).
+    """
+    total = 0
+    for k in range(m):
+        total += 12 * nnz + rp_bytes * (n + 1) + 8 * n * 4 + 8 * n * (k + 1)
+    total += 8 * n + 16 * n + 8 * n * (m + 2)
+    return total

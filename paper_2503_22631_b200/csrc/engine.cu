@@ -1,0 +1,913 @@
+// Host C++ engine and C ABI of rkmf_b200.
+//
+// rkmf_restarted_krylov restates restart::restarted_krylov
+// (proj/src/restart.cpp:27-122) with the randomized builder
+// (proj/src/basis.cpp:92-142) running as device kernels:
+//
+//   per cycle:  start_init (alpha_k, U[:,0])                          1 block
+//               m x [ spmv_sketch (K2) -> rgs_step (K3) -> basis_update (K4) ]
+//               dense f (K6: FULL exp(-tR)e1 or restart quadrature)
+//               final_update (K5: last basis update + y = alpha W g, f += y)
+//               spmv_sketch in sketch-only mode on the next start vector
+//
+// The host reads a few scalars back once (quadrature) or twice (FULL: the
+// squaring count needs ||R_accum||_1) per cycle; everything else stays on the
+// device. There is no CPU fallback: without a CUDA device every call fails
+// with RKMF_DEVICE_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "rkmf_internal.cuh"
+
+using namespace rkmf_b200;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* ensure(size_t bytes) {
+    if (bytes <= cap && p) return p;
+    if (p) RKMF_CUDA(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    RKMF_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    cap = std::max<size_t>(bytes, 256);
+    return p;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace
+
+struct rkmf_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int64_t launches = 0;
+  SolveState* st_dev = nullptr;
+  SolveState* st_host = nullptr;  // pinned
+  DevBuf z, pacc, sacc, W, U, Rbar, Racc, ws, u, g, fhat, ref, partial, qshift, qweight, qpi,
+      qemx, scratch;
+  int64_t racc_ld = 0;
+  std::vector<double> last_R;
+  int64_t last_M = 0;
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t event(size_t i) {
+    while (events.size() <= i) {
+      cudaEvent_t e;
+      RKMF_CUDA(cudaEventCreate(&e));
+      events.push_back(e);
+    }
+    return events[i];
+  }
+  void sync_state() {
+    RKMF_CUDA(cudaMemcpyAsync(st_host, st_dev, sizeof(SolveState), cudaMemcpyDeviceToHost, stream));
+    RKMF_CUDA(cudaStreamSynchronize(stream));
+  }
+  // ---- optional per-kernel-class timing (rkmf_context_kernel_timing) ----
+  bool ktime = false;
+  std::vector<cudaEvent_t> kpool;
+  std::vector<std::pair<int, size_t>> kpend;  // (class, index of the start event)
+  double kms[RKMF_KCLASS_COUNT] = {0};
+  int64_t kcnt[RKMF_KCLASS_COUNT] = {0};
+  template <class F>
+  void timed(int cls, F&& launch) {
+    if (!ktime) { launch(); return; }
+    const size_t i = 2 * kpend.size();
+    while (kpool.size() < i + 2) {
+      cudaEvent_t e;
+      RKMF_CUDA(cudaEventCreate(&e));
+      kpool.push_back(e);
+    }
+    RKMF_CUDA(cudaEventRecord(kpool[i], stream));
+    launch();
+    RKMF_CUDA(cudaEventRecord(kpool[i + 1], stream));
+    kpend.push_back({cls, i});
+  }
+  void collect_ktimes() {  // call after a stream synchronize
+    for (auto& p : kpend) {
+      float ms = 0.f;
+      RKMF_CUDA(cudaEventElapsedTime(&ms, kpool[p.second], kpool[p.second + 1]));
+      kms[p.first] += ms;
+      kcnt[p.first] += 1;
+    }
+    kpend.clear();
+  }
+};
+
+struct rkmf_matrix {
+  rkmf_context* ctx = nullptr;
+  CsrView view{};
+  void* rp = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+  double norm1 = 0.0;
+};
+
+struct rkmf_sketch {
+  rkmf_context* ctx = nullptr;
+  int64_t d = 0, n = 0, zeta = 0;
+  uint64_t seed = 0;
+  double scale = 1.0;
+  uint16_t* rows = nullptr;
+  int8_t* signs = nullptr;
+  uint16_t* tile_off = nullptr;
+  uint8_t* tile_ent = nullptr;
+  SketchView view() const {
+    SketchView v;
+    v.d = d;
+    v.n = n;
+    v.zeta = zeta;
+    v.tile_off = tile_off;
+    v.tile_ent = tile_ent;
+    v.scale = scale;
+    return v;
+  }
+};
+
+namespace {
+
+template <class F>
+int guarded(rkmf_context* ctx, F&& fn) {
+  try {
+    fn();
+    if (ctx) ctx->last_error.clear();
+    return RKMF_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return RKMF_INTERNAL_ERROR;
+  }
+}
+
+void set_device(rkmf_context* ctx) { RKMF_CUDA(cudaSetDevice(ctx->device)); }
+
+int choose_cap(const std::vector<int64_t>& tile_nnz_max) {
+  int64_t mx = 1;
+  for (int64_t v : tile_nnz_max) mx = std::max(mx, v);
+  return int(std::min<int64_t>(4096, round_up(std::max<int64_t>(mx, 128), 128)));
+}
+
+// ---- matrix construction helpers ----
+// Validates the CSR on device (sparse.cpp:61-81) and caches norm1
+// (sparse.cpp:97-102): once per matrix instead of every cycle (basis.cpp:15,118).
+void finish_matrix(rkmf_matrix* M, int64_t max_tile_nnz) {
+  rkmf_context* ctx = M->ctx;
+  M->view.cap = choose_cap({max_tile_nnz});
+  M->view.row_ptr = M->rp;
+  M->view.col = M->col;
+  M->view.val = M->val;
+  char* scr = static_cast<char*>(ctx->scratch.ensure(64));
+  int32_t* flags = reinterpret_cast<int32_t*>(scr);
+  double* out = reinterpret_cast<double*>(scr + 16);
+  DevBuf colsum;
+  colsum.ensure(sizeof(double) * size_t(M->view.n_cols + 1));
+  launch_matrix_check(&M->view, flags, ctx->stream);
+  launch_matrix_norm1(&M->view, colsum.as<double>(), out, ctx->stream);
+  ctx->launches += 3;
+  int32_t hf[2] = {0, 0};
+  RKMF_CUDA(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+  RKMF_CUDA(cudaMemcpyAsync(&M->norm1, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+  colsum.release();
+  if (hf[0]) shape_error("invalid CSR structure (sparse.cpp:61-81 invariants)");
+  if (hf[1]) numerical_error("non-finite matrix entry");
+}
+
+__global__ void rp_narrow_kernel(int64_t n, const int64_t* __restrict__ src, int32_t* dst) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = int32_t(src[i]);
+}
+
+__global__ void tile_nnz_max_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                    unsigned long long* out) {
+  const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < tiles;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r0 = t * kTileRows, r1 = min(n, r0 + kTileRows);
+    atomicMax(out, (unsigned long long)(rp[r1] - rp[r0]));
+  }
+}
+
+rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
+                                     int64_t nnz, const int64_t* rp64_dev,
+                                     const int32_t* col_dev, const double* val_dev,
+                                     bool copy_colval) {
+  auto* M = new rkmf_matrix();
+  M->ctx = ctx;
+  M->view.n_rows = n_rows;
+  M->view.n_cols = n_cols;
+  M->view.nnz = nnz;
+  try {
+    const bool rp64 = nnz >= (int64_t(1) << 31) - 1;
+    M->view.rp64 = rp64;
+    if (rp64) {
+      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int64_t) * size_t(n_rows + 1)));
+      RKMF_CUDA(cudaMemcpyAsync(M->rp, rp64_dev, sizeof(int64_t) * size_t(n_rows + 1),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int32_t) * size_t(n_rows + 1)));
+      rp_narrow_kernel<<<256, 256, 0, ctx->stream>>>(n_rows, rp64_dev,
+                                                     static_cast<int32_t*>(M->rp));
+      RKMF_CUDA(cudaGetLastError());
+      ctx->launches++;
+    }
+    if (!copy_colval) {
+      M->col = const_cast<int32_t*>(col_dev);
+      M->val = const_cast<double*>(val_dev);
+    } else {
+      RKMF_CUDA(cudaMalloc(&M->col, sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1))));
+      RKMF_CUDA(cudaMalloc(&M->val, sizeof(double) * size_t(std::max<int64_t>(nnz, 1))));
+      if (nnz > 0) {
+        RKMF_CUDA(cudaMemcpyAsync(M->col, col_dev, sizeof(int32_t) * size_t(nnz),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+        RKMF_CUDA(cudaMemcpyAsync(M->val, val_dev, sizeof(double) * size_t(nnz),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    }
+    unsigned long long* mx = reinterpret_cast<unsigned long long*>(ctx->scratch.ensure(64));
+    RKMF_CUDA(cudaMemsetAsync(mx, 0, 8, ctx->stream));
+    tile_nnz_max_kernel<<<256, 256, 0, ctx->stream>>>(n_rows, rp64_dev, mx);
+    RKMF_CUDA(cudaGetLastError());
+    ctx->launches++;
+    unsigned long long hmx = 0;
+    RKMF_CUDA(cudaMemcpyAsync(&hmx, mx, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    finish_matrix(M, int64_t(hmx));
+  } catch (...) {
+    if (M->rp) cudaFree(M->rp);
+    if (copy_colval && M->col) cudaFree(M->col);
+    if (copy_colval && M->val) cudaFree(M->val);
+    delete M;
+    throw;
+  }
+  return M;
+}
+
+double host_norm(const double* x, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += x[i] * x[i];
+  return std::sqrt(s);
+}
+
+struct SolveBuffers {
+  int64_t n, d, m_eff, ldw, ldr;
+  double *W, *U, *Rbar, *z, *pacc, *sacc;
+};
+
+SolveBuffers prepare(rkmf_context* ctx, int64_t n, int64_t d, int64_t m_eff) {
+  SolveBuffers b;
+  b.n = n;
+  b.d = d;
+  b.m_eff = m_eff;
+  b.ldw = round_up(std::max<int64_t>(n, 1), 32);
+  b.ldr = m_eff + 1;
+  b.W = static_cast<double*>(ctx->W.ensure(sizeof(double) * size_t(b.ldw) * size_t(m_eff + 1)));
+  b.U = static_cast<double*>(ctx->U.ensure(sizeof(double) * size_t(d) * size_t(m_eff + 1)));
+  b.Rbar = static_cast<double*>(ctx->Rbar.ensure(sizeof(double) * size_t(b.ldr) * size_t(m_eff)));
+  b.z = static_cast<double*>(ctx->z.ensure(sizeof(double) * size_t(b.ldw)));
+  b.pacc = static_cast<double*>(ctx->pacc.ensure(sizeof(double) * size_t(d)));
+  b.sacc = static_cast<double*>(ctx->sacc.ensure(sizeof(double) * size_t(d)));
+  RKMF_CUDA(cudaMemsetAsync(b.pacc, 0, sizeof(double) * size_t(d), ctx->stream));
+  RKMF_CUDA(cudaMemsetAsync(b.sacc, 0, sizeof(double) * size_t(d), ctx->stream));
+  RKMF_CUDA(cudaMemsetAsync(b.Rbar, 0, sizeof(double) * size_t(b.ldr) * size_t(m_eff), ctx->stream));
+  RKMF_CUDA(cudaMemsetAsync(ctx->st_dev, 0, sizeof(SolveState), ctx->stream));
+  return b;
+}
+
+void check_builder_args(const rkmf_matrix* A, const rkmf_sketch* S, int64_t m) {
+  // basis.cpp:14-23, 96-101
+  if (A->view.n_rows != A->view.n_cols) shape_error("arnoldi: matrix must be square");
+  if (m < 1) param_error("arnoldi: m must be >= 1");
+  if (m > A->view.n_rows) param_error("arnoldi: m exceeds matrix dimension");
+  if (S->n != A->view.n_rows) shape_error("randomized_arnoldi: sketch width mismatch");
+  const int64_t need = (m == A->view.n_rows) ? m : m + 1;
+  if (S->d < need) param_error("randomized_arnoldi: sketch dimension d too small for m");
+}
+
+// The m_eff steps of one cycle (basis.cpp:119-139). fuse_last: leave the
+// last basis update to final_update (K5).
+void run_steps(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
+               const SolveBuffers& b, double tol, bool fuse_last) {
+  const SketchView sv = S->view();
+  const int grid = spmv_sketch_grid(&A->view, &sv, 1);
+  int32_t* stop = &ctx->st_dev->stopped;
+  for (int64_t k = 0; k < b.m_eff; ++k) {
+    const double* x = b.W + k * b.ldw;
+    ctx->timed(0, [&] {
+      launch_spmv_sketch(&A->view, &sv, 1, x, k == 0 ? &ctx->st_dev->sigma : nullptr, b.z,
+                         b.pacc, stop, int(k), grid, ctx->stream);
+    });
+    ctx->timed(1, [&] {
+      launch_rgs_step(b.d, int(k), b.ldr, b.n, tol, b.pacc, b.U, b.Rbar, ctx->st_dev, ctx->stream);
+    });
+    ctx->launches += 2;
+    if (!(fuse_last && k == b.m_eff - 1)) {
+      ctx->timed(2, [&] {
+        launch_basis_update(b.n, int(k), b.ldw, b.W, b.z, b.Rbar, b.ldr, ctx->st_dev, ctx->stream);
+      });
+      ctx->launches++;
+    }
+  }
+}
+
+void start_sketch(rkmf_context* ctx, const rkmf_sketch* S, const SolveBuffers& b) {
+  const SketchView sv = S->view();
+  ctx->timed(5, [&] {
+    launch_spmv_sketch(nullptr, &sv, 2, b.W, nullptr, nullptr, b.sacc, nullptr, 0, 0,
+                       ctx->stream);
+  });
+  ctx->launches++;
+}
+
+void copy_in(rkmf_context* ctx, double* dst, const double* src, int64_t n, bool on_device) {
+  if (n <= 0) return;
+  RKMF_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * size_t(n),
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            ctx->stream));
+}
+
+}  // namespace
+
+// ============================== C ABI ==============================
+extern "C" {
+
+int rkmf_context_create(int device, rkmf_context** out) {
+  return guarded(nullptr, [&] {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      throw Error(RKMF_DEVICE_ERROR, "rkmf_b200: no CUDA device available (no CPU fallback)");
+    if (device < 0 || device >= count) param_error("rkmf_b200: invalid device index");
+    auto* ctx = new rkmf_context();
+    ctx->device = device;
+    try {
+      RKMF_CUDA(cudaSetDevice(device));
+      RKMF_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+      ctx->stream = ctx->own_stream;
+      RKMF_CUDA(cudaMalloc(&ctx->st_dev, sizeof(SolveState)));
+      RKMF_CUDA(cudaMallocHost(&ctx->st_host, sizeof(SolveState)));
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+int rkmf_context_destroy(rkmf_context* ctx) {
+  if (!ctx) return RKMF_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->z, &ctx->pacc, &ctx->sacc, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
+                    &ctx->ws, &ctx->u, &ctx->g, &ctx->fhat, &ctx->ref, &ctx->partial,
+                    &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch})
+    b->release();
+  for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+  if (ctx->st_dev) cudaFree(ctx->st_dev);
+  if (ctx->st_host) cudaFreeHost(ctx->st_host);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return RKMF_OK;
+}
+
+const char* rkmf_last_error(const rkmf_context* ctx) {
+  return ctx ? ctx->last_error.c_str() : "rkmf_b200: null context";
+}
+
+int rkmf_context_set_stream(rkmf_context* ctx, void* s) {
+  return guarded(ctx, [&] {
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  });
+}
+
+int64_t rkmf_context_launch_count(const rkmf_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int rkmf_context_kernel_timing(rkmf_context* ctx, int enable) {
+  return guarded(ctx, [&] {
+    ctx->ktime = enable != 0;
+    ctx->kpend.clear();
+  });
+}
+
+int rkmf_context_kernel_times(rkmf_context* ctx, double* ms, int64_t* launches, int reset) {
+  return guarded(ctx, [&] {
+    for (int c = 0; c < RKMF_KCLASS_COUNT; ++c) {
+      if (ms) ms[c] = ctx->kms[c];
+      if (launches) launches[c] = ctx->kcnt[c];
+      if (reset) {
+        ctx->kms[c] = 0.0;
+        ctx->kcnt[c] = 0;
+      }
+    }
+  });
+}
+
+void rkmf_restart_options_default(rkmf_restart_options* o) {  // restart.hpp:20-26
+  o->m_r = 20;
+  o->tol = 1e-10;
+  o->k_max = 100;
+  o->budget_total_m = 4000;
+  o->divergence_factor = 1e6;
+  o->dense_f = RKMF_DENSE_AUTO;
+  o->quad_nodes = 0;
+}
+
+int rkmf_matrix_create_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
+                            const int64_t* h_rp, const int32_t* h_ci, const double* h_v,
+                            rkmf_matrix** out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (n_rows < 0 || n_cols < 0) shape_error("negative dimension");
+    if (h_rp[0] != 0) shape_error("row_ptr[0] != 0");
+    const int64_t nnz = h_rp[n_rows];
+    int64_t* rp_dev = nullptr;
+    int32_t* col = nullptr;
+    double* val = nullptr;
+    RKMF_CUDA(cudaMalloc(&rp_dev, sizeof(int64_t) * size_t(n_rows + 1)));
+    RKMF_CUDA(cudaMalloc(&col, sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1))));
+    RKMF_CUDA(cudaMalloc(&val, sizeof(double) * size_t(std::max<int64_t>(nnz, 1))));
+    RKMF_CUDA(cudaMemcpyAsync(rp_dev, h_rp, sizeof(int64_t) * size_t(n_rows + 1),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    if (nnz > 0) {
+      RKMF_CUDA(cudaMemcpyAsync(col, h_ci, sizeof(int32_t) * size_t(nnz), cudaMemcpyHostToDevice,
+                                ctx->stream));
+      RKMF_CUDA(cudaMemcpyAsync(val, h_v, sizeof(double) * size_t(nnz), cudaMemcpyHostToDevice,
+                                ctx->stream));
+    }
+    rkmf_matrix* M = nullptr;
+    try {
+      M = create_from_device_rp64(ctx, n_rows, n_cols, nnz, rp_dev, col, val, false);
+    } catch (...) {
+      cudaFree(rp_dev);
+      cudaFree(col);
+      cudaFree(val);
+      throw;
+    }
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    RKMF_CUDA(cudaFree(rp_dev));
+    *out = M;
+  });
+}
+
+int rkmf_matrix_create_device(rkmf_context* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                              const int64_t* d_rp, const int32_t* d_ci, const double* d_v,
+                              rkmf_matrix** out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (n_rows < 0 || n_cols < 0) shape_error("negative dimension");
+    *out = create_from_device_rp64(ctx, n_rows, n_cols, nnz, d_rp, d_ci, d_v, true);
+  });
+}
+
+int rkmf_matrix_destroy(rkmf_matrix* M) {
+  if (!M) return RKMF_OK;
+  cudaSetDevice(M->ctx->device);
+  cudaStreamSynchronize(M->ctx->stream);
+  if (M->rp) cudaFree(M->rp);
+  if (M->col) cudaFree(M->col);
+  if (M->val) cudaFree(M->val);
+  delete M;
+  return RKMF_OK;
+}
+
+int rkmf_matrix_info(const rkmf_matrix* M, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
+                     double* norm1) {
+  if (!M) return RKMF_PARAMETER_ERROR;
+  if (n_rows) *n_rows = M->view.n_rows;
+  if (n_cols) *n_cols = M->view.n_cols;
+  if (nnz) *nnz = M->view.nnz;
+  if (norm1) *norm1 = M->norm1;
+  return RKMF_OK;
+}
+
+int rkmf_sketch_create(rkmf_context* ctx, int64_t d, int64_t n, int64_t zeta, uint64_t seed,
+                       rkmf_sketch** out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (zeta < 1) param_error("sketch: zeta must be >= 1");  // sketch.cpp:14-16
+    if (zeta > d) param_error("sketch: zeta must not exceed d");
+    if (d > n) param_error("sketch: d must not exceed n");
+    auto* S = new rkmf_sketch();
+    S->ctx = ctx;
+    S->d = d;
+    S->n = n;
+    S->zeta = zeta;
+    S->seed = seed;
+    S->scale = 1.0 / std::sqrt(double(zeta));  // sketch.cpp:23
+    try {
+      const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+      const int64_t off_stride = (d + 1 + 7) / 8 * 8;
+      RKMF_CUDA(cudaMalloc(&S->rows, sizeof(uint16_t) * size_t(std::max<int64_t>(n * zeta, 1))));
+      RKMF_CUDA(cudaMalloc(&S->signs, size_t(std::max<int64_t>(n * zeta, 1))));
+      RKMF_CUDA(cudaMalloc(&S->tile_off, sizeof(uint16_t) * size_t(std::max<int64_t>(tiles * off_stride, 1))));
+      RKMF_CUDA(cudaMalloc(&S->tile_ent, size_t(std::max<int64_t>(tiles * kTileRows * zeta, 16))));
+      launch_sketch_generate(d, n, zeta, seed, S->rows, S->signs, ctx->stream);
+      launch_sketch_tiles(d, n, zeta, S->rows, S->signs, S->tile_off, S->tile_ent, ctx->stream);
+      ctx->launches += 2;
+      RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      if (S->rows) cudaFree(S->rows);
+      if (S->signs) cudaFree(S->signs);
+      if (S->tile_off) cudaFree(S->tile_off);
+      if (S->tile_ent) cudaFree(S->tile_ent);
+      delete S;
+      throw;
+    }
+    *out = S;
+  });
+}
+
+int rkmf_sketch_destroy(rkmf_sketch* S) {
+  if (!S) return RKMF_OK;
+  cudaSetDevice(S->ctx->device);
+  cudaStreamSynchronize(S->ctx->stream);
+  cudaFree(S->rows);
+  cudaFree(S->signs);
+  cudaFree(S->tile_off);
+  cudaFree(S->tile_ent);
+  delete S;
+  return RKMF_OK;
+}
+
+int rkmf_sketch_set_scale(rkmf_sketch* S, double scale) {
+  if (!S) return RKMF_PARAMETER_ERROR;
+  S->scale = scale;
+  return RKMF_OK;
+}
+
+int rkmf_sketch_export(rkmf_context* ctx, const rkmf_sketch* S, int64_t* h_rows, int8_t* h_signs,
+                       double* h_scale) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    const int64_t cnt = S->n * S->zeta;
+    if (h_rows && cnt > 0) {
+      DevBuf tmp;
+      tmp.ensure(sizeof(int64_t) * size_t(cnt));
+      launch_sketch_export(cnt, S->rows, S->signs, tmp.as<int64_t>(), ctx->stream);
+      ctx->launches++;
+      RKMF_CUDA(cudaMemcpyAsync(h_rows, tmp.p, sizeof(int64_t) * size_t(cnt),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+      tmp.release();
+    }
+    if (h_signs && cnt > 0) {
+      RKMF_CUDA(cudaMemcpyAsync(h_signs, S->signs, size_t(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+      RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    if (h_scale) *h_scale = S->scale;
+  });
+}
+
+int rkmf_spmv(rkmf_context* ctx, const rkmf_matrix* A, const double* d_x, double* d_y) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    launch_spmv_sketch(&A->view, nullptr, 0, d_x, nullptr, d_y, nullptr, nullptr, 0, 0,
+                       ctx->stream);
+    ctx->launches++;
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int rkmf_sketch_apply(rkmf_context* ctx, const rkmf_sketch* S, const double* d_x, double* d_y) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    const SketchView sv = S->view();
+    RKMF_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * size_t(S->d), ctx->stream));
+    launch_spmv_sketch(nullptr, &sv, 2, d_x, nullptr, nullptr, d_y, nullptr, 0, 0, ctx->stream);
+    ctx->launches++;
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int rkmf_spmv_sketch(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
+                     const double* d_x, double* d_z, double* d_p) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (S->n != A->view.n_rows) shape_error("spmv_sketch: sketch width mismatch");
+    const SketchView sv = S->view();
+    RKMF_CUDA(cudaMemsetAsync(d_p, 0, sizeof(double) * size_t(S->d), ctx->stream));
+    launch_spmv_sketch(&A->view, &sv, 1, d_x, nullptr, d_z, d_p, nullptr, 0, 0, ctx->stream);
+    ctx->launches++;
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int rkmf_randomized_arnoldi(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
+                            const double* d_b, int64_t m, double* d_W, int64_t ldw, double* d_U,
+                            double* h_Rbar, double* start_norm, int64_t* mk,
+                            int64_t* breakdown_at, int64_t* counters) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    check_builder_args(A, S, m);
+    const int64_t n = A->view.n_rows;
+    if (ldw < n) param_error("randomized_arnoldi: ldw < n");
+    SolveBuffers b = prepare(ctx, n, S->d, m);
+    copy_in(ctx, b.W, d_b, n, true);
+    start_sketch(ctx, S, b);
+    launch_start_init_m(b.d, b.sacc, b.U, ctx->st_dev, true, int(m), ctx->stream);
+    ctx->launches++;
+    ctx->sync_state();
+    if (ctx->st_host->zero_start)  // basis.cpp:105-106
+      param_error("randomized_arnoldi: zero start vector after sketching");
+    run_steps(ctx, A, S, b, 1e-14 * A->norm1, false);
+    launch_scale_copy(n, b.W, b.W, ctx->st_dev, ctx->stream);  // W[:,0] = b / alpha
+    ctx->launches++;
+    ctx->sync_state();
+    const SolveState& h = *ctx->st_host;
+    const int64_t kept = h.stopped;
+    const bool next = h.breakdown == 0;
+    const int64_t cols = next ? m + 1 : kept;
+    RKMF_CUDA(cudaMemcpy2DAsync(d_W, sizeof(double) * size_t(ldw), b.W, sizeof(double) * size_t(b.ldw),
+                                sizeof(double) * size_t(n), size_t(cols), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    RKMF_CUDA(cudaMemcpyAsync(d_U, b.U, sizeof(double) * size_t(S->d) * size_t(cols),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    RKMF_CUDA(cudaMemcpyAsync(h_Rbar, b.Rbar, sizeof(double) * size_t(b.ldr) * size_t(m),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    *start_norm = h.alpha_k;
+    *mk = kept;
+    *breakdown_at = h.breakdown;
+    if (counters) {  // types.hpp:57-75, cost formulas of test_basis.cpp:230-254
+      counters[0] = kept;
+      counters[1] = 0;
+      counters[2] = kept * (kept + 1) / 2;
+      counters[3] = next ? m : kept - 1;
+      counters[4] = next ? m + 1 : kept;
+    }
+  });
+}
+
+int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
+                          const double* b_in, int b_on_device, int32_t fn_kind, double fn_t,
+                          const rkmf_restart_options* opts_in, double* f_out, int f_on_device,
+                          const double* reference, rkmf_restart_result* res,
+                          rkmf_cycle_record* records, int64_t records_cap) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    rkmf_restart_options opts;
+    if (opts_in) opts = *opts_in;
+    else rkmf_restart_options_default(&opts);
+    // restart.cpp:33-37
+    if (opts.m_r < 1) param_error("restart: m_r must be >= 1");
+    if (opts.k_max < 1) param_error("restart: k_max must be >= 1");
+    if (!(opts.tol > 0.0)) param_error("restart: tol must be > 0");
+    if (opts.budget_total_m < opts.m_r) param_error("restart: total-m budget below one cycle");
+    if (fn_kind != RKMF_FN_EXP_NEG && fn_kind != RKMF_FN_INV_SQRT)
+      param_error("funm: unknown FunctionSpec kind");
+    if (fn_kind == RKMF_FN_EXP_NEG && !(fn_t >= 0.0)) param_error("FunctionSpec: t must be >= 0");
+    if (!S) param_error("rkmf_b200: the classical builder (S == nullptr) is not on the device path");
+    int dense = opts.dense_f;
+    if (dense == RKMF_DENSE_AUTO) dense = fn_kind == RKMF_FN_EXP_NEG ? RKMF_DENSE_FULL : RKMF_DENSE_QUADRATURE;
+    if (dense == RKMF_DENSE_FULL && fn_kind != RKMF_FN_EXP_NEG)
+      param_error("rkmf_b200: FULL dense f is implemented for exp_neg only");
+    if (dense == RKMF_DENSE_QUADRATURE && fn_kind != RKMF_FN_INV_SQRT)
+      param_error("rkmf_b200: quadrature restart is implemented for inv_sqrt only");
+    const int64_t n = A->view.n_rows;
+    const int64_t m_eff = std::min(opts.m_r, n);  // restart.cpp:38
+    check_builder_args(A, S, m_eff);
+    std::memset(res, 0, sizeof(*res));
+    ctx->kpend.clear();
+
+    cudaStream_t st = ctx->stream;
+    SolveBuffers bb = prepare(ctx, n, S->d, m_eff);
+    double* g = static_cast<double*>(ctx->g.ensure(sizeof(double) * size_t(m_eff)));
+    double* fhat = f_on_device ? f_out : static_cast<double*>(ctx->fhat.ensure(sizeof(double) * size_t(std::max<int64_t>(n, 1))));
+    RKMF_CUDA(cudaMemsetAsync(fhat, 0, sizeof(double) * size_t(n), st));
+    const double* ref_dev = nullptr;
+    double ref_norm = 0.0;
+    if (reference) {
+      std::vector<double> hr;
+      if (b_on_device) {
+        hr.resize(size_t(n));
+        RKMF_CUDA(cudaMemcpyAsync(hr.data(), reference, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+        ref_dev = reference;
+        ref_norm = host_norm(hr.data(), n);
+      } else {
+        double* rd = static_cast<double*>(ctx->ref.ensure(sizeof(double) * size_t(n)));
+        copy_in(ctx, rd, reference, n, false);
+        ref_dev = rd;
+        ref_norm = host_norm(reference, n);
+      }
+    }
+    copy_in(ctx, bb.W, b_in, n, b_on_device != 0);  // start = b (restart.cpp:45)
+
+    // dense-f state
+    const int64_t Ncap = std::min<int64_t>(opts.budget_total_m, opts.k_max * m_eff);
+    int64_t ldR = 0;
+    double* Racc = nullptr;
+    auto ensure_racc = [&](int64_t N) {
+      if (N <= ldR) return;
+      int64_t newld = std::min<int64_t>(Ncap, std::max<int64_t>(N, 2 * ldR));
+      newld = std::max(newld, N);
+      DevBuf nb;
+      nb.ensure(sizeof(double) * size_t(newld) * size_t(newld));
+      RKMF_CUDA(cudaMemsetAsync(nb.p, 0, sizeof(double) * size_t(newld) * size_t(newld), st));
+      if (ldR > 0)
+        RKMF_CUDA(cudaMemcpy2DAsync(nb.p, sizeof(double) * size_t(newld), Racc,
+                                    sizeof(double) * size_t(ldR), sizeof(double) * size_t(ldR),
+                                    size_t(ldR), cudaMemcpyDeviceToDevice, st));
+      RKMF_CUDA(cudaStreamSynchronize(st));
+      ctx->Racc.release();
+      ctx->Racc = nb;
+      nb.p = nullptr;
+      Racc = ctx->Racc.as<double>();
+      ldR = newld;
+    };
+    QuadState q{};
+    double* partial = nullptr;
+    if (dense == RKMF_DENSE_QUADRATURE) {
+      q.nq = opts.quad_nodes > 0 ? opts.quad_nodes : 512;
+      q.shift = static_cast<double*>(ctx->qshift.ensure(sizeof(double) * size_t(q.nq)));
+      q.weight = static_cast<double*>(ctx->qweight.ensure(sizeof(double) * size_t(q.nq)));
+      q.pi = static_cast<double*>(ctx->qpi.ensure(sizeof(double) * size_t(q.nq)));
+      q.emx = static_cast<double*>(ctx->qemx.ensure(sizeof(double) * size_t(q.nq)));
+      partial = static_cast<double*>(ctx->partial.ensure(sizeof(double) * size_t(q.nq) * size_t(m_eff)));
+      // trapezoid nodes u in [0.5 ln(||A|| * 1e-14) - 37, 0.5 ln(||A||) + 37]
+      const double an = std::max(A->norm1, 1e-300);
+      const double u0 = 0.5 * std::log(an * 1e-14) - 37.0, u1 = 0.5 * std::log(an) + 37.0;
+      const double h = (u1 - u0) / double(q.nq);
+      std::vector<double> hs(size_t(q.nq)), hw(size_t(q.nq)), ones(size_t(q.nq), 1.0);
+      for (int i = 0; i < q.nq; ++i) {
+        const double u = u0 + (double(i) + 0.5) * h;
+        hs[size_t(i)] = std::exp(2.0 * u);
+        hw[size_t(i)] = (2.0 / M_PI) * h * std::exp(u);
+      }
+      RKMF_CUDA(cudaMemcpyAsync(q.shift, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice, st));
+      RKMF_CUDA(cudaMemcpyAsync(q.weight, hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice, st));
+      RKMF_CUDA(cudaMemcpyAsync(q.pi, ones.data(), sizeof(double) * ones.size(), cudaMemcpyHostToDevice, st));
+      RKMF_CUDA(cudaStreamSynchronize(st));
+    }
+
+    const double tol_break = 1e-14 * A->norm1;  // basis.cpp:118
+    int64_t M = 0;
+    double first_update = -1.0;
+    long long matvecs = 0, dot_d = 0, updates = 0, peak = 0;
+    RKMF_CUDA(cudaEventRecord(ctx->event(0), st));
+    start_sketch(ctx, S, bb);
+    struct CycleEv { size_t e0, e1, e2, e3; };
+    size_t next_ev = 1;
+    std::vector<CycleEv> evs;
+    std::vector<rkmf_cycle_record> recs;
+    for (int64_t k = 1; k <= opts.k_max; ++k) {
+      if (M + m_eff > opts.budget_total_m) break;  // restart.cpp:50
+      const size_t base = next_ev;
+      next_ev += 4;
+      CycleEv ce{base, base + 1, base + 2, base + 3};
+      RKMF_CUDA(cudaEventRecord(ctx->event(ce.e0), st));
+      ctx->timed(5, [&] {
+        launch_start_init_m(bb.d, bb.sacc, bb.U, ctx->st_dev, k == 1, int(m_eff), st);
+      });
+      ctx->launches++;
+      if (k == 1) {
+        ctx->sync_state();
+        if (ctx->st_host->zero_start)
+          param_error("randomized_arnoldi: zero start vector after sketching");
+      }
+      run_steps(ctx, A, S, bb, tol_break, true);
+      RKMF_CUDA(cudaEventRecord(ctx->event(ce.e1), st));
+      // ---- dense f ----
+      if (dense == RKMF_DENSE_FULL) {
+        const int64_t N = M + m_eff;
+        ensure_racc(N);
+        ctx->timed(3, [&] {
+          launch_raccum_append(Racc, ldR, M, bb.Rbar, bb.ldr, ctx->st_dev, st);
+          launch_dense_norm1(Racc, ldR, N, &ctx->st_dev->rnorm1, st);
+        });
+        ctx->launches += 2;
+        ctx->sync_state();
+        const double xn = std::fabs(fn_t) * ctx->st_host->rnorm1;
+        int s = 0;
+        if (xn > 1.0) s = std::min(64, int(std::ceil(std::log2(xn))));
+        double* ws = static_cast<double*>(ctx->ws.ensure(sizeof(double) * 6 * size_t(N) * size_t(N)));
+        double* u = static_cast<double*>(ctx->u.ensure(sizeof(double) * size_t(N)));
+        int64_t nl = 0;
+        ctx->timed(3, [&] {
+          dense_expneg_e1(Racc, ldR, N, fn_t, s, ws, u, st, &nl);
+          launch_make_g(u, M, int(m_eff), g, ctx->st_dev, st);
+        });
+        ctx->launches += nl + 2;
+      } else {
+        ctx->timed(3, [&] {
+          if (M + m_eff <= Ncap) {  // keep R_accum for rkmf_last_r_accum
+            ensure_racc(M + m_eff);
+            launch_raccum_append(Racc, ldR, M, bb.Rbar, bb.ldr, ctx->st_dev, st);
+            ctx->launches++;
+          }
+          launch_quad_invsqrt_cycle(bb.Rbar, bb.ldr, int(m_eff), k, &q, g, ctx->st_dev, partial,
+                                    st);
+        });
+        ctx->launches += 2;
+      }
+      RKMF_CUDA(cudaEventRecord(ctx->event(ce.e2), st));
+      ctx->timed(4, [&] {
+        launch_final_update(n, int(m_eff), bb.ldw, bb.W, bb.z, bb.Rbar, bb.ldr, g, fhat, ref_dev,
+                            ctx->st_dev, st);
+      });
+      ctx->launches++;
+      RKMF_CUDA(cudaEventRecord(ctx->event(ce.e3), st));
+      ctx->sync_state();
+      const SolveState& h = *ctx->st_host;
+      const int64_t mk = h.stopped;
+      const bool next = h.breakdown == 0;
+      if (k == 1) res->alpha = h.alpha1;
+      matvecs += mk;
+      dot_d += mk * (mk + 1) / 2;
+      updates += next ? m_eff : mk - 1;
+      peak = std::max<long long>(peak, next ? m_eff + 1 : mk);
+      if (h.nonfinite) numerical_error("restart divergence (cycle " + std::to_string(k) + ")");
+      const double yn = std::sqrt(h.yn2);
+      rkmf_cycle_record rec;
+      rec.cycle = k;
+      rec.total_m = M + mk;
+      rec.total_matvecs = matvecs;
+      rec.update_norm = yn;
+      rec.error_vs_reference = (reference && ref_norm > 0.0) ? std::sqrt(h.err2) / ref_norm
+                                                             : std::numeric_limits<double>::quiet_NaN();
+      rec.kappa_W = std::numeric_limits<double>::quiet_NaN();
+      rec.leftmost_ritz_re = std::numeric_limits<double>::quiet_NaN();
+      rec.alpha_dev = k == 1 ? 0.0 : std::fabs(h.alpha_k - 1.0);
+      rec.start_norm = h.alpha_k;
+      rec.subdiag = h.coupling;
+      rec.elapsed_ms = rec.build_ms = rec.funm_ms = 0.0;
+      recs.push_back(rec);
+      evs.push_back(ce);
+      if (first_update < 0.0) first_update = yn;
+      else if (yn > opts.divergence_factor * first_update)
+        numerical_error("restart divergence (cycle " + std::to_string(k) + ")");
+      M += mk;
+      res->cycles = k;
+      res->total_m = M;
+      if (yn <= opts.tol || !next) {  // restart.cpp:113-116
+        res->converged = 1;
+        break;
+      }
+      start_sketch(ctx, S, bb);  // next cycle's S * start
+    }
+    const size_t e_end = next_ev;
+    RKMF_CUDA(cudaEventRecord(ctx->event(e_end), st));
+    if (!f_on_device)
+      RKMF_CUDA(cudaMemcpyAsync(f_out, fhat, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, st));
+    RKMF_CUDA(cudaStreamSynchronize(st));
+    ctx->collect_ktimes();
+    float ms = 0.f;
+    RKMF_CUDA(cudaEventElapsedTime(&ms, ctx->event(0), ctx->event(e_end)));
+    res->solve_ms = ms;
+    for (size_t i = 0; i < recs.size(); ++i) {
+      float a = 0.f, b2 = 0.f, c = 0.f;
+      RKMF_CUDA(cudaEventElapsedTime(&a, ctx->event(evs[i].e0), ctx->event(evs[i].e3)));
+      RKMF_CUDA(cudaEventElapsedTime(&b2, ctx->event(evs[i].e0), ctx->event(evs[i].e1)));
+      RKMF_CUDA(cudaEventElapsedTime(&c, ctx->event(evs[i].e1), ctx->event(evs[i].e2)));
+      recs[i].elapsed_ms = a;
+      recs[i].build_ms = b2;
+      recs[i].funm_ms = c;
+    }
+    res->matvecs = matvecs;
+    res->dot_n = 0;
+    res->dot_d = dot_d;
+    res->basis_updates = updates;
+    res->peak_basis_cols = peak;
+    res->n_records = int64_t(recs.size());
+    if (records)
+      for (int64_t i = 0; i < std::min<int64_t>(records_cap, res->n_records); ++i) records[i] = recs[size_t(i)];
+    ctx->racc_ld = ldR;
+    ctx->last_M = (ldR >= M) ? M : 0;
+  });
+}
+
+int rkmf_last_r_accum(rkmf_context* ctx, double* h_R, int64_t n_cap, int64_t* total_m) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    const int64_t M = ctx->last_M;
+    *total_m = M;
+    if (!h_R || M == 0) return;
+    if (n_cap < M) param_error("rkmf_last_r_accum: capacity too small");
+    RKMF_CUDA(cudaMemcpy2DAsync(h_R, sizeof(double) * size_t(M), ctx->Racc.p,
+                                sizeof(double) * size_t(ctx->racc_ld), sizeof(double) * size_t(M),
+                                size_t(M), cudaMemcpyDeviceToHost, ctx->stream));
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+// K3 (sketched Gram-Schmidt), K4 (basis update), K5 (fused restart update)
+// and the start normalisation of each cycle.
+//
+// Column 0 of the basis holds the UNscaled start vector s of the cycle; the
+// scale sigma = 1/alpha_k (alpha_k = ||S s||, basis.cpp:103-104) is folded into
+// the step-0 SpMV and into every coefficient that multiplies column 0, so the
+// reference's W[:,0] = b/alpha pass (basis.cpp:114) and the next cycle's
+// start copy (restart.cpp:118) never touch HBM.
+#include <cuda_runtime.h>
+
+#include "rkmf_internal.cuh"
+
+namespace rkmf_b200 {
+
+namespace {
+
+constexpr int kRgsThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum with a fixed reduction order (bitwise reproducible); every
+// thread returns the total. `buf` holds one slot per warp.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* buf) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) buf[w] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < NT / 32; ++q) s += buf[q];
+  __syncthreads();
+  return s;
+}
+
+// basis.cpp:103-115 on device: alpha = ||S s||, U[:,0] = S s / alpha.
+__global__ void __launch_bounds__(kRgsThreads)
+    start_init_kernel(int64_t d, double* sacc, double* U, SolveState* st, int first, int m_eff) {
+  __shared__ double buf[kRgsThreads / 32];
+  double ss = 0.0;
+  for (int64_t b = threadIdx.x; b < d; b += kRgsThreads) ss += sacc[b] * sacc[b];
+  const double alpha = sqrt(block_sum<kRgsThreads>(ss, buf));
+  for (int64_t b = threadIdx.x; b < d; b += kRgsThreads) {
+    U[b] = sacc[b] / alpha;
+    sacc[b] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    st->alpha_k = alpha;
+    st->sigma = 1.0 / alpha;
+    if (first) st->alpha1 = alpha;
+    st->zero_start = alpha == 0.0;
+    st->stopped = m_eff;
+    st->breakdown = 0;
+    st->nonfinite = 0;
+    st->yn2 = 0.0;
+    st->err2 = 0.0;
+  }
+}
+
+// One modified Gram-Schmidt sweep in the sketch space (basis.cpp:123-138):
+// r_i = <u_i, p>, p -= r_i u_i for i = 0..k, r_kk = ||p||, breakdown test,
+// U[:,k+1] = p / r_kk. The sketch p arrives as the reduced partials in pacc,
+// which this kernel re-zeroes for the next step. One __syncthreads per MGS
+// iteration (ping-pong reduction slots); the next column of U is prefetched.
+template <int PT>
+__global__ void __launch_bounds__(kRgsThreads)
+    rgs_step_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
+                    double* U, double* Rbar, SolveState* st) {
+  if (st->stopped <= k) return;
+  __shared__ double red[2][kRgsThreads / 32];
+  __shared__ double rs[1024];
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  double p[PT], u[PT], un[PT];
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    const int64_t b = t + int64_t(j) * kRgsThreads;
+    p[j] = b < d ? pacc[b] : 0.0;
+    if (b < d) pacc[b] = 0.0;
+    un[j] = b < d ? U[b] : 0.0;
+  }
+  for (int i = 0; i <= k; ++i) {
+    double part = 0.0;
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+      u[j] = un[j];
+      part += u[j] * p[j];
+    }
+    if (i < k) {
+#pragma unroll
+      for (int j = 0; j < PT; ++j) {
+        const int64_t b = t + int64_t(j) * kRgsThreads;
+        un[j] = b < d ? U[int64_t(i + 1) * d + b] : 0.0;
+      }
+    }
+    part = warp_sum(part);
+    if (l == 0) red[i & 1][w] = part;
+    __syncthreads();
+    double r = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRgsThreads / 32; ++q) r += red[i & 1][q];
+#pragma unroll
+    for (int j = 0; j < PT; ++j) p[j] -= r * u[j];
+    if (t == 0) rs[i] = r;
+  }
+  double ss = 0.0;
+#pragma unroll
+  for (int j = 0; j < PT; ++j) ss += p[j] * p[j];
+  ss = warp_sum(ss);
+  if (l == 0) red[(k + 1) & 1][w] = ss;
+  __syncthreads();
+  double tot = 0.0;
+#pragma unroll
+  for (int q = 0; q < kRgsThreads / 32; ++q) tot += red[(k + 1) & 1][q];
+  const double rkk = sqrt(tot);
+  for (int i = t; i <= k; i += kRgsThreads) Rbar[int64_t(k) * ldr + i] = rs[i];
+  if (rkk <= tol || int64_t(k) + 1 == n) {  // basis.cpp:131-134
+    if (t == 0) {
+      st->stopped = k + 1;
+      st->breakdown = k + 1;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    const int64_t b = t + int64_t(j) * kRgsThreads;
+    if (b < d) U[int64_t(k + 1) * d + b] = p[j] / rkk;
+  }
+  if (t == 0) Rbar[int64_t(k) * ldr + k + 1] = rkk;
+}
+
+constexpr int kUpdThreads = 256;
+constexpr int kMaxCoef = 1024;
+
+// W[:,k+1] = (z - W[:,0..k] r) / r_kk   (basis.cpp:135). Two rows per thread
+// with 16-byte loads; the k+1 column streams are issued 4 at a time.
+__global__ void __launch_bounds__(kUpdThreads)
+    basis_update_kernel(int64_t n, int k, int64_t ldw, double* W, const double* __restrict__ z,
+                        const double* __restrict__ Rbar, int64_t ldr, const SolveState* st) {
+  if (st->stopped <= k) return;  // no update at (or after) a breakdown step
+  __shared__ double coef[kMaxCoef];
+  for (int c = threadIdx.x; c <= k; c += kUpdThreads)
+    coef[c] = Rbar[int64_t(k) * ldr + c] * (c == 0 ? st->sigma : 1.0);
+  __syncthreads();
+  const double rkk = Rbar[int64_t(k) * ldr + k + 1];
+  double* out = W + int64_t(k + 1) * ldw;
+  const int64_t n2 = n / 2;
+  for (int64_t i2 = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x; i2 < n2;
+       i2 += int64_t(gridDim.x) * kUpdThreads) {
+    double a0 = 0.0, a1 = 0.0;
+    int c = 0;
+    for (; c + 3 <= k; c += 4) {
+      double2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const double2*>(W + int64_t(c + q) * ldw) + i2);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a0 += v[q].x * coef[c + q];
+        a1 += v[q].y * coef[c + q];
+      }
+    }
+    for (; c <= k; ++c) {
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(W + int64_t(c) * ldw) + i2);
+      a0 += v.x * coef[c];
+      a1 += v.y * coef[c];
+    }
+    const double2 zz = __ldcs(reinterpret_cast<const double2*>(z) + i2);
+    double2 o;
+    o.x = (zz.x - a0) / rkk;
+    o.y = (zz.y - a1) / rkk;
+    reinterpret_cast<double2*>(out)[i2] = o;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t i = n - 1;
+    double a = 0.0;
+    for (int c = 0; c <= k; ++c) a += W[int64_t(c) * ldw + i] * coef[c];
+    out[i] = (z[i] - a) / rkk;
+  }
+}
+
+// K5: the last basis update of the cycle fused with the restart update
+// (restart.cpp:80-85): one pass over W[:,0..m-1] and z computes
+//   y = alpha_1 * W[:,0..mk-1] g,   f_hat += y,   ||y||^2, finiteness,
+//   w_m = (z - W[:,0..m-1] r)/r_kk  written in place into column 0 (the next
+//   cycle's unscaled start vector, restart.cpp:118),
+// and, with a reference vector, ||f_hat - ref||^2 for error_vs_reference.
+__global__ void __launch_bounds__(kUpdThreads)
+    final_update_kernel(int64_t n, int m_eff, int64_t ldw, double* W,
+                        const double* __restrict__ z, const double* __restrict__ Rbar,
+                        int64_t ldr, const double* __restrict__ g, double* f_hat,
+                        const double* __restrict__ ref, SolveState* st) {
+  __shared__ double cg[kMaxCoef], cr[kMaxCoef];
+  __shared__ double buf[kUpdThreads / 32], buf2[kUpdThreads / 32];
+  const int mk = st->stopped;
+  const bool next = st->breakdown == 0;
+  const double sigma = st->sigma, alpha1 = st->alpha1;
+  const int km = m_eff - 1;
+  for (int c = threadIdx.x; c < m_eff; c += kUpdThreads) {
+    cg[c] = c < mk ? g[c] : 0.0;
+    cr[c] = next ? Rbar[int64_t(km) * ldr + c] * (c == 0 ? sigma : 1.0) : 0.0;
+  }
+  __syncthreads();
+  const double rkk = next ? Rbar[int64_t(km) * ldr + km + 1] : 1.0;
+  const int ncol = next ? m_eff : mk;
+  double yy = 0.0, ee = 0.0;
+  bool bad = false;
+  for (int64_t i = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kUpdThreads) {
+    double ay = 0.0, aw = 0.0;
+    int c = 0;
+    for (; c + 3 < ncol; c += 4) {
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = __ldcs(W + int64_t(c + q) * ldw + i);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ay += v[q] * cg[c + q];
+        aw += v[q] * cr[c + q];
+      }
+    }
+    for (; c < ncol; ++c) {
+      const double v = __ldcs(W + int64_t(c) * ldw + i);
+      ay += v * cg[c];
+      aw += v * cr[c];
+    }
+    const double y = alpha1 * ay;
+    bad |= !isfinite(y);
+    const double fn = f_hat[i] + y;
+    f_hat[i] = fn;
+    yy += y * y;
+    if (ref) {
+      const double e = fn - ref[i];
+      ee += e * e;
+    }
+    if (next) W[i] = (__ldcs(z + i) - aw) / rkk;
+  }
+  yy = block_sum<kUpdThreads>(yy, buf);
+  if (ref) ee = block_sum<kUpdThreads>(ee, buf2);
+  if (threadIdx.x == 0) {
+    atomicAdd(&st->yn2, yy);
+    if (ref) atomicAdd(&st->err2, ee);
+  }
+  if (bad) st->nonfinite = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0)  // coupling for the next R_accum block
+    st->coupling = next ? Rbar[int64_t(km) * ldr + km + 1] : 0.0;
+}
+
+__global__ void scale_copy_kernel(int64_t n, const double* __restrict__ src, double* dst,
+                                  const SolveState* st) {
+  const double a = st->alpha_k;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i] / a;
+}
+
+__global__ void fill_kernel(int64_t n, double v, double* x) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int stream_grid(int64_t work, int threads) {
+  const int64_t need = (work + threads - 1) / threads;
+  const int64_t cap = int64_t(sm_count()) * 8;
+  return int(std::max<int64_t>(1, std::min(need, cap)));
+}
+
+}  // namespace
+
+void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev, bool first,
+                         int m_eff, cudaStream_t st) {
+  start_init_kernel<<<1, kRgsThreads, 0, st>>>(d, sacc, U, st_dev, first ? 1 : 0, m_eff);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
+                     double* U, double* Rbar, SolveState* st_dev, cudaStream_t st) {
+  if (k >= 1024) param_error("randomized_arnoldi: m > 1024 is not supported on device");
+  const int64_t pt = (d + kRgsThreads - 1) / kRgsThreads;
+#define RKMF_RGS(P) rgs_step_kernel<P><<<1, kRgsThreads, 0, st>>>(d, k, ldr, n, tol, pacc, U, Rbar, st_dev)
+  if (pt <= 1) RKMF_RGS(1);
+  else if (pt <= 2) RKMF_RGS(2);
+  else if (pt <= 4) RKMF_RGS(4);
+  else if (pt <= 8) RKMF_RGS(8);
+  else if (pt <= 16) RKMF_RGS(16);
+  else param_error("sketch: d > 4096 is not supported on device");
+#undef RKMF_RGS
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double* z,
+                         const double* Rbar, int64_t ldr, const SolveState* st_dev,
+                         cudaStream_t st) {
+  basis_update_kernel<<<stream_grid(std::max<int64_t>(n / 2, 1), kUpdThreads), kUpdThreads, 0,
+                        st>>>(n, k, ldw, W, z, Rbar, ldr, st_dev);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const double* z,
+                         const double* Rbar, int64_t ldr, const double* g, double* f_hat,
+                         const double* ref, SolveState* st_dev, cudaStream_t st) {
+  if (m_eff > kMaxCoef) param_error("restart: m_r > 1024 is not supported on device");
+  final_update_kernel<<<stream_grid(n, kUpdThreads), kUpdThreads, 0, st>>>(
+      n, m_eff, ldw, W, z, Rbar, ldr, g, f_hat, ref, st_dev);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_scale_copy(int64_t n, const double* src, double* dst, const SolveState* st_dev,
+                       cudaStream_t st) {
+  scale_copy_kernel<<<stream_grid(n, 256), 256, 0, st>>>(n, src, dst, st_dev);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_fill(int64_t n, double v, double* x, cudaStream_t st) {
+  if (n <= 0) return;
+  fill_kernel<<<stream_grid(n, 256), 256, 0, st>>>(n, v, x);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+}  // namespace rkmf_b200

@@ -1,0 +1,128 @@
+// Internal declarations of the rkmf_b200 CUDA library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rkmf_b200.h"
+
+namespace rkmf_b200 {
+
+// ---- error plumbing: C++ exceptions inside, status codes at the C ABI ----
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void param_error(const std::string& m) { throw Error(RKMF_PARAMETER_ERROR, m); }
+[[noreturn]] inline void shape_error(const std::string& m) { throw Error(RKMF_SHAPE_ERROR, m); }
+[[noreturn]] inline void numerical_error(const std::string& m) {
+  throw Error(RKMF_NUMERICAL_ERROR, m);
+}
+
+#define RKMF_CUDA(call)                                                                  \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::rkmf_b200::Error(RKMF_DEVICE_ERROR, std::string("CUDA error: ") +          \
+                                                      cudaGetErrorString(e_) + " at " + \
+                                                      __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+// Tile geometry shared by the SpMV, sketch and update kernels: one tile is
+// kTileRows consecutive rows handled by one 128-thread block iteration.
+constexpr int kTileRows = 128;
+constexpr int kBlock = 128;
+
+// Per-solve device state: scalars that the kernels communicate through, read
+// back by the host once or twice per cycle (pinned mirror in the context).
+struct SolveState {
+  int32_t stopped;     // number of valid steps this cycle (m_eff unless breakdown)
+  int32_t breakdown;   // 1-based breakdown step, 0 = none
+  int32_t zero_start;  // start vector sketched to zero
+  int32_t nonfinite;   // y had a NaN/Inf
+  double alpha_k;      // this cycle's start norm ||S start||
+  double sigma;        // 1 / alpha_k (folded into column 0)
+  double alpha1;       // cycle-1 start norm (global scale)
+  double coupling;     // previous cycle's subdiagonal r_{m+1,m}
+  double yn2;          // ||y_k||^2 accumulator
+  double rnorm1;       // ||R_accum||_1 (full dense-f path)
+  double err2;         // ||f_hat - reference||^2
+};
+
+// ---- kernels (definitions in *.cu) ----
+// sketch.cu
+void launch_sketch_generate(int64_t d, int64_t n, int64_t zeta, uint64_t seed, uint16_t* rows,
+                            int8_t* signs, cudaStream_t st);
+void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
+                         const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
+                         cudaStream_t st);
+void launch_sketch_export(int64_t count, const uint16_t* rows, const int8_t* signs,
+                          int64_t* rows64, cudaStream_t st);
+
+// spmv.cu
+struct CsrView {
+  int64_t n_rows, n_cols, nnz;
+  const void* row_ptr;  // int32 or int64
+  bool rp64;
+  const int32_t* col;
+  const double* val;
+  int cap;  // products staged per chunk (shared memory)
+};
+struct SketchView {
+  int64_t d, n, zeta;
+  const uint16_t* tile_off;  // [num_tiles][d+1]
+  const uint8_t* tile_ent;   // [num_tiles][kTileRows*zeta]: local row | sign<<7
+  double scale;
+};
+// mode: 0 = z = xscale*A x ; 1 = also sketch z into pacc ; 2 = sketch x into pacc only.
+void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const double* x,
+                        const double* xscale_dev, double* z, double* pacc,
+                        const int32_t* stop_flag, int step, int grid, cudaStream_t st);
+int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode);
+void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st);
+void launch_matrix_check(const CsrView* A, int32_t* flags, cudaStream_t st);
+
+// krylov.cu
+void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev, bool first,
+                         int m_eff, cudaStream_t st);
+void launch_rgs_step(int64_t d, int k, int64_t m, int64_t n, double tol, double* pacc, double* U,
+                     double* Rbar, SolveState* st_dev, cudaStream_t st);
+void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double* z,
+                         const double* Rbar, int64_t ldr, const SolveState* st_dev,
+                         cudaStream_t st);
+void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const double* z,
+                         const double* Rbar, int64_t ldr, const double* g, double* f_hat,
+                         const double* ref, SolveState* st_dev, cudaStream_t st);
+void launch_scale_copy(int64_t n, const double* src, double* dst, const SolveState* st_dev,
+                       cudaStream_t st);
+void launch_fill(int64_t n, double v, double* x, cudaStream_t st);
+
+// densef.cu
+void launch_raccum_append(double* R, int64_t ldr_acc, int64_t M, const double* Rbar,
+                          int64_t ldr, SolveState* st_dev, cudaStream_t st);
+void launch_dense_norm1(const double* R, int64_t ld, int64_t N, double* out, cudaStream_t st);
+// Full exp(-t R) e1 by Taylor-19 Paterson-Stockmeyer scaling and squaring.
+// Writes u = exp(-tR) e1 (length N) into u_out. ws must hold 6*N*N doubles.
+void dense_expneg_e1(const double* R, int64_t ldr, int64_t N, double t, int s, double* ws,
+                     double* u_out, cudaStream_t st, int64_t* launches);
+// g[j] = alpha1 * u[M + j] (j < mk), g[0] *= sigma
+void launch_make_g(const double* u, int64_t M, int mk, double* g, const SolveState* st_dev,
+                   cudaStream_t st);
+// InvSqrt restart quadrature: see densef.cu for the recursion.
+struct QuadState {
+  int nq;
+  double* log_w;   // per node scalar state (double), size nq
+  double* pi;      // running products, size nq
+  double* emx;     // e_m^T x of the current block, size nq
+  double* shift;   // sigma_q, size nq
+  double* weight;  // w_q, size nq
+};
+void launch_quad_invsqrt_cycle(const double* Rbar, int64_t ldr, int mk, int64_t cycle,
+                               QuadState* q, double* g, const SolveState* st_dev,
+                               double* partial, cudaStream_t st);
+
+}  // namespace rkmf_b200

@@ -1,0 +1,188 @@
+// K1: sparse-sign sketch generation on device (setup, integer only).
+//
+// Restates make_sketch (proj/src/sketch.cpp:13-49) with SplitMix64
+// (proj/include/rkmf/rng.hpp:17-63): column j draws from the stream
+// derive(seed, j); Floyd's sampling picks zeta distinct rows of d, which are
+// sorted ascending; zeta Rademacher signs follow in sorted order. The output is
+// bit-identical to the reference definition (checked against the CPU oracle).
+//
+// Two device layouts are produced:
+//   rows/signs  [n][zeta]  uint16 / int8   the operator itself (export, tests)
+//   tile layout            per 128-column tile, the d x 128 block of S in CSR
+//                          by sketch row ("bin"): tile_off[tile][d+1] uint16
+//                          offsets and tile_ent[tile][128*zeta] uint8 entries
+//                          (local column | sign << 7), entries of a bin sorted
+//                          by local column. This is what the fused SpMV epilogue
+//                          reads: each thread owns a bin and gathers its ~zeta*128/d
+//                          contributions from shared memory, so the scatter-add of
+//                          sketch.cpp:55-61 becomes a deterministic gather with no
+//                          shared-memory atomics (fp64 smem atomics are CAS loops
+//                          on sm_100a).
+#include "rkmf_internal.cuh"
+
+namespace rkmf_b200 {
+
+namespace {
+
+constexpr int kMaxZeta = 64;
+
+__device__ __forceinline__ uint64_t sm64_next(uint64_t& s) {  // rng.hpp:21-26
+  uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t sm64_derive(uint64_t seed, uint64_t tag) {  // rng.hpp:56-59
+  uint64_t s = seed ^ (0xA0761D6478BD642FULL + tag * 0xE7037ED1A0B428DBULL);
+  return sm64_next(s);
+}
+
+// limits[i - (d - zeta)] = bound * (UINT64_MAX / bound) for bound = i + 1
+// (rng.hpp:35), precomputed on the host: the 64-bit division runs once per
+// distinct bound instead of once per draw.
+__global__ void sketch_generate_kernel(int64_t d, int64_t n, int zeta, uint64_t seed,
+                                       const uint64_t* __restrict__ limits,
+                                       uint16_t* __restrict__ rows, int8_t* __restrict__ signs) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  uint64_t s = sm64_derive(seed, uint64_t(j));
+  uint16_t chosen[kMaxZeta];
+  int cnt = 0;
+  for (int64_t i = d - zeta; i < d; ++i) {  // Floyd: sketch.cpp:33-40
+    const uint64_t bound = uint64_t(i) + 1;
+    const uint64_t limit = limits[i - (d - zeta)];
+    uint64_t v;
+    do { v = sm64_next(s); } while (v >= limit);  // next_below, rng.hpp:34-41
+    const uint16_t t = uint16_t(v % bound);
+    bool seen = false;
+    for (int q = 0; q < cnt; ++q) seen |= (chosen[q] == t);
+    chosen[cnt++] = seen ? uint16_t(i) : t;
+  }
+  for (int a = 1; a < zeta; ++a) {  // ascending sort, sketch.cpp:41
+    const uint16_t key = chosen[a];
+    int b = a - 1;
+    while (b >= 0 && chosen[b] > key) { chosen[b + 1] = chosen[b]; --b; }
+    chosen[b + 1] = key;
+  }
+  const int64_t base = j * zeta;
+  for (int k = 0; k < zeta; ++k) {  // signs in sorted order, sketch.cpp:43-46
+    rows[base + k] = chosen[k];
+    signs[base + k] = (sm64_next(s) & 1ULL) ? int8_t(1) : int8_t(-1);
+  }
+}
+
+// One block per 128-column tile: counting sort of the tile's n_tile*zeta
+// entries by sketch row, then a per-bin insertion sort by local column so the
+// layout (and hence every sketch sum) is deterministic.
+__global__ void sketch_tiles_kernel(int64_t d, int64_t n, int zeta, int64_t off_stride,
+                                    const uint16_t* __restrict__ rows,
+                                    const int8_t* __restrict__ signs,
+                                    uint16_t* __restrict__ tile_off,
+                                    uint8_t* __restrict__ tile_ent) {
+  extern __shared__ int sh[];
+  int* cnt = sh;                   // d + 1
+  int* cur = sh + (d + 1);         // d
+  uint8_t* ent = reinterpret_cast<uint8_t*>(cur + d);  // kTileRows * zeta
+  __shared__ int chunk_sum[kBlock];
+  const int64_t tile = blockIdx.x;
+  const int t = threadIdx.x;
+  const int64_t col = tile * kTileRows + t;
+  const bool live = col < n;
+  for (int64_t b = t; b <= d; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  if (live)
+    for (int k = 0; k < zeta; ++k) atomicAdd(&cnt[rows[col * zeta + k]], 1);
+  __syncthreads();
+  // exclusive scan of cnt[0..d) -> cnt (block scan over contiguous chunks)
+  const int64_t per = (d + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = min(d, int64_t(t) * per), hi = min(d, lo + per);
+  int s = 0;
+  for (int64_t b = lo; b < hi; ++b) s += cnt[b];
+  chunk_sum[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int q = 0; q < blockDim.x; ++q) { const int v = chunk_sum[q]; chunk_sum[q] = acc; acc += v; }
+  }
+  __syncthreads();
+  int run = chunk_sum[t];
+  for (int64_t b = lo; b < hi; ++b) { const int v = cnt[b]; cnt[b] = run; cur[b] = run; run += v; }
+  if (t == blockDim.x - 1) cnt[d] = run;  // == n_tile * zeta
+  __syncthreads();
+  if (live)
+    for (int k = 0; k < zeta; ++k) {
+      const int r = rows[col * zeta + k];
+      const int pos = atomicAdd(&cur[r], 1);
+      ent[pos] = uint8_t(t | (signs[col * zeta + k] < 0 ? 0x80 : 0));
+    }
+  __syncthreads();
+  for (int64_t b = t; b < d; b += blockDim.x) {  // deterministic order inside a bin
+    const int b0 = cnt[b], b1 = cnt[b + 1];
+    for (int a = b0 + 1; a < b1; ++a) {
+      const uint8_t key = ent[a];
+      int q = a - 1;
+      while (q >= b0 && (ent[q] & 0x7f) > (key & 0x7f)) { ent[q + 1] = ent[q]; --q; }
+      ent[q + 1] = key;
+    }
+  }
+  __syncthreads();
+  uint16_t* toff = tile_off + tile * off_stride;
+  for (int64_t b = t; b <= d; b += blockDim.x) toff[b] = uint16_t(cnt[b]);
+  uint8_t* tent = tile_ent + tile * int64_t(kTileRows) * zeta;
+  const int total = cnt[d];
+  for (int e = t; e < kTileRows * zeta; e += blockDim.x) tent[e] = e < total ? ent[e] : 0;
+}
+
+__global__ void sketch_export_kernel(int64_t count, const uint16_t* __restrict__ rows,
+                                     int64_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = rows[i];
+}
+
+}  // namespace
+
+void launch_sketch_generate(int64_t d, int64_t n, int64_t zeta, uint64_t seed, uint16_t* rows,
+                            int8_t* signs, cudaStream_t st) {
+  if (zeta > kMaxZeta) param_error("sketch: zeta > 64 is not supported on device");
+  if (d > 65535) param_error("sketch: d > 65535 is not supported on device");
+  std::vector<uint64_t> lim(static_cast<size_t>(zeta));
+  for (int64_t i = d - zeta; i < d; ++i) {
+    const uint64_t bound = uint64_t(i) + 1;
+    lim[size_t(i - (d - zeta))] = bound * (UINT64_MAX / bound);
+  }
+  uint64_t* dl = nullptr;
+  RKMF_CUDA(cudaMallocAsync(&dl, sizeof(uint64_t) * size_t(zeta), st));
+  RKMF_CUDA(cudaMemcpyAsync(dl, lim.data(), sizeof(uint64_t) * size_t(zeta),
+                            cudaMemcpyHostToDevice, st));
+  const int threads = 128;
+  const int64_t blocks = (n + threads - 1) / threads;
+  sketch_generate_kernel<<<unsigned(blocks), threads, 0, st>>>(d, n, int(zeta), seed, dl, rows,
+                                                               signs);
+  RKMF_CUDA(cudaGetLastError());
+  RKMF_CUDA(cudaFreeAsync(dl, st));
+}
+
+void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
+                         const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
+                         cudaStream_t st) {
+  const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+  const int64_t off_stride = (d + 1 + 7) / 8 * 8;
+  const size_t smem = sizeof(int) * size_t(2 * d + 1) + size_t(kTileRows * zeta) + 16;
+  if (smem > 200 * 1024) param_error("sketch: d too large for the device tile layout");
+  if (smem > 48 * 1024)
+    RKMF_CUDA(cudaFuncSetAttribute(sketch_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+  sketch_tiles_kernel<<<unsigned(tiles), kBlock, smem, st>>>(d, n, int(zeta), off_stride, rows,
+                                                              signs, tile_off, tile_ent);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_sketch_export(int64_t count, const uint16_t* rows, const int8_t* /*signs*/,
+                          int64_t* rows64, cudaStream_t st) {
+  if (count == 0) return;
+  sketch_export_kernel<<<unsigned((count + 255) / 256), 256, 0, st>>>(count, rows, rows64);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+}  // namespace rkmf_b200

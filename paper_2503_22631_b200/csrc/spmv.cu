@@ -1,0 +1,265 @@
+// K2: CSR SpMV with the sparse-sign sketch fused into its epilogue.
+//
+// Replaces spmv (proj/src/sparse.cpp:83-95) followed by sketch_apply
+// (proj/src/sketch.cpp:51-63) in the per-step loop of randomized_arnoldi
+// (proj/src/basis.cpp:120-121). HBM-bound (~0.2 flop/byte): the design goal is
+// to stream values/columns exactly once, coalesced, and never re-read z.
+//
+//  * Persistent grid (SM count x resident blocks). Block b walks tiles
+//    b, b+G, ... of 128 consecutive rows, so the sketch partial of a block
+//    accumulates in shared memory across all its tiles.
+//  * CSR-stream: the tile's nonzero range [rp[r0], rp[r0+128]) is read with
+//    fully coalesced loads into shared memory as products val*x[col] (chunks
+//    of `cap` products for long rows), then thread t reduces row t from shared
+//    memory in column order — the reference's row-sequential order.
+//  * Sketch epilogue: z_t*scale goes to shared memory; each thread owns sketch
+//    rows ("bins") b = t, t+128, ... and gathers the tile's contributions from
+//    the per-tile transposed layout (see sketch.cu). No atomics except one
+//    fp64 RED per bin per block at kernel end.
+#include <cuda_runtime.h>
+
+#include "rkmf_internal.cuh"
+
+namespace rkmf_b200 {
+
+namespace {
+
+template <typename RP, int MODE>
+__global__ void __launch_bounds__(kBlock)
+    spmv_sketch_kernel(int64_t n, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ val, const double* __restrict__ x,
+                       const double* xscale, double* __restrict__ z, int64_t num_tiles, int cap,
+                       int d, int zeta, int64_t off_stride, const uint16_t* __restrict__ toff,
+                       const uint8_t* __restrict__ tent, double sscale, double* pacc,
+                       const int32_t* stop, int step) {
+  if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool kSpmv = MODE <= 1;
+  constexpr bool kSketch = MODE >= 1;
+  double* acc = reinterpret_cast<double*>(smem_raw);       // [d]
+  double* zs = acc + (kSketch ? d : 0);                    // [128]
+  double* prod = zs + (kSketch ? kTileRows : 0);           // [cap]
+  uint16_t* off = reinterpret_cast<uint16_t*>(prod + (kSpmv ? cap : 0));  // [off_stride]
+  uint8_t* ent = reinterpret_cast<uint8_t*>(off + (kSketch ? off_stride : 0));  // [128*zeta]
+
+  const int t = threadIdx.x;
+  const double xs = xscale ? *xscale : 1.0;
+  if (kSketch)
+    for (int b = t; b < d; b += kBlock) acc[b] = 0.0;
+
+  for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kTileRows;
+    const int64_t row = r0 + t;
+    const bool live = row < n;
+    double zrow = 0.0;
+    if (kSpmv) {
+      const int64_t r1 = min(n, r0 + kTileRows);
+      const int64_t rs = int64_t(rp[r0]), re = int64_t(rp[r1]);
+      const int64_t my_lo = live ? int64_t(rp[row]) : 0, my_hi = live ? int64_t(rp[row + 1]) : 0;
+      double sum = 0.0;
+      for (int64_t c0 = rs; c0 < re; c0 += cap) {
+        const int64_t c1 = min(re, c0 + cap);
+        const int cnt = int(c1 - c0);
+        // coalesced stream of values and column indices; 4 loads in flight
+        int e = t;
+        for (; e + 3 * kBlock < cnt; e += 4 * kBlock) {
+          double v[4];
+          int c[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            v[q] = __ldcs(val + c0 + e + q * kBlock);
+            c[q] = __ldcs(ci + c0 + e + q * kBlock);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) prod[e + q * kBlock] = v[q] * __ldg(x + c[q]);
+        }
+        for (; e < cnt; e += kBlock) prod[e] = __ldcs(val + c0 + e) * __ldg(x + __ldcs(ci + c0 + e));
+        __syncthreads();
+        const int64_t lo = max(my_lo, c0), hi = min(my_hi, c1);
+        for (int64_t q = lo; q < hi; ++q) sum += prod[q - c0];
+        __syncthreads();
+      }
+      zrow = sum * xs;
+      if (live) z[row] = zrow;
+    } else {
+      zrow = live ? x[row] * xs : 0.0;
+    }
+    if (kSketch) {
+      zs[t] = live ? zrow * sscale : 0.0;
+      const uint16_t* go = toff + tile * off_stride;
+      for (int q = t; q < off_stride; q += kBlock) off[q] = go[q];
+      const uint4* ge = reinterpret_cast<const uint4*>(tent + tile * int64_t(kTileRows) * zeta);
+      uint4* se = reinterpret_cast<uint4*>(ent);
+      for (int q = t; q < 8 * zeta; q += kBlock) se[q] = __ldcs(ge + q);
+      __syncthreads();
+      for (int b = t; b < d; b += kBlock) {
+        const int e0 = off[b], e1 = off[b + 1];
+        double s = 0.0;
+        for (int e = e0; e < e1; ++e) {
+          const unsigned u = ent[e];
+          const double v = zs[u & 0x7f];
+          s += (u & 0x80) ? -v : v;
+        }
+        acc[b] += s;
+      }
+      __syncthreads();
+    }
+  }
+  if (kSketch)
+    for (int b = t; b < d; b += kBlock) atomicAdd(pacc + b, acc[b]);
+}
+
+size_t smem_bytes(int mode, int cap, int64_t d, int64_t zeta, int64_t off_stride) {
+  size_t s = 0;
+  if (mode >= 1) s += sizeof(double) * size_t(d + kTileRows);
+  if (mode <= 1) s += sizeof(double) * size_t(cap);
+  if (mode >= 1) s += sizeof(uint16_t) * size_t(off_stride) + size_t(kTileRows * zeta);
+  return (s + 15) / 16 * 16;
+}
+
+template <typename RP, int MODE>
+void* kernel_ptr() {
+  return reinterpret_cast<void*>(&spmv_sketch_kernel<RP, MODE>);
+}
+
+void* pick(bool rp64, int mode) {
+  if (rp64) {
+    if (mode == 0) return kernel_ptr<int64_t, 0>();
+    if (mode == 1) return kernel_ptr<int64_t, 1>();
+    return kernel_ptr<int64_t, 2>();
+  }
+  if (mode == 0) return kernel_ptr<int32_t, 0>();
+  if (mode == 1) return kernel_ptr<int32_t, 1>();
+  return kernel_ptr<int32_t, 2>();
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+}  // namespace
+
+int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode) {
+  const int64_t n = A ? A->n_rows : S->n;
+  const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+  const int cap = A ? A->cap : 0;
+  const int64_t d = S ? S->d : 0, zeta = S ? S->zeta : 0;
+  const int64_t off_stride = S ? (d + 1 + 7) / 8 * 8 : 0;
+  const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
+  void* fn = pick(A ? A->rp64 : false, mode);
+  if (smem > 48 * 1024)
+    RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int per_sm = 0;
+  RKMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t g = int64_t(per_sm) * num_sms();
+  return int(std::max<int64_t>(1, std::min<int64_t>(g, tiles)));
+}
+
+void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const double* x,
+                        const double* xscale_dev, double* z, double* pacc,
+                        const int32_t* stop_flag, int step, int grid, cudaStream_t st) {
+  const int64_t n = A ? A->n_rows : S->n;
+  const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+  const int cap = A ? A->cap : 0;
+  const int d = S ? int(S->d) : 0, zeta = S ? int(S->zeta) : 0;
+  const int64_t off_stride = S ? (S->d + 1 + 7) / 8 * 8 : 0;
+  const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
+  if (grid <= 0) grid = spmv_sketch_grid(A, S, mode);
+  const uint16_t* toff = S ? S->tile_off : nullptr;
+  const uint8_t* tent = S ? S->tile_ent : nullptr;
+  const double sscale = S ? S->scale : 1.0;
+  const bool rp64 = A ? A->rp64 : false;
+#define RKMF_LAUNCH_SPMV(RP, MODE)                                                             \
+  spmv_sketch_kernel<RP, MODE><<<grid, kBlock, smem, st>>>(                                    \
+      n, A ? static_cast<const RP*>(A->row_ptr) : nullptr, A ? A->col : nullptr,               \
+      A ? A->val : nullptr, x, xscale_dev, z, tiles, cap, d, zeta, off_stride, toff, tent,     \
+      sscale, pacc, stop_flag, step)
+  if (smem > 48 * 1024)
+    RKMF_CUDA(cudaFuncSetAttribute(pick(rp64, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+  if (rp64) {
+    if (mode == 0) RKMF_LAUNCH_SPMV(int64_t, 0);
+    else if (mode == 1) RKMF_LAUNCH_SPMV(int64_t, 1);
+    else RKMF_LAUNCH_SPMV(int64_t, 2);
+  } else {
+    if (mode == 0) RKMF_LAUNCH_SPMV(int32_t, 0);
+    else if (mode == 1) RKMF_LAUNCH_SPMV(int32_t, 1);
+    else RKMF_LAUNCH_SPMV(int32_t, 2);
+  }
+#undef RKMF_LAUNCH_SPMV
+  RKMF_CUDA(cudaGetLastError());
+}
+
+// ---- setup kernels: norm1 (sparse.cpp:97-102) and validate (sparse.cpp:61-81) ----
+namespace {
+
+template <typename RP>
+__global__ void colsum_kernel(int64_t nnz, const int32_t* __restrict__ ci,
+                              const double* __restrict__ val, double* colsum) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(colsum + ci[k], fabs(val[k]));
+}
+
+__global__ void max_kernel(int64_t n, const double* __restrict__ v, double* out) {
+  double m = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    m = fmax(m, v[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0)  // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(m));
+}
+
+// flags[0]: shape violation, flags[1]: non-finite value
+template <typename RP>
+__global__ void check_kernel(int64_t n_rows, int64_t n_cols, const RP* __restrict__ rp,
+                             const int32_t* __restrict__ ci, const double* __restrict__ val,
+                             int32_t* flags) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t lo = rp[r], hi = rp[r + 1];
+    if (hi < lo) { flags[0] = 1; continue; }
+    for (int64_t k = lo; k < hi; ++k) {
+      const int64_t c = ci[k];
+      if (c < 0 || c >= n_cols || (k > lo && c <= ci[k - 1])) flags[0] = 1;
+      if (!isfinite(val[k])) flags[1] = 1;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st) {
+  RKMF_CUDA(cudaMemsetAsync(colsum, 0, sizeof(double) * size_t(A->n_cols), st));
+  RKMF_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+  const int g = 4 * num_sms();
+  if (A->nnz > 0) colsum_kernel<int32_t><<<g, 256, 0, st>>>(A->nnz, A->col, A->val, colsum);
+  if (A->n_cols > 0) max_kernel<<<g, 256, 0, st>>>(A->n_cols, colsum, out);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_matrix_check(const CsrView* A, int32_t* flags, cudaStream_t st) {
+  RKMF_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), st));
+  const int g = 4 * num_sms();
+  if (A->n_rows == 0) return;
+  if (A->rp64)
+    check_kernel<int64_t><<<g, 256, 0, st>>>(A->n_rows, A->n_cols,
+                                             static_cast<const int64_t*>(A->row_ptr), A->col,
+                                             A->val, flags);
+  else
+    check_kernel<int32_t><<<g, 256, 0, st>>>(A->n_rows, A->n_cols,
+                                             static_cast<const int32_t*>(A->row_ptr), A->col,
+                                             A->val, flags);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+}  // namespace rkmf_b200

@@ -1,0 +1,277 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle.
+
+Bars (BASELINE.json north_star / SURVEY.md §7-8): sketch bit-exact; SpMV within
+1e-14 and the sketch within 1e-13 relative; restarted f(A)b within 1e-9
+relative 2-norm with the cycle count within +-1; the reference's identities at
+its own tolerances (test_basis.cpp, test_restart.cpp, acceptance.cpp).
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as T
+    assert T.cuda.is_available()
+    return T
+
+
+def rel(a, b):
+    a = np.asarray(a.cpu() if hasattr(a, "cpu") else a)
+    b = np.asarray(b.cpu() if hasattr(b, "cpu") else b)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------- K1: sketch generation, bit-exact ----------------
+@pytest.mark.parametrize("d,n,z,s", [(40, 300, 5, 123), (24, 24, 24, 9), (60, 500, 4, 77),
+                                     (30, 200, 1, 5), (120, 65536, 8, 1), (200, 100003, 8, 1),
+                                     (800, 3600, 4, 5)])
+def test_sketch_bitexact(rk, oracle, d, n, z, s):
+    S = rk.make_sketch(d, n, z, s)
+    rows, signs, scale = S.export()
+    O = oracle.make_sketch(d, n, z, s)
+    assert np.array_equal(rows, O.rows)
+    assert np.array_equal(signs, O.signs)
+    assert scale == O.scale
+
+
+def test_sketch_validation(rk):
+    for args in [(10, 5, 2, 0), (10, 50, 11, 0), (10, 50, 0, 0)]:
+        with pytest.raises(rk.ParameterError):
+            rk.make_sketch(*args)
+
+
+# ---------------- K2: SpMV + sketch ----------------
+@pytest.mark.parametrize("name,N", [("cfg1", 256), ("cfg2", 40), ("cfg4", 24), ("cfg3", 20)])
+def test_spmv_and_sketch(rk, oracle, torch, name, N):
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    OS = oracle.make_sketch(P.d, P.n, P.zeta, 1)
+    x = P.b
+    z = rk.spmv(A, x)
+    zo = oracle.spmv((P.row_ptr, P.col_idx, P.values), x)
+    assert rel(z, zo) <= 1e-14
+    p = rk.sketch_apply(S, x)
+    assert rel(p, oracle.sketch_apply(OS, x)) <= 1e-13
+    z2, p2 = rk.spmv_sketch(A, S, x)
+    assert rel(z2, zo) <= 1e-14
+    assert rel(p2, oracle.sketch_apply(OS, zo)) <= 1e-13
+    assert A.norm1 == pytest.approx(oracle.norm1((P.row_ptr, P.col_idx, P.values)), rel=1e-13)
+
+
+def test_spmv_irregular_rows(rk, oracle, torch):
+    # long rows exercise the chunked CSR-stream path; empty rows too
+    rng = np.random.default_rng(3)
+    n = 3000
+    A = H.random_sparse(n, 0.002, 5).tolil()
+    A[7, :] = rng.standard_normal(n)  # one dense row (n nnz > cap)
+    A[11, :] = 0
+    A = A.tocsr()
+    A.eliminate_zeros()
+    A.sort_indices()
+    M = rk.SparseMatrix.from_scipy(A)
+    x = rng.standard_normal(n)
+    assert rel(rk.spmv(M, x), A @ x) <= 1e-14
+
+
+def test_invalid_csr_rejected(rk):
+    A = H.random_sparse(50, 0.1, 1)
+    ci = A.indices.copy()
+    ci[0] = 500
+    with pytest.raises(rk.ShapeError):
+        rk.SparseMatrix.from_csr(A.indptr, ci, A.data)
+    v = A.data.copy()
+    v[0] = np.inf
+    with pytest.raises(rk.NumericalError):
+        rk.SparseMatrix.from_csr(A.indptr, A.indices, v)
+
+
+# ---------------- K3/K4: one randomized Arnoldi decomposition ----------------
+def test_randomized_arnoldi_matches_oracle(rk, oracle, torch):
+    for seed in range(5):
+        n, m = 400, 20
+        A = H.random_sparse(n, 0.02, seed + 100, shift=3.0)
+        b = H.random_vector(n, seed + 500)
+        S = rk.make_sketch(4 * m, n, 8, seed)
+        OS = oracle.make_sketch(4 * m, n, 8, seed)
+        dec = rk.randomized_arnoldi(rk.SparseMatrix.from_scipy(A), S, b, m)
+        od = oracle.arnoldi_decomp(A, b, m, OS)
+        assert dec.breakdown_at is None and od.breakdown_at is None
+        assert dec.start_norm == pytest.approx(od.start_norm, rel=1e-13)
+        assert np.abs(dec.Rbar - od.Rbar).max() <= 1e-10 * np.abs(od.Rbar).max()
+        assert rel(dec.W, od.W) <= 1e-10
+        assert rel(dec.U, od.U) <= 1e-10
+        assert dec.counters == od.counters
+        W = dec.W.cpu().numpy()
+        # residual identity A W_m = W_{m+1} Rbar (test_basis.cpp:21-29, <= 1e-12)
+        res = np.linalg.norm(A @ W[:, :m] - W @ dec.Rbar)
+        assert res / (oracle.norm1(A) * max(1, np.linalg.norm(W))) <= 1e-12
+        U = dec.U.cpu().numpy()
+        assert np.abs(U.T @ U - np.eye(m + 1)).max() <= 1e-8
+
+
+def test_randomized_arnoldi_breakdown_and_errors(rk, oracle, torch):
+    D = sp.diags([2.5, 1.0, 3.0, 4.0]).tocsr()
+    A = rk.SparseMatrix.from_scipy(D)
+    S = rk.make_sketch(4, 4, 4, 0)
+    dec = rk.randomized_arnoldi(A, S, np.array([2.0, 0, 0, 0]), 3)
+    assert dec.breakdown_at == 1
+    assert dec.Rm()[0, 0] == pytest.approx(2.5, rel=1e-14)
+    with pytest.raises(rk.ParameterError, match="zero start vector"):
+        rk.randomized_arnoldi(A, S, np.zeros(4), 2)
+    S3 = rk.make_sketch(3, 6, 2, 0)
+    A6 = rk.SparseMatrix.from_scipy(sp.identity(6, format="csr"))
+    with pytest.raises(rk.ParameterError):
+        rk.randomized_arnoldi(A6, S3, np.ones(6), 4)  # d < m+1
+
+
+# ---------------- the drop-in boundary: restarted_krylov ----------------
+def _solve_both(rk, oracle, P, S_seed=1, opts=None, **kw):
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    S = rk.make_sketch(P.d, P.n, P.zeta, S_seed)
+    OS = oracle.make_sketch(P.d, P.n, P.zeta, S_seed)
+    f = rk.FunctionSpec.exp_neg(P.t) if P.fn == "exp_neg" else rk.FunctionSpec.inv_sqrt()
+    opts = opts or rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
+    r = rk.restarted_krylov(A, P.b, f, opts, S, **kw)
+    o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b,
+                                oracle.KIND_EXP_NEG if P.fn == "exp_neg" else oracle.KIND_INV_SQRT,
+                                P.t, m_r=opts.m_r, tol=opts.tol, k_max=opts.k_max,
+                                budget_total_m=opts.budget_total_m, S=OS, want_R=True)
+    return r, o
+
+
+@pytest.mark.parametrize("name,N", [("cfg1", 256), ("cfg1", 64), ("cfg2", 32), ("cfg4", 32)])
+def test_restart_parity(rk, oracle, torch, name, N):
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    r, o = _solve_both(rk, oracle, P)
+    assert r.converged == o.converged
+    assert abs(r.cycles - o.cycles) <= 1
+    assert rel(r.f_hat, o.f_hat) <= 1e-9
+    if r.cycles == o.cycles:
+        for hr, ho in zip(r.history, o.history):
+            assert hr.total_m == ho["total_m"] and hr.total_matvecs == ho["total_matvecs"]
+            assert hr.start_norm == pytest.approx(ho["start_norm"], rel=1e-10)
+        R = r.R_accum
+        assert np.abs(R - o.R_accum).max() <= 1e-9 * np.abs(o.R_accum).max()
+    assert r.counters["matvecs"] == r.cycles * P.m or r.history[-1].total_m < r.cycles * P.m
+
+
+def test_restart_equal_cycles_forced(rk, oracle, torch):
+    """tol = 1e-30 forces equal cycle counts (test_restart.cpp:60, acceptance.cpp:304)."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build("cfg4", 20)
+    opts = rk.RestartOptions(m_r=P.m, tol=1e-30, k_max=5)
+    r, o = _solve_both(rk, oracle, P, opts=opts)
+    assert r.cycles == o.cycles == 5 and not r.converged
+    assert rel(r.f_hat, o.f_hat) <= 1e-9
+
+
+def test_restart_device_resident_and_reference(rk, oracle, torch):
+    from paper_2503_22631_b200 import configs
+    P = configs.build("cfg1", 64)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    f = rk.FunctionSpec.exp_neg(P.t)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
+    rh = rk.restarted_krylov(A, P.b, f, opts, S)
+    bd = torch.tensor(P.b, device="cuda")
+    ref = torch.tensor(rh.f_hat, device="cuda")
+    rd = rk.restarted_krylov(A, bd, f, opts, S, reference=ref)
+    assert rd.f_hat.is_cuda
+    assert rel(rd.f_hat, rh.f_hat) <= 1e-14
+    assert rd.history[-1].error_vs_reference <= 1e-14
+    assert rd.solve_ms > 0 and all(h.build_ms > 0 for h in rd.history)
+
+
+def test_restart_scale_cancellation(rk, torch):
+    """Global rescaling of S leaves the result unchanged (acceptance.cpp:464-493)."""
+    C = H.conv_diff_2d(20, 20, 0.01, 10.0, 0.0)
+    A = rk.SparseMatrix.from_scipy(C)
+    b = H.random_vector(C.shape[0], 1)
+    f = rk.FunctionSpec.exp_neg(1.0 / C.diagonal().max())
+    opts = rk.RestartOptions(m_r=8, k_max=6, tol=1e-12)
+    S1 = rk.make_sketch(120, C.shape[0], 4, 3)
+    r1 = rk.restarted_krylov(A, b, f, opts, S1)
+    S1.scale = S1.scale * 7.3
+    r2 = rk.restarted_krylov(A, b, f, opts, S1)
+    assert rel(r2.f_hat, r1.f_hat) <= 1e-13
+
+
+def test_restart_semantics(rk, oracle, torch):
+    """k_max / budget / validation / divergence (test_restart.cpp:209-277)."""
+    T = H.random_spd_tridiag(120, 1.0, 9.0, 31)
+    A = rk.SparseMatrix.from_scipy(T)
+    b = H.random_vector(120, 32)
+    S = rk.make_sketch(44, 120, 4, 1)
+    f = rk.FunctionSpec.exp_neg(1.0)
+    r = rk.restarted_krylov(A, b, f, rk.RestartOptions(m_r=10, tol=1e-30, k_max=3), S)
+    assert r.cycles == 3 and not r.converged and r.total_m == 30
+    r = rk.restarted_krylov(A, b, f, rk.RestartOptions(m_r=10, tol=1e-30, k_max=50,
+                                                       budget_total_m=25), S)
+    assert r.cycles == 2 and r.total_m == 20 and not r.converged
+    for kw in [dict(m_r=0), dict(k_max=0), dict(tol=0.0), dict(m_r=10, budget_total_m=5)]:
+        with pytest.raises(rk.ParameterError):
+            rk.restarted_krylov(A, b, f, rk.RestartOptions(**kw), S)
+    C = H.conv_diff_2d(60, 60, 0.001, 10.0, 0.0)
+    AC = rk.SparseMatrix.from_scipy(C)
+    Sd = rk.make_sketch(6, C.shape[0], 1, 3)
+    with pytest.raises(rk.NumericalError, match="^restart divergence"):
+        rk.restarted_krylov(AC, H.random_vector(C.shape[0], 1),
+                            rk.FunctionSpec.exp_neg(10.0 / oracle.norm1(C)),
+                            rk.RestartOptions(m_r=5, tol=1e-12, k_max=60), Sd)
+
+
+def test_restart_happy_breakdown(rk, oracle, torch):
+    """m_r = n: the Krylov space saturates in one cycle (test_restart.cpp:91-112)."""
+    n = 25
+    D = sp.diags([10.0 * (1.0 + np.arange(n)), 2.0 * np.ones(n - 1)], [0, -1]).tocsr()
+    D.sort_indices()
+    A = rk.SparseMatrix.from_scipy(D)
+    b = H.random_vector(n, 100)
+    S = rk.make_sketch(n, n, 4, 2)
+    r = rk.restarted_krylov(A, b, rk.FunctionSpec.exp_neg(0.02),
+                            rk.RestartOptions(m_r=n, tol=1e-30, k_max=10), S)
+    assert r.converged and r.cycles == 1
+    import scipy.linalg as sla
+    ex = sla.expm(-0.02 * D.toarray()) @ b
+    assert rel(r.f_hat, ex) <= 1e-9
+
+
+def test_inv_sqrt_quadrature_parity(rk, oracle, torch):
+    """InvSqrt (cfg3 kind, not in the reference): device restart quadrature vs
+    the oracle's full Denman-Beavers f(R_accum) — parity unpinned by the reference."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build("cfg3", 10)
+    P.m, P.d = 10, 40
+    P.tol = 1e-9 * np.linalg.norm(P.b)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=60)
+    r, o = _solve_both(rk, oracle, P, opts=opts)
+    assert abs(r.cycles - o.cycles) <= 1
+    assert rel(r.f_hat, o.f_hat) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["cfg2"])
+def test_full_size_properties(rk, torch, name):
+    """Full BASELINE size: converged, and f matches an independent check."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    r = rk.restarted_krylov(A, torch.tensor(P.b, device="cuda"), rk.FunctionSpec.exp_neg(P.t),
+                            rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max), S)
+    assert r.converged
+    assert r.history[-1].update_norm <= P.tol
+    # semigroup check: exp(-tA) b computed with two half-step solves
+    f = rk.FunctionSpec.exp_neg(P.t / 2)
+    o = rk.RestartOptions(m_r=P.m, tol=P.tol * 1e-2, k_max=P.k_max)
+    h1 = rk.restarted_krylov(A, torch.tensor(P.b, device="cuda"), f, o, S)
+    h2 = rk.restarted_krylov(A, h1.f_hat, f, o, S)
+    assert rel(h2.f_hat, r.f_hat) <= 1e-6
