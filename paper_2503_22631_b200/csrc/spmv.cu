@@ -36,8 +36,8 @@ __global__ void __launch_bounds__(kBlock)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool kSpmv = MODE <= 1;
   constexpr bool kSketch = MODE >= 1;
-  double* acc = reinterpret_cast<double*>(smem_raw);       // [d]
-  double* zs = acc + (kSketch ? d : 0);                    // [128]
+  double* acc = reinterpret_cast<double*>(smem_raw);       // [d rounded up to even]
+  double* zs = acc + (kSketch ? (d + 1) / 2 * 2 : 0);      // [128], 16-byte aligned
   double* prod = zs + (kSketch ? kTileRows : 0);           // [cap]
   uint16_t* off = reinterpret_cast<uint16_t*>(prod + (kSpmv ? cap : 0));  // [off_stride]
   uint8_t* ent = reinterpret_cast<uint8_t*>(off + (kSketch ? off_stride : 0));  // [128*zeta]
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kBlock)
 
 size_t smem_bytes(int mode, int cap, int64_t d, int64_t zeta, int64_t off_stride) {
   size_t s = 0;
-  if (mode >= 1) s += sizeof(double) * size_t(d + kTileRows);
+  if (mode >= 1) s += sizeof(double) * size_t((d + 1) / 2 * 2 + kTileRows);
   if (mode <= 1) s += sizeof(double) * size_t(cap);
   if (mode >= 1) s += sizeof(uint16_t) * size_t(off_stride) + size_t(kTileRows * zeta);
   return (s + 15) / 16 * 16;
