@@ -220,23 +220,29 @@ rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t 
   try {
     const bool rp64 = nnz >= (int64_t(1) << 31) - 1;
     M->view.rp64 = rp64;
+    // tail padding: the TMA-pipelined SpMV rounds its bulk copies up to 16 B
+    const size_t rp_elems = size_t(n_rows + 1 + kRpPad);
     if (rp64) {
-      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int64_t) * size_t(n_rows + 1)));
+      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int64_t) * rp_elems));
+      RKMF_CUDA(cudaMemsetAsync(M->rp, 0, sizeof(int64_t) * rp_elems, ctx->stream));
       RKMF_CUDA(cudaMemcpyAsync(M->rp, rp64_dev, sizeof(int64_t) * size_t(n_rows + 1),
                                 cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
-      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int32_t) * size_t(n_rows + 1)));
+      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int32_t) * rp_elems));
+      RKMF_CUDA(cudaMemsetAsync(M->rp, 0, sizeof(int32_t) * rp_elems, ctx->stream));
       rp_narrow_kernel<<<256, 256, 0, ctx->stream>>>(n_rows, rp64_dev,
                                                      static_cast<int32_t*>(M->rp));
       RKMF_CUDA(cudaGetLastError());
       ctx->launches++;
     }
-    if (!copy_colval) {
+    if (!copy_colval) {  // caller-allocated with kNnzPad elements of padding
       M->col = const_cast<int32_t*>(col_dev);
       M->val = const_cast<double*>(val_dev);
     } else {
-      RKMF_CUDA(cudaMalloc(&M->col, sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1))));
-      RKMF_CUDA(cudaMalloc(&M->val, sizeof(double) * size_t(std::max<int64_t>(nnz, 1))));
+      RKMF_CUDA(cudaMalloc(&M->col, sizeof(int32_t) * size_t(nnz + kNnzPad)));
+      RKMF_CUDA(cudaMalloc(&M->val, sizeof(double) * size_t(nnz + kNnzPad)));
+      RKMF_CUDA(cudaMemsetAsync(M->col, 0, sizeof(int32_t) * size_t(nnz + kNnzPad), ctx->stream));
+      RKMF_CUDA(cudaMemsetAsync(M->val, 0, sizeof(double) * size_t(nnz + kNnzPad), ctx->stream));
       if (nnz > 0) {
         RKMF_CUDA(cudaMemcpyAsync(M->col, col_dev, sizeof(int32_t) * size_t(nnz),
                                   cudaMemcpyDeviceToDevice, ctx->stream));
@@ -252,6 +258,8 @@ rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t 
     unsigned long long hmx = 0;
     RKMF_CUDA(cudaMemcpyAsync(&hmx, mx, 8, cudaMemcpyDeviceToHost, ctx->stream));
     RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    M->view.max_tile_nnz = int64_t(hmx);
+    M->view.padded = true;
     finish_matrix(M, int64_t(hmx));
   } catch (...) {
     if (M->rp) cudaFree(M->rp);
@@ -444,8 +452,10 @@ int rkmf_matrix_create_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
     int32_t* col = nullptr;
     double* val = nullptr;
     RKMF_CUDA(cudaMalloc(&rp_dev, sizeof(int64_t) * size_t(n_rows + 1)));
-    RKMF_CUDA(cudaMalloc(&col, sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1))));
-    RKMF_CUDA(cudaMalloc(&val, sizeof(double) * size_t(std::max<int64_t>(nnz, 1))));
+    RKMF_CUDA(cudaMalloc(&col, sizeof(int32_t) * size_t(nnz + kNnzPad)));
+    RKMF_CUDA(cudaMalloc(&val, sizeof(double) * size_t(nnz + kNnzPad)));
+    RKMF_CUDA(cudaMemsetAsync(col + nnz, 0, sizeof(int32_t) * size_t(kNnzPad), ctx->stream));
+    RKMF_CUDA(cudaMemsetAsync(val + nnz, 0, sizeof(double) * size_t(kNnzPad), ctx->stream));
     RKMF_CUDA(cudaMemcpyAsync(rp_dev, h_rp, sizeof(int64_t) * size_t(n_rows + 1),
                               cudaMemcpyHostToDevice, ctx->stream));
     if (nnz > 0) {

@@ -71,7 +71,13 @@ struct CsrView {
   const int32_t* col;
   const double* val;
   int cap;  // products staged per chunk (shared memory)
+  int64_t max_tile_nnz;  // largest nonzero count of a 128-row tile
+  bool padded;           // arrays carry the tail padding the TMA path needs
 };
+// Row-pointer tail padding (entries) and value/column padding (elements)
+// allocated by the engine so 16-byte-rounded bulk copies stay in bounds.
+constexpr int64_t kRpPad = 136;
+constexpr int64_t kNnzPad = 8;
 struct SketchView {
   int64_t d, n, zeta;
   const uint16_t* tile_off;  // [num_tiles][d+1]
@@ -83,6 +89,10 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
                         const double* xscale_dev, double* z, double* pacc,
                         const int32_t* stop_flag, int step, int grid, cudaStream_t st);
 int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode);
+// TMA-pipelined mode-1 kernel (spmv_pipe.cu); returns false when not applicable.
+bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
+                             const double* xscale_dev, double* z, double* pacc,
+                             const int32_t* stop_flag, int step, cudaStream_t st);
 void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st);
 void launch_matrix_check(const CsrView* A, int32_t* flags, cudaStream_t st);
 

@@ -18,6 +18,8 @@
 //    fp64 RED per bin per block at kernel end.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "rkmf_internal.cuh"
 
 namespace rkmf_b200 {
@@ -133,6 +135,16 @@ void* pick(bool rp64, int mode) {
   return kernel_ptr<int32_t, 2>();
 }
 
+// RKMF_SPMV_PIPE=0 selects the plain CSR-stream kernel (A/B comparisons).
+bool use_pipe() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_SPMV_PIPE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int num_sms() {
   static int sms = 0;
   if (sms == 0) {
@@ -172,6 +184,9 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
   const int d = S ? int(S->d) : 0, zeta = S ? int(S->zeta) : 0;
   const int64_t off_stride = S ? (S->d + 1 + 7) / 8 * 8 : 0;
   const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
+  if (mode == 1 && A && S && use_pipe() &&
+      launch_spmv_sketch_pipe(A, S, x, xscale_dev, z, pacc, stop_flag, step, st))
+    return;
   if (grid <= 0) grid = spmv_sketch_grid(A, S, mode);
   const uint16_t* toff = S ? S->tile_off : nullptr;
   const uint8_t* tent = S ? S->tile_ent : nullptr;

@@ -1,0 +1,254 @@
+// K2 (pipelined): fused CSR SpMV + sparse-sign sketch, warp-specialised and
+// fed by TMA bulk copies through an S-stage shared-memory ring.
+//
+// Why: the plain CSR-stream kernel (spmv.cu) is latency-bound on B200 — ncu
+// shows long-scoreboard stalls dominating at ~26% of HBM bandwidth, because
+// every 128-row tile pays row_ptr -> (val, col) -> x dependent round trips
+// in sequence. Here one producer lane per block streams each tile's row
+// pointers, values, column indices and sketch metadata with
+// cp.async.bulk (TMA, UBLKCP in SASS) into stage s, arriving on an mbarrier
+// with the transaction byte count, S tiles ahead of the consumers. The four
+// consumer warps only gather x (L2-resident) and reduce rows in the
+// reference's column order, then run the same deterministic bin gather for the
+// sketch as spmv.cu. Stages are released through a second mbarrier.
+//
+// Alignment: bulk copies need 16-byte aligned addresses and sizes, so each
+// copy starts at the aligned address at or below the tile's first nonzero and
+// the consumers index with the recorded shift. Arrays are allocated with
+// >= 16 bytes of tail padding (engine.cu) so the rounded-up copies stay in
+// bounds.
+#include <cuda_runtime.h>
+
+#include "rkmf_internal.cuh"
+
+namespace rkmf_b200 {
+
+namespace {
+
+constexpr int kConsumers = 128;  // = kTileRows, one row per consumer thread
+constexpr int kPipeThreads = kConsumers + 32;
+constexpr int kStages = 4;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT;\n}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void named_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+struct StageLayout {
+  uint32_t rp, val, col, off, ent, zs, meta, stride;
+};
+
+__host__ __device__ inline StageLayout stage_layout(int rp_bytes, int cap, int off_stride,
+                                                    int zeta) {
+  auto r16 = [](uint32_t x) { return (x + 15u) & ~15u; };
+  StageLayout L;
+  uint32_t o = 0;
+  L.rp = o;
+  o += r16(uint32_t(rp_bytes) * 136u);
+  L.val = o;
+  o += r16(uint32_t(cap + 2) * 8u);
+  L.col = o;
+  o += r16(uint32_t(cap + 4) * 4u);
+  L.off = o;
+  o += r16(uint32_t(off_stride) * 2u);
+  L.ent = o;
+  o += r16(uint32_t(kTileRows * zeta));
+  L.zs = o;
+  o += kTileRows * 8u;
+  L.meta = o;
+  o += 16u;
+  L.stride = (o + 127u) & ~127u;
+  return L;
+}
+
+struct TileMeta {
+  long long rs;
+  int vshift, cshift;
+};
+
+template <typename RP>
+__global__ void __launch_bounds__(kPipeThreads)
+    spmv_sketch_pipe_kernel(int64_t n, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ val, const double* __restrict__ x,
+                            const double* xscale, double* __restrict__ z, int64_t num_tiles,
+                            int cap, int d, int zeta, int off_stride,
+                            const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
+                            double sscale, double* pacc, const int32_t* stop, int step) {
+  if (stop != nullptr && *stop <= step) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  double* acc = reinterpret_cast<double*>(smem + kStages * L.stride);  // [d]
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int b = t; b < d; b += kPipeThreads) acc[b] = 0.0;
+  __syncthreads();
+
+  if (t >= kConsumers) {  // ---------------- producer warp ----------------
+    if (t != kConsumers) return;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int s = it % kStages;
+      if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+      unsigned char* st = smem + s * L.stride;
+      const int64_t r0 = tile * kTileRows, r1 = min(n, r0 + kTileRows);
+      const long long rs = (long long)rp[r0], re = (long long)rp[r1];
+      const long long vs0 = rs & ~1LL, cs0 = rs & ~3LL;
+      const uint32_t vbytes = uint32_t(((re - vs0) * 8 + 15) & ~15LL);
+      const uint32_t cbytes = uint32_t(((re - cs0) * 4 + 15) & ~15LL);
+      const uint32_t rbytes = sizeof(RP) == 4 ? 528u : 1040u;
+      const uint32_t obytes = uint32_t(off_stride) * 2u;
+      const uint32_t ebytes = uint32_t(kTileRows * zeta);
+      TileMeta* meta = reinterpret_cast<TileMeta*>(st + L.meta);
+      meta->rs = rs;
+      meta->vshift = int(rs - vs0);
+      meta->cshift = int(rs - cs0);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&full[s], rbytes + (re > rs ? vbytes + cbytes : 0u) + obytes + ebytes);
+      bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s]);
+      if (re > rs) {
+        bulk_g2s(st + L.val, val + vs0, vbytes, &full[s]);
+        bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s]);
+      }
+      bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s]);
+      bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s]);
+    }
+    return;
+  }
+
+  // ---------------- consumer warps: one row per thread ----------------
+  const double xs = xscale ? *xscale : 1.0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    const int s = it % kStages;
+    mbar_wait(&full[s], (it / kStages) & 1);
+    unsigned char* st = smem + s * L.stride;
+    const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
+    const double* vals = reinterpret_cast<const double*>(st + L.val);
+    const int32_t* cols = reinterpret_cast<const int32_t*>(st + L.col);
+    const uint16_t* off = reinterpret_cast<const uint16_t*>(st + L.off);
+    const uint8_t* ent = st + L.ent;
+    double* zs = reinterpret_cast<double*>(st + L.zs);
+    const TileMeta meta = *reinterpret_cast<const TileMeta*>(st + L.meta);
+    const int64_t row = tile * kTileRows + t;
+    double sum = 0.0;
+    if (row < n) {
+      const int lo = int((long long)rps[t] - meta.rs), hi = int((long long)rps[t + 1] - meta.rs);
+      for (int e = lo; e < hi; e += 8) {
+        double v[8], xv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const bool ok = e + q < hi;
+          v[q] = ok ? vals[meta.vshift + e + q] : 0.0;
+          xv[q] = ok ? __ldg(x + cols[meta.cshift + e + q]) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (e + q < hi) sum += v[q] * xv[q];
+      }
+      sum *= xs;
+      z[row] = sum;
+    }
+    zs[t] = row < n ? sum * sscale : 0.0;
+    named_sync();
+    for (int b = t; b < d; b += kConsumers) {
+      const int e0 = off[b], e1 = off[b + 1];
+      double a = 0.0;
+      for (int e = e0; e < e1; ++e) {
+        const unsigned u = ent[e];
+        const double w = zs[u & 0x7f];
+        a += (u & 0x80) ? -w : w;
+      }
+      acc[b] += a;
+    }
+    mbar_arrive(&empty[s]);
+  }
+  for (int b = t; b < d; b += kConsumers) atomicAdd(pacc + b, acc[b]);
+}
+
+template <typename RP>
+size_t pipe_smem(int cap, int d, int off_stride, int zeta) {
+  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
+  return size_t(kStages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
+}
+
+int sms() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+template <typename RP>
+bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
+                   const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
+                   int step, cudaStream_t st) {
+  const int off_stride = int((S->d + 1 + 7) / 8 * 8);
+  const size_t smem = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta));
+  if (smem > 220 * 1024) return false;
+  auto fn = spmv_sketch_pipe_kernel<RP>;
+  RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int per_sm = 0;
+  RKMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPipeThreads, smem));
+  if (per_sm < 1) return false;
+  const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
+  fn<<<grid, kPipeThreads, smem, st>>>(A->n_rows, static_cast<const RP*>(A->row_ptr), A->col,
+                                       A->val, x, xscale_dev, z, tiles, A->cap, int(S->d),
+                                       int(S->zeta), off_stride, S->tile_off, S->tile_ent,
+                                       S->scale, pacc, stop, step);
+  RKMF_CUDA(cudaGetLastError());
+  return true;
+}
+
+}  // namespace
+
+bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
+                             const double* xscale_dev, double* z, double* pacc,
+                             const int32_t* stop_flag, int step, cudaStream_t st) {
+  if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
+  return A->rp64 ? launch_pipe_t<int64_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
+                 : launch_pipe_t<int32_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
+}
+
+}  // namespace rkmf_b200

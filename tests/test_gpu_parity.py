@@ -240,9 +240,16 @@ def test_restart_happy_breakdown(rk, oracle, torch):
     r = rk.restarted_krylov(A, b, rk.FunctionSpec.exp_neg(0.02),
                             rk.RestartOptions(m_r=n, tol=1e-30, k_max=10), S)
     assert r.converged and r.cycles == 1
+    assert r.counters["matvecs"] == n and r.counters["basis_updates"] == n - 1
     import scipy.linalg as sla
     ex = sla.expm(-0.02 * D.toarray()) @ b
-    assert rel(r.f_hat, ex) <= 1e-9
+    # a square sparse-sign S (d = n) limits the randomized basis' accuracy; the
+    # oracle with the same S shows the same ~1e-8 gap to the exact value
+    o = oracle.restarted_krylov(D, b, oracle.KIND_EXP_NEG, 0.02, m_r=n, tol=1e-30, k_max=10,
+                                S=oracle.make_sketch(n, n, 4, 2))
+    assert o.cycles == 1
+    assert rel(r.f_hat, o.f_hat) <= 1e-8
+    assert rel(r.f_hat, ex) <= 1e-7
 
 
 def test_inv_sqrt_quadrature_parity(rk, oracle, torch):
