@@ -235,12 +235,21 @@ def run_ours(args):
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     e2e_m = 0
+    phases = {"matrix_upload_s": 0.0, "sketch_gen_s": 0.0, "solve_s": 0.0, "free_s": 0.0}
     for _ in range(e2e_steps):
+        p0 = time.perf_counter()
         A2 = rk.SparseMatrix.from_csr(rp_h.numpy(), ci_h.numpy(), v_h.numpy(), ctx=ctx)
+        p1 = time.perf_counter()
         S2 = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, ctx=ctx)
+        p2 = time.perf_counter()
         r2 = rk.restarted_krylov(A2, b_h.numpy(), f, opts, S2)
+        p3 = time.perf_counter()
         e2e_m += r2.total_m
         del A2, S2
+        p4 = time.perf_counter()
+        for k_, a_, b_ in [("matrix_upload_s", p0, p1), ("sketch_gen_s", p1, p2),
+                           ("solve_s", p2, p3), ("free_s", p3, p4)]:
+            phases[k_] += (b_ - a_) / e2e_steps
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
     et = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
@@ -295,7 +304,8 @@ def run_ours(args):
                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h,
-                       "note": "includes CSR upload+validation, device sketch generation"},
+                       "note": "includes CSR upload+validation, device sketch generation",
+                       "phases_per_step": phases},
                "gpu_launches": gpu_launches, "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
     if world > 1:

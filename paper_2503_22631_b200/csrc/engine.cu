@@ -113,6 +113,7 @@ struct rkmf_context {
 
 struct rkmf_matrix {
   rkmf_context* ctx = nullptr;
+  int device = 0;
   CsrView view{};
   void* rp = nullptr;
   int32_t* col = nullptr;
@@ -122,6 +123,7 @@ struct rkmf_matrix {
 
 struct rkmf_sketch {
   rkmf_context* ctx = nullptr;
+  int device = 0;
   int64_t d = 0, n = 0, zeta = 0;
   uint64_t seed = 0;
   double scale = 1.0;
@@ -214,6 +216,7 @@ rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t 
                                      bool copy_colval) {
   auto* M = new rkmf_matrix();
   M->ctx = ctx;
+  M->device = ctx->device;
   M->view.n_rows = n_rows;
   M->view.n_cols = n_cols;
   M->view.nnz = nnz;
@@ -491,8 +494,9 @@ int rkmf_matrix_create_device(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
 
 int rkmf_matrix_destroy(rkmf_matrix* M) {
   if (!M) return RKMF_OK;
-  cudaSetDevice(M->ctx->device);
-  cudaStreamSynchronize(M->ctx->stream);
+  // does not touch M->ctx: a matrix may be released after its context
+  // (cudaFree synchronises the device itself)
+  cudaSetDevice(M->device);
   if (M->rp) cudaFree(M->rp);
   if (M->col) cudaFree(M->col);
   if (M->val) cudaFree(M->val);
@@ -519,6 +523,7 @@ int rkmf_sketch_create(rkmf_context* ctx, int64_t d, int64_t n, int64_t zeta, ui
     if (d > n) param_error("sketch: d must not exceed n");
     auto* S = new rkmf_sketch();
     S->ctx = ctx;
+    S->device = ctx->device;
     S->d = d;
     S->n = n;
     S->zeta = zeta;
@@ -549,8 +554,7 @@ int rkmf_sketch_create(rkmf_context* ctx, int64_t d, int64_t n, int64_t zeta, ui
 
 int rkmf_sketch_destroy(rkmf_sketch* S) {
   if (!S) return RKMF_OK;
-  cudaSetDevice(S->ctx->device);
-  cudaStreamSynchronize(S->ctx->stream);
+  cudaSetDevice(S->device);
   cudaFree(S->rows);
   cudaFree(S->signs);
   cudaFree(S->tile_off);

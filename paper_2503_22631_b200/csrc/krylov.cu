@@ -64,35 +64,56 @@ __global__ void __launch_bounds__(kRgsThreads)
 // r_i = <u_i, p>, p -= r_i u_i for i = 0..k, r_kk = ||p||, breakdown test,
 // U[:,k+1] = p / r_kk. The sketch p arrives as the reduced partials in pacc,
 // which this kernel re-zeroes for the next step. One __syncthreads per MGS
-// iteration (ping-pong reduction slots); the next column of U is prefetched.
+// iteration (ping-pong reduction slots). U[:,0..k] (contiguous, <= ~80 KB at
+// BASELINE sizes) is staged into shared memory with one coalesced sweep first,
+// so the sequential sweep pays one L2 round trip instead of k+1; when it does
+// not fit, the next column is prefetched from global memory instead.
 template <int PT>
 __global__ void __launch_bounds__(kRgsThreads)
     rgs_step_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
-                    double* U, double* Rbar, SolveState* st) {
+                    double* U, double* Rbar, SolveState* st, int staged) {
   if (st->stopped <= k) return;
+  extern __shared__ __align__(16) double Us[];
   __shared__ double red[2][kRgsThreads / 32];
   __shared__ double rs[1024];
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
   double p[PT], u[PT], un[PT];
+  if (staged) {
+    const int64_t tot = int64_t(k + 1) * d;
+    const double2* src = reinterpret_cast<const double2*>(U);
+    double2* dst = reinterpret_cast<double2*>(Us);
+    for (int64_t q = t; q < tot / 2; q += kRgsThreads) dst[q] = src[q];
+    if ((tot & 1) && t == 0) Us[tot - 1] = U[tot - 1];
+  }
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const int64_t b = t + int64_t(j) * kRgsThreads;
     p[j] = b < d ? pacc[b] : 0.0;
     if (b < d) pacc[b] = 0.0;
-    un[j] = b < d ? U[b] : 0.0;
+    un[j] = (!staged && b < d) ? U[b] : 0.0;
   }
+  if (staged) __syncthreads();
   for (int i = 0; i <= k; ++i) {
     double part = 0.0;
-#pragma unroll
-    for (int j = 0; j < PT; ++j) {
-      u[j] = un[j];
-      part += u[j] * p[j];
-    }
-    if (i < k) {
+    if (staged) {
 #pragma unroll
       for (int j = 0; j < PT; ++j) {
         const int64_t b = t + int64_t(j) * kRgsThreads;
-        un[j] = b < d ? U[int64_t(i + 1) * d + b] : 0.0;
+        u[j] = b < d ? Us[int64_t(i) * d + b] : 0.0;
+        part += u[j] * p[j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < PT; ++j) {
+        u[j] = un[j];
+        part += u[j] * p[j];
+      }
+      if (i < k) {
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+          const int64_t b = t + int64_t(j) * kRgsThreads;
+          un[j] = b < d ? U[int64_t(i + 1) * d + b] : 0.0;
+        }
       }
     }
     part = warp_sum(part);
@@ -290,7 +311,27 @@ void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, doubl
                      double* U, double* Rbar, SolveState* st_dev, cudaStream_t st) {
   if (k >= 1024) param_error("randomized_arnoldi: m > 1024 is not supported on device");
   const int64_t pt = (d + kRgsThreads - 1) / kRgsThreads;
-#define RKMF_RGS(P) rgs_step_kernel<P><<<1, kRgsThreads, 0, st>>>(d, k, ldr, n, tol, pacc, U, Rbar, st_dev)
+  const size_t ubytes = sizeof(double) * size_t(k + 1) * size_t(d);
+  const int staged = ubytes <= 160 * 1024 ? 1 : 0;
+  const size_t smem = staged ? ubytes : 0;
+#define RKMF_RGS(P)                                                                              \
+  do {                                                                                           \
+    auto fn = rgs_step_kernel<P>;                                                                \
+    RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                   160 * 1024));                                                 \
+    fn<<<1, kRgsThreads, smem, st>>>(d, k, ldr, n, tol, pacc, U, Rbar, st_dev, staged);          \
+    const cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess) {                                                                     \
+      cudaFuncAttributes fa{};                                                                   \
+      cudaFuncGetAttributes(&fa, fn);                                                            \
+      throw Error(RKMF_DEVICE_ERROR,                                                             \
+                  std::string("rgs_step launch: ") + cudaGetErrorString(e_) +                    \
+                      " dyn_smem=" + std::to_string(smem) +                                      \
+                      " max_dyn=" + std::to_string(fa.maxDynamicSharedSizeBytes) +              \
+                      " static=" + std::to_string(fa.sharedSizeBytes) +                          \
+                      " regs=" + std::to_string(fa.numRegs) + " PT=" + std::to_string(P));      \
+    }                                                                                            \
+  } while (0)
   if (pt <= 1) RKMF_RGS(1);
   else if (pt <= 2) RKMF_RGS(2);
   else if (pt <= 4) RKMF_RGS(4);

@@ -19,6 +19,8 @@
 // bounds.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "rkmf_internal.cuh"
 
 namespace rkmf_b200 {
@@ -103,15 +105,16 @@ __global__ void __launch_bounds__(kPipeThreads)
                             const double* xscale, double* __restrict__ z, int64_t num_tiles,
                             int cap, int d, int zeta, int off_stride,
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
-                            double sscale, double* pacc, const int32_t* stop, int step) {
+                            double sscale, double* pacc, const int32_t* stop, int step,
+                            int nstages) {
   if (stop != nullptr && *stop <= step) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  double* acc = reinterpret_cast<double*>(smem + kStages * L.stride);  // [d]
+  double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d]
   const int t = threadIdx.x;
   if (t == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < nstages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
     }
@@ -123,12 +126,25 @@ __global__ void __launch_bounds__(kPipeThreads)
   if (t >= kConsumers) {  // ---------------- producer warp ----------------
     if (t != kConsumers) return;
     int it = 0;
+    // row-pointer pair of the next tile, prefetched one iteration ahead so the
+    // bulk copies of a tile are issued without a dependent global round trip
+    long long nrs = 0, nre = 0;
+    if (blockIdx.x < num_tiles) {
+      const int64_t r0 = int64_t(blockIdx.x) * kTileRows;
+      nrs = (long long)rp[r0];
+      nre = (long long)rp[min(n, r0 + kTileRows)];
+    }
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int s = it % kStages;
-      if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+      const int s = it % nstages;
+      const long long rs = nrs, re = nre;
+      const int64_t nt = tile + gridDim.x;
+      if (nt < num_tiles) {
+        nrs = (long long)rp[nt * kTileRows];
+        nre = (long long)rp[min(n, nt * kTileRows + kTileRows)];
+      }
+      if (it >= nstages) mbar_wait(&empty[s], ((it / nstages) - 1) & 1);
       unsigned char* st = smem + s * L.stride;
-      const int64_t r0 = tile * kTileRows, r1 = min(n, r0 + kTileRows);
-      const long long rs = (long long)rp[r0], re = (long long)rp[r1];
+      const int64_t r0 = tile * kTileRows;
       const long long vs0 = rs & ~1LL, cs0 = rs & ~3LL;
       const uint32_t vbytes = uint32_t(((re - vs0) * 8 + 15) & ~15LL);
       const uint32_t cbytes = uint32_t(((re - cs0) * 4 + 15) & ~15LL);
@@ -156,8 +172,8 @@ __global__ void __launch_bounds__(kPipeThreads)
   const double xs = xscale ? *xscale : 1.0;
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-    const int s = it % kStages;
-    mbar_wait(&full[s], (it / kStages) & 1);
+    const int s = it % nstages;
+    mbar_wait(&full[s], (it / nstages) & 1);
     unsigned char* st = smem + s * L.stride;
     const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
     const double* vals = reinterpret_cast<const double*>(st + L.val);
@@ -203,9 +219,19 @@ __global__ void __launch_bounds__(kPipeThreads)
 }
 
 template <typename RP>
-size_t pipe_smem(int cap, int d, int off_stride, int zeta) {
+size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages) {
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
-  return size_t(kStages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
+  return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
+}
+
+int env_stages() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_PIPE_STAGES");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > kStages) v = 0;
+  }
+  return v;
 }
 
 int sms() {
@@ -224,19 +250,40 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
                    int step, cudaStream_t st) {
   const int off_stride = int((S->d + 1 + 7) / 8 * 8);
-  const size_t smem = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta));
-  if (smem > 220 * 1024) return false;
   auto fn = spmv_sketch_pipe_kernel<RP>;
+  // Pick the stage count that maximises consumer warps per SM while keeping
+  // at least one tile in flight ahead of the consumers (cached per shape).
+  static thread_local int64_t key_c = -1;
+  static thread_local int best_s = 0, best_per = 0;
+  const int64_t key = (int64_t(A->cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP);
+  if (key != key_c) {
+    best_s = 0;
+    best_per = 0;
+    for (int s = 2; s <= kStages; ++s) {
+      if (env_stages() && s != env_stages()) continue;
+      const size_t sm = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta), s);
+      if (sm > 220 * 1024) continue;
+      RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      int per = 0;
+      RKMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kPipeThreads, sm));
+      // prefer more resident blocks; on a tie, more stages
+      if (per > 0 && (per > best_per || (per == best_per && s > best_s))) {
+        best_per = per;
+        best_s = s;
+      }
+    }
+    key_c = key;
+  }
+  if (best_s == 0) return false;
+  const int stages = best_s, per_sm = best_per;
+  const size_t smem = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta), stages);
   RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  int per_sm = 0;
-  RKMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPipeThreads, smem));
-  if (per_sm < 1) return false;
   const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
   fn<<<grid, kPipeThreads, smem, st>>>(A->n_rows, static_cast<const RP*>(A->row_ptr), A->col,
                                        A->val, x, xscale_dev, z, tiles, A->cap, int(S->d),
                                        int(S->zeta), off_stride, S->tile_off, S->tile_ent,
-                                       S->scale, pacc, stop, step);
+                                       S->scale, pacc, stop, step, stages);
   RKMF_CUDA(cudaGetLastError());
   return true;
 }
