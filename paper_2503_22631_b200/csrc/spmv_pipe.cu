@@ -54,12 +54,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Streamed operands (values, columns, sketch metadata) are read exactly once
+// per step: copy them with an L2 evict-first policy so they do not evict the
+// x vector being gathered or the z vector the basis update reads next.
+__device__ __forceinline__ uint64_t l2_policy(int evict_first) {
+  uint64_t pol;
+  if (evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
+                                         uint64_t* bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void named_sync() {
@@ -106,7 +117,7 @@ __global__ void __launch_bounds__(kPipeThreads)
                             int cap, int d, int zeta, int off_stride,
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
                             double sscale, double* pacc, const int32_t* stop, int step,
-                            int nstages) {
+                            int nstages, int evict_first) {
   if (stop != nullptr && *stop <= step) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
@@ -125,6 +136,7 @@ __global__ void __launch_bounds__(kPipeThreads)
 
   if (t >= kConsumers) {  // ---------------- producer warp ----------------
     if (t != kConsumers) return;
+    const uint64_t pol = l2_policy(evict_first);
     int it = 0;
     // row-pointer pair of the next tile, prefetched one iteration ahead so the
     // bulk copies of a tile are issued without a dependent global round trip
@@ -157,13 +169,13 @@ __global__ void __launch_bounds__(kPipeThreads)
       meta->cshift = int(rs - cs0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&full[s], rbytes + (re > rs ? vbytes + cbytes : 0u) + obytes + ebytes);
-      bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s]);
+      bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s], pol);
       if (re > rs) {
-        bulk_g2s(st + L.val, val + vs0, vbytes, &full[s]);
-        bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s]);
+        bulk_g2s(st + L.val, val + vs0, vbytes, &full[s], pol);
+        bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s], pol);
       }
-      bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s]);
-      bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s]);
+      bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], pol);
+      bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], pol);
     }
     return;
   }
@@ -222,6 +234,15 @@ template <typename RP>
 size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages) {
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
   return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
+}
+
+int env_evict_first() {  // RKMF_EVICT_FIRST=0 disables the streaming L2 hint
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_EVICT_FIRST");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
 }
 
 int env_stages() {
@@ -283,7 +304,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   fn<<<grid, kPipeThreads, smem, st>>>(A->n_rows, static_cast<const RP*>(A->row_ptr), A->col,
                                        A->val, x, xscale_dev, z, tiles, A->cap, int(S->d),
                                        int(S->zeta), off_stride, S->tile_off, S->tile_ent,
-                                       S->scale, pacc, stop, step, stages);
+                                       S->scale, pacc, stop, step, stages, env_evict_first());
   RKMF_CUDA(cudaGetLastError());
   return true;
 }
