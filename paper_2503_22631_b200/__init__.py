@@ -475,11 +475,12 @@ class RestartResult:
 
 
 def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions = None,
-                     S: SketchOperator = None, reference=None) -> RestartResult:
+                     S: SketchOperator = None, reference=None, out=None) -> RestartResult:
     """restart::restarted_krylov (restart.hpp:74-79) with the randomized builder.
 
     b may be a numpy array (host: the host<->device copies are part of the call)
-    or a CUDA tensor (device-resident); f_hat comes back in the same residency.
+    or a CUDA tensor (device-resident); f_hat comes back in the same residency
+    (into `out` when given: a float64 array/tensor of length n).
     """
     opts = opts or RestartOptions()
     ctx = A.ctx
@@ -491,12 +492,14 @@ def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions =
     if on_dev:
         import torch
         bb = b.to(torch.float64).contiguous()
-        fout = torch.empty(n, dtype=torch.float64, device=bb.device)
+        fout = out if out is not None else torch.empty(n, dtype=torch.float64, device=bb.device)
         ref = None if reference is None else _dev(reference, ctx)
         bptr, fptr = bb.data_ptr(), fout.data_ptr()
     else:
         bb = np.ascontiguousarray(b, np.float64)
-        fout = np.zeros(n)
+        fout = out if out is not None else np.zeros(n)
+        if fout.dtype != np.float64 or not fout.flags["C_CONTIGUOUS"] or fout.size != n:
+            raise ShapeError("restarted_krylov: out must be a contiguous float64 array of length n")
         ref = None if reference is None else np.ascontiguousarray(reference, np.float64)
         bptr, fptr = _ptr(bb), _ptr(fout)
     if len(bb) != n:
