@@ -281,9 +281,17 @@ def run_ours(args):
         dom = max((c for c in cb if kernels[c]["ms"] > 0), key=lambda c: kernels[c]["ms"])
         dk = kernels[dom]
         cyc_bytes = sum(cb.values())
+        traffic = None  # per-launch DRAM bytes of the committed ncu --set full capture
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+                tj = json.load(fh)
+            if args.config == "cfg2" and dom in tj:
+                traffic = tj[dom]["bytes"]
+        except Exception:
+            pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"],
                     "peak": peak, "unit": "GB/s", "frac": dk["frac"],
-                    "traffic": None, "alg_bytes_per_launch": dk["alg_bytes"] / dk["launches"],
+                    "traffic": traffic, "alg_bytes_per_launch": dk["alg_bytes"] / dk["launches"],
                     "avg_launch_ms": dk["ms"] / dk["launches"], "peak_source": peak_src,
                     "whole_solve_gbs": cyc_bytes / (max_ms / args.steps / 1e3) / 1e9}
         cpu = None

@@ -282,3 +282,14 @@ def test_full_size_properties(rk, torch, name):
     h1 = rk.restarted_krylov(A, torch.tensor(P.b, device="cuda"), f, o, S)
     h2 = rk.restarted_krylov(A, h1.f_hat, f, o, S)
     assert rel(h2.f_hat, r.f_hat) <= 1e-6
+
+
+def test_cpp_host_api(rk):
+    """include/rkmf_b200.hpp (the C++ mirror of restart.hpp) end to end."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(rk.LIB_PATH), "cpp_api_smoke")
+    assert os.path.exists(exe), "build() must produce the C++ smoke program"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "converged=1" in r.stdout
