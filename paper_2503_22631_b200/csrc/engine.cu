@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -26,6 +27,17 @@
 #include "rkmf_internal.cuh"
 
 using namespace rkmf_b200;
+
+namespace rkmf_b200 {
+bool pdl_enabled() {  // RKMF_PDL=0 launches the step kernels without PDL
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+}  // namespace rkmf_b200
 
 namespace {
 

@@ -72,12 +72,13 @@ template <int PT>
 __global__ void __launch_bounds__(kRgsThreads)
     rgs_step_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
                     double* U, double* Rbar, SolveState* st, int staged) {
-  if (st->stopped <= k) return;
   extern __shared__ __align__(16) double Us[];
   __shared__ double red[2][kRgsThreads / 32];
   __shared__ double rs[1024];
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
   double p[PT], u[PT], un[PT];
+  // Prologue (overlaps the SpMV's tail under PDL): U[:,0..k] is final — it was
+  // written by rgs steps that completed before the SpMV of this step started.
   if (staged) {
     const int64_t tot = int64_t(k + 1) * d;
     const double2* src = reinterpret_cast<const double2*>(U);
@@ -85,6 +86,8 @@ __global__ void __launch_bounds__(kRgsThreads)
     for (int64_t q = t; q < tot / 2; q += kRgsThreads) dst[q] = src[q];
     if ((tot & 1) && t == 0) Us[tot - 1] = U[tot - 1];
   }
+  pdl_wait_then_trigger();
+  if (st->stopped <= k) return;
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const int64_t b = t + int64_t(j) * kRgsThreads;
@@ -160,6 +163,7 @@ constexpr int kMaxCoef = 1024;
 __global__ void __launch_bounds__(kUpdThreads)
     basis_update_kernel(int64_t n, int k, int64_t ldw, double* W, const double* __restrict__ z,
                         const double* __restrict__ Rbar, int64_t ldr, const SolveState* st) {
+  pdl_wait_then_trigger();
   if (st->stopped <= k) return;  // no update at (or after) a breakdown step
   __shared__ double coef[kMaxCoef];
   for (int c = threadIdx.x; c <= k; c += kUpdThreads)
@@ -314,23 +318,13 @@ void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, doubl
   const size_t ubytes = sizeof(double) * size_t(k + 1) * size_t(d);
   const int staged = ubytes <= 160 * 1024 ? 1 : 0;
   const size_t smem = staged ? ubytes : 0;
-#define RKMF_RGS(P)                                                                              \
-  do {                                                                                           \
-    auto fn = rgs_step_kernel<P>;                                                                \
-    RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
-                                   160 * 1024));                                                 \
-    fn<<<1, kRgsThreads, smem, st>>>(d, k, ldr, n, tol, pacc, U, Rbar, st_dev, staged);          \
-    const cudaError_t e_ = cudaGetLastError();                                                   \
-    if (e_ != cudaSuccess) {                                                                     \
-      cudaFuncAttributes fa{};                                                                   \
-      cudaFuncGetAttributes(&fa, fn);                                                            \
-      throw Error(RKMF_DEVICE_ERROR,                                                             \
-                  std::string("rgs_step launch: ") + cudaGetErrorString(e_) +                    \
-                      " dyn_smem=" + std::to_string(smem) +                                      \
-                      " max_dyn=" + std::to_string(fa.maxDynamicSharedSizeBytes) +              \
-                      " static=" + std::to_string(fa.sharedSizeBytes) +                          \
-                      " regs=" + std::to_string(fa.numRegs) + " PT=" + std::to_string(P));      \
-    }                                                                                            \
+#define RKMF_RGS(P)                                                                    \
+  do {                                                                                 \
+    auto fn = rgs_step_kernel<P>;                                                      \
+    RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                   160 * 1024));                                       \
+    launch_maybe_pdl(fn, dim3(1), dim3(kRgsThreads), smem, st, d, k, ldr, n, tol, pacc, \
+                     U, Rbar, st_dev, staged);                                         \
   } while (0)
   if (pt <= 1) RKMF_RGS(1);
   else if (pt <= 2) RKMF_RGS(2);
@@ -345,9 +339,8 @@ void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, doubl
 void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double* z,
                          const double* Rbar, int64_t ldr, const SolveState* st_dev,
                          cudaStream_t st) {
-  basis_update_kernel<<<stream_grid(std::max<int64_t>(n / 2, 1), kUpdThreads), kUpdThreads, 0,
-                        st>>>(n, k, ldw, W, z, Rbar, ldr, st_dev);
-  RKMF_CUDA(cudaGetLastError());
+  launch_maybe_pdl(basis_update_kernel, dim3(stream_grid(std::max<int64_t>(n / 2, 1), kUpdThreads)),
+                   dim3(kUpdThreads), 0, st, n, k, ldw, W, z, Rbar, ldr, st_dev);
 }
 
 void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const double* z,

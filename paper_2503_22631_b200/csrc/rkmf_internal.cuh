@@ -32,6 +32,36 @@ struct Error : std::runtime_error {
                                                       __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
 
+// ---- programmatic dependent launch (PDL) between the per-step kernels ----
+// Each step kernel runs its dependency-free prologue, then waits for the
+// previous kernel in the stream (griddepcontrol.wait: full completion and
+// memory visibility), then lets the next kernel launch. Triggering only after
+// the wait keeps the chain strictly ordered (kernel i+1 never overlaps i-1).
+// Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait_then_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();  // RKMF_PDL=0 disables (engine.cu)
+
+template <typename... KArgs, typename... Args>
+void launch_maybe_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess)
+    throw Error(RKMF_DEVICE_ERROR, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+}
+
 // Tile geometry shared by the SpMV, sketch and update kernels: one tile is
 // kTileRows consecutive rows handled by one 128-thread block iteration.
 constexpr int kTileRows = 128;

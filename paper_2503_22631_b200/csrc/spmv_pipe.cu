@@ -118,7 +118,6 @@ __global__ void __launch_bounds__(kPipeThreads)
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
                             double sscale, double* pacc, const int32_t* stop, int step,
                             int nstages, int evict_first) {
-  if (stop != nullptr && *stop <= step) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -133,6 +132,8 @@ __global__ void __launch_bounds__(kPipeThreads)
   }
   for (int b = t; b < d; b += kPipeThreads) acc[b] = 0.0;
   __syncthreads();
+  pdl_wait_then_trigger();  // x, pacc and the stop flag come from earlier kernels
+  if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
 
   if (t >= kConsumers) {  // ---------------- producer warp ----------------
     if (t != kConsumers) return;
@@ -301,11 +302,10 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
-  fn<<<grid, kPipeThreads, smem, st>>>(A->n_rows, static_cast<const RP*>(A->row_ptr), A->col,
-                                       A->val, x, xscale_dev, z, tiles, A->cap, int(S->d),
-                                       int(S->zeta), off_stride, S->tile_off, S->tile_ent,
-                                       S->scale, pacc, stop, step, stages, env_evict_first());
-  RKMF_CUDA(cudaGetLastError());
+  launch_maybe_pdl(fn, dim3(grid), dim3(kPipeThreads), smem, st, A->n_rows,
+                   static_cast<const RP*>(A->row_ptr), A->col, A->val, x, xscale_dev, z, tiles,
+                   A->cap, int(S->d), int(S->zeta), off_stride, S->tile_off, S->tile_ent,
+                   S->scale, pacc, stop, step, stages, env_evict_first());
   return true;
 }
 
