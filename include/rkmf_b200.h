@@ -174,6 +174,30 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
                           const double* reference, rkmf_restart_result* result,
                           rkmf_cycle_record* records, int64_t records_cap);
 
+/* ---- multi-GPU: one process per GPU, rows block-partitioned.
+ * rkmf_nccl_unique_id fills 128 bytes on one rank; broadcast them (any
+ * transport) and call rkmf_context_init_comm on every rank. A partitioned
+ * matrix takes the rank's rows [row_starts[rank], row_starts[rank+1]) with
+ * local row pointers and GLOBAL column indices; a partitioned sketch is the
+ * same column range of make_sketch(d, n_global, zeta, seed). With both,
+ * rkmf_restarted_krylov / rkmf_randomized_arnoldi run the distributed solve:
+ * b, f_out and reference are the rank's local slices. ---- */
+int rkmf_nccl_unique_id(void* out128);
+int rkmf_context_init_comm(rkmf_context* ctx, int32_t nranks, int32_t rank,
+                           const void* unique_id128);
+int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const int64_t* row_starts,
+                                   const int64_t* h_row_ptr_local, const int32_t* h_col_global,
+                                   const double* h_values, rkmf_matrix** out);
+int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_global, int64_t zeta,
+                                   uint64_t seed, int64_t col_begin, int64_t n_local,
+                                   rkmf_sketch** out);
+/* Host-only partition helpers (no GPU needed): nnz-balanced contiguous row
+ * blocks, and one rank's halo plan (see partition.cpp). */
+int rkmf_partition_rows(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* row_starts);
+int rkmf_partition_halo(int32_t nranks, int32_t rank, const int64_t* row_starts,
+                        const int64_t* row_ptr_local, const int32_t* col_global, int64_t* n_halo,
+                        int64_t* halo_global, int64_t* recv_counts, int32_t* col_local);
+
 /* R_accum of the last solve on this context (total_m x total_m, column-major,
  * host); n_cap is the caller's capacity in rows. */
 int rkmf_last_r_accum(rkmf_context* ctx, double* h_R, int64_t n_cap, int64_t* total_m);

@@ -118,6 +118,12 @@ SYMBOLS = [
     ("rkmf_restarted_krylov", C.c_int,
      [_P, _P, _P, _P, C.c_int, _I32, _D, _P, _P, C.c_int, _P, _P, _P, _I64]),
     ("rkmf_last_r_accum", C.c_int, [_P, _P, _I64, _P]),
+    ("rkmf_nccl_unique_id", C.c_int, [_P]),
+    ("rkmf_context_init_comm", C.c_int, [_P, _I32, _I32, _P]),
+    ("rkmf_matrix_create_partitioned", C.c_int, [_P, _I64, _P, _P, _P, _P, _PP]),
+    ("rkmf_sketch_create_partitioned", C.c_int, [_P, _I64, _I64, _I64, _U64, _I64, _I64, _PP]),
+    ("rkmf_partition_rows", C.c_int, [_I64, _P, _I32, _P]),
+    ("rkmf_partition_halo", C.c_int, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
     ("rkmf_gen_laplacian", C.c_int, [_I32, _I64, _P, _P, _P, _P, _P]),
     ("rkmf_gen_q1_hex", C.c_int, [_I64, _I32, _U64, _I32, _P, _P, _P, _P, _P]),
     ("rkmf_gen_convdiff_upwind", C.c_int, [_I64, _D, _D, _D, _D, _P, _P, _P, _P, _P]),
@@ -525,6 +531,75 @@ def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions =
                                        basis_updates=res.basis_updates,
                                        peak_basis_cols=res.peak_basis_cols),
                          solve_ms=res.solve_ms, _ctx=ctx)
+
+
+# ---- multi-GPU: row-block partition ----
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    if lib().rkmf_nccl_unique_id(buf) != RKMF_OK:
+        raise DeviceError("ncclGetUniqueId failed")
+    return buf.raw
+
+
+def init_comm(ctx: Context, nranks: int, rank: int, unique_id: bytes) -> None:
+    """One NCCL communicator per context (one process per GPU)."""
+    buf = C.create_string_buffer(unique_id, 128)
+    ctx.check(lib().rkmf_context_init_comm(ctx.h, nranks, rank, buf))
+    ctx.nranks, ctx.rank = nranks, rank
+
+
+def partition_rows(row_ptr, nranks: int) -> np.ndarray:
+    """nnz-balanced contiguous row blocks: row_starts[nranks+1] (host)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    out = np.empty(nranks + 1, np.int64)
+    lib().rkmf_partition_rows(len(rp) - 1, _ptr(rp), nranks, _ptr(out))
+    return out
+
+
+def local_rows(row_ptr, col_idx, values, row_starts, rank):
+    """Rows [row_starts[rank], row_starts[rank+1]) with local row pointers and
+    global columns."""
+    rb, re = int(row_starts[rank]), int(row_starts[rank + 1])
+    lo, hi = int(row_ptr[rb]), int(row_ptr[re])
+    rp = np.ascontiguousarray(row_ptr[rb:re + 1] - lo, np.int64)
+    return rp, np.ascontiguousarray(col_idx[lo:hi], np.int32), np.ascontiguousarray(values[lo:hi])
+
+
+def partition_halo(row_starts, rank: int, rp_local, col_global):
+    """Halo plan of one rank (host): (halo_global, recv_counts, col_local)."""
+    rs = np.ascontiguousarray(row_starts, np.int64)
+    rp = np.ascontiguousarray(rp_local, np.int64)
+    cg = np.ascontiguousarray(col_global, np.int32)
+    P = len(rs) - 1
+    nh = C.c_int64()
+    lib().rkmf_partition_halo(P, rank, _ptr(rs), _ptr(rp), _ptr(cg), C.byref(nh), None, None,
+                              None)
+    halo = np.empty(nh.value, np.int64)
+    rc = np.empty(P, np.int64)
+    cl = np.empty(len(cg), np.int32)
+    lib().rkmf_partition_halo(P, rank, _ptr(rs), _ptr(rp), _ptr(cg), C.byref(nh), _ptr(halo),
+                              _ptr(rc), _ptr(cl))
+    return halo, rc, cl
+
+
+def partitioned_matrix(ctx: Context, n_global: int, row_starts, rp_local, col_global,
+                       values) -> SparseMatrix:
+    rs = np.ascontiguousarray(row_starts, np.int64)
+    rp = np.ascontiguousarray(rp_local, np.int64)
+    cg = np.ascontiguousarray(col_global, np.int32)
+    v = np.ascontiguousarray(values, np.float64)
+    h = C.c_void_p()
+    ctx.check(lib().rkmf_matrix_create_partitioned(ctx.h, n_global, _ptr(rs), _ptr(rp), _ptr(cg),
+                                                   _ptr(v), C.byref(h)))
+    return SparseMatrix(ctx, h)
+
+
+def partitioned_sketch(ctx: Context, d: int, n_global: int, zeta: int, seed: int, col_begin: int,
+                       n_local: int) -> SketchOperator:
+    h = C.c_void_p()
+    ctx.check(lib().rkmf_sketch_create_partitioned(ctx.h, d, n_global, zeta, C.c_uint64(seed),
+                                                   col_begin, n_local, C.byref(h)))
+    return SketchOperator(ctx, h, d, n_local, zeta, seed)
 
 
 # ---- synthetic inputs (host; need only the shared library, not a GPU) ----

@@ -1,0 +1,301 @@
+// Multi-GPU plumbing: NCCL communicator, row-partitioned matrices and sketches,
+// the per-step halo exchange and the sketch allreduce.
+//
+// One process per GPU. Rank r owns rows [row_starts[r], row_starts[r+1]) of A,
+// the same rows of every basis vector, of z and of f; its sketch is the same
+// column range of the global S (bit-identical to make_sketch on n_global).
+// Per Krylov step:
+//   halo exchange   pack the owned x entries other ranks reference, then
+//                   ncclSend/ncclRecv with every neighbour in one group; the
+//                   received values land directly in the halo tail of the x
+//                   column (W is allocated with ld >= n_local + n_halo)
+//   local K2        SpMV over [owned | halo] columns + local sketch partial
+//   allreduce       ncclAllReduce(sum) of the d sketch doubles, in place
+//   K3              replicated (every rank holds the same p, hence the same r)
+//   K4              local
+// Per cycle: allreduce of the start sketch (d) and of ||y||^2, ||f-ref||^2 (2).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "engine_types.cuh"
+
+extern "C" int rkmf_partition_halo(int32_t nranks, int32_t rank, const int64_t* row_starts,
+                                   const int64_t* row_ptr_local, const int32_t* col_global,
+                                   int64_t* n_halo, int64_t* halo_global, int64_t* recv_counts,
+                                   int32_t* col_local);
+
+namespace rkmf_b200 {
+
+#define RKMF_NCCL(call)                                                                   \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      throw Error(RKMF_DEVICE_ERROR, std::string("NCCL error: ") + ncclGetErrorString(r_) + \
+                                         " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+namespace {
+
+__global__ void pack_kernel(int64_t cnt, const int32_t* __restrict__ idx,
+                            const double* __restrict__ x, double* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = x[idx[i]];
+}
+
+__global__ void colsum_abs_kernel(int64_t nnz, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ val, double* colsum) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(colsum + ci[k], fabs(val[k]));
+}
+
+__global__ void scatter_add_kernel(int64_t cnt, const int32_t* __restrict__ idx,
+                                   const double* __restrict__ v, double* out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(out + idx[i], v[i]);
+}
+
+__global__ void max_abs_kernel(int64_t n, const double* __restrict__ v, double* out) {
+  double m = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    m = fmax(m, v[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(m));
+}
+
+int blocks_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096))); }
+
+}  // namespace
+
+void comm_allreduce_sum(rkmf_context* ctx, double* buf, size_t count) {
+  if (!ctx->comm || ctx->nranks <= 1 || count == 0) return;
+  RKMF_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+}
+
+void comm_halo_exchange(rkmf_context* ctx, const rkmf_matrix* A, double* x) {
+  if (!A->partitioned || !ctx->comm || ctx->nranks <= 1) return;
+  const HaloPlan& h = A->halo;
+  if (h.send_total > 0) {
+    pack_kernel<<<blocks_for(h.send_total), 256, 0, ctx->stream>>>(h.send_total, h.send_idx, x,
+                                                                    h.sendbuf);
+    RKMF_CUDA(cudaGetLastError());
+    ctx->launches++;
+  }
+  RKMF_NCCL(ncclGroupStart());
+  for (int q = 0; q < ctx->nranks; ++q) {
+    if (q == ctx->rank) continue;
+    if (h.send_cnt[q] > 0)
+      RKMF_NCCL(ncclSend(h.sendbuf + h.send_off[q], size_t(h.send_cnt[q]), ncclFloat64, q,
+                         ctx->comm, ctx->stream));
+    if (h.recv_cnt[q] > 0)
+      RKMF_NCCL(ncclRecv(x + h.n_local + h.recv_off[q], size_t(h.recv_cnt[q]), ncclFloat64, q,
+                         ctx->comm, ctx->stream));
+  }
+  RKMF_NCCL(ncclGroupEnd());
+}
+
+}  // namespace rkmf_b200
+
+using namespace rkmf_b200;
+
+namespace {
+
+template <class F>
+int guarded_c(rkmf_context* ctx, F&& fn) {
+  try {
+    fn();
+    if (ctx) ctx->last_error.clear();
+    return RKMF_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return RKMF_INTERNAL_ERROR;
+  }
+}
+
+// int64 all-to-all of per-rank segments through grouped send/recv
+void exchange_i64(rkmf_context* ctx, const int64_t* send_dev, const std::vector<int64_t>& soff,
+                  const std::vector<int64_t>& scnt, int64_t* recv_dev,
+                  const std::vector<int64_t>& roff, const std::vector<int64_t>& rcnt) {
+  RKMF_NCCL(ncclGroupStart());
+  for (int q = 0; q < ctx->nranks; ++q) {
+    if (q == ctx->rank) continue;
+    if (scnt[q] > 0)
+      RKMF_NCCL(ncclSend(send_dev + soff[q], size_t(scnt[q]), ncclInt64, q, ctx->comm,
+                         ctx->stream));
+    if (rcnt[q] > 0)
+      RKMF_NCCL(ncclRecv(recv_dev + roff[q], size_t(rcnt[q]), ncclInt64, q, ctx->comm,
+                         ctx->stream));
+  }
+  RKMF_NCCL(ncclGroupEnd());
+}
+
+}  // namespace
+
+extern "C" {
+
+int rkmf_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return RKMF_DEVICE_ERROR;
+  std::memcpy(out128, &id, sizeof(id));
+  return RKMF_OK;
+}
+
+int rkmf_context_init_comm(rkmf_context* ctx, int32_t nranks, int32_t rank,
+                           const void* unique_id128) {
+  return guarded_c(ctx, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) param_error("comm: invalid rank/nranks");
+    RKMF_CUDA(cudaSetDevice(ctx->device));
+    if (ctx->comm) {
+      ncclCommDestroy(ctx->comm);
+      ctx->comm = nullptr;
+    }
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    if (nranks == 1) return;
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id128, sizeof(id));
+    RKMF_NCCL(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+  });
+}
+
+int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const int64_t* row_starts,
+                                   const int64_t* h_row_ptr_local, const int32_t* h_col_global,
+                                   const double* h_values, rkmf_matrix** out) {
+  return guarded_c(ctx, [&] {
+    RKMF_CUDA(cudaSetDevice(ctx->device));
+    const int P = ctx->nranks, me = ctx->rank;
+    if (P > 1 && !ctx->comm) param_error("partitioned matrix: call rkmf_context_init_comm first");
+    const int64_t rb = row_starts[me], re = row_starts[me + 1];
+    const int64_t n_local = re - rb;
+    if (rb < 0 || re < rb || row_starts[P] != n_global) shape_error("partition: bad row_starts");
+    if (h_row_ptr_local[0] != 0) shape_error("row_ptr[0] != 0");
+    const int64_t nnz = h_row_ptr_local[n_local];
+    // validate the rows in global numbering (sparse.cpp:61-81)
+    for (int64_t r = 0; r < n_local; ++r) {
+      const int64_t lo = h_row_ptr_local[r], hi = h_row_ptr_local[r + 1];
+      if (hi < lo) shape_error("row_ptr not nondecreasing");
+      for (int64_t k = lo; k < hi; ++k) {
+        const int64_t c = h_col_global[k];
+        if (c < 0 || c >= n_global) shape_error("column index out of range");
+        if (k > lo && c <= h_col_global[k - 1])
+          shape_error("columns not strictly increasing within a row");
+        if (!std::isfinite(h_values[k])) numerical_error("non-finite matrix entry");
+      }
+    }
+    int64_t n_halo = 0;
+    rkmf_partition_halo(P, me, row_starts, h_row_ptr_local, h_col_global, &n_halo, nullptr,
+                        nullptr, nullptr);
+    std::vector<int64_t> halo(static_cast<size_t>(n_halo)), recv_cnt(static_cast<size_t>(P));
+    std::vector<int32_t> col_local(static_cast<size_t>(nnz));
+    rkmf_partition_halo(P, me, row_starts, h_row_ptr_local, h_col_global, &n_halo, halo.data(),
+                        recv_cnt.data(), col_local.data());
+    rkmf_matrix* M = create_matrix_host(ctx, n_local, n_local + n_halo, h_row_ptr_local,
+                                        col_local.data(), h_values, false);
+    try {
+      HaloPlan& h = M->halo;
+      M->partitioned = true;
+      h.n_global = n_global;
+      h.row_begin = rb;
+      h.n_local = n_local;
+      h.n_halo = n_halo;
+      h.recv_cnt = recv_cnt;
+      h.recv_off.assign(size_t(P), 0);
+      for (int q = 1; q < P; ++q) h.recv_off[q] = h.recv_off[q - 1] + h.recv_cnt[q - 1];
+      h.send_cnt.assign(size_t(P), 0);
+      h.send_off.assign(size_t(P), 0);
+      cudaStream_t st = ctx->stream;
+      if (P > 1) {
+        // 1) counts: what each rank needs from me
+        DevBuf rc, sc;
+        rc.ensure(sizeof(int64_t) * size_t(P));
+        sc.ensure(sizeof(int64_t) * size_t(P));
+        RKMF_CUDA(cudaMemcpyAsync(rc.p, h.recv_cnt.data(), sizeof(int64_t) * size_t(P),
+                                  cudaMemcpyHostToDevice, st));
+        RKMF_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(int64_t) * size_t(P), st));
+        std::vector<int64_t> one(static_cast<size_t>(P), 1), idx(static_cast<size_t>(P));
+        for (int q = 0; q < P; ++q) idx[q] = q;
+        exchange_i64(ctx, rc.as<int64_t>(), idx, one, sc.as<int64_t>(), idx, one);
+        RKMF_CUDA(cudaMemcpyAsync(h.send_cnt.data(), sc.p, sizeof(int64_t) * size_t(P),
+                                  cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+        h.send_cnt[me] = 0;
+        for (int q = 1; q < P; ++q) h.send_off[q] = h.send_off[q - 1] + h.send_cnt[q - 1];
+        h.send_total = h.send_off[P - 1] + h.send_cnt[P - 1];
+        // 2) index lists: my requests (global ids, grouped by owner) -> owners
+        DevBuf req, got;
+        req.ensure(sizeof(int64_t) * size_t(std::max<int64_t>(n_halo, 1)));
+        got.ensure(sizeof(int64_t) * size_t(std::max<int64_t>(h.send_total, 1)));
+        if (n_halo > 0)
+          RKMF_CUDA(cudaMemcpyAsync(req.p, halo.data(), sizeof(int64_t) * size_t(n_halo),
+                                    cudaMemcpyHostToDevice, st));
+        exchange_i64(ctx, req.as<int64_t>(), h.recv_off, h.recv_cnt, got.as<int64_t>(), h.send_off,
+                     h.send_cnt);
+        std::vector<int64_t> sg(static_cast<size_t>(h.send_total));
+        if (h.send_total > 0)
+          RKMF_CUDA(cudaMemcpyAsync(sg.data(), got.p, sizeof(int64_t) * size_t(h.send_total),
+                                    cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+        std::vector<int32_t> sl(static_cast<size_t>(h.send_total));
+        for (int64_t i = 0; i < h.send_total; ++i) {
+          if (sg[size_t(i)] < rb || sg[size_t(i)] >= re) shape_error("partition: bad halo request");
+          sl[size_t(i)] = int32_t(sg[size_t(i)] - rb);
+        }
+        RKMF_CUDA(cudaMalloc(&h.send_idx, sizeof(int32_t) * size_t(std::max<int64_t>(h.send_total, 1))));
+        RKMF_CUDA(cudaMalloc(&h.sendbuf, sizeof(double) * size_t(std::max<int64_t>(h.send_total, 1))));
+        if (h.send_total > 0)
+          RKMF_CUDA(cudaMemcpyAsync(h.send_idx, sl.data(), sizeof(int32_t) * size_t(h.send_total),
+                                    cudaMemcpyHostToDevice, st));
+        // 3) global norm1 = max column abs-sum (sparse.cpp:97-102): local column
+        //    sums, halo parts returned to their owners, max, allreduce(max)
+        DevBuf cs, back, mx;
+        cs.ensure(sizeof(double) * size_t(n_local + n_halo + 1));
+        back.ensure(sizeof(double) * size_t(std::max<int64_t>(h.send_total, 1)));
+        mx.ensure(sizeof(double));
+        RKMF_CUDA(cudaMemsetAsync(cs.p, 0, sizeof(double) * size_t(n_local + n_halo + 1), st));
+        RKMF_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(double), st));
+        if (nnz > 0)
+          colsum_abs_kernel<<<blocks_for(nnz), 256, 0, st>>>(nnz, M->col, M->val, cs.as<double>());
+        RKMF_NCCL(ncclGroupStart());
+        for (int q = 0; q < P; ++q) {
+          if (q == me) continue;
+          if (h.recv_cnt[q] > 0)
+            RKMF_NCCL(ncclSend(cs.as<double>() + n_local + h.recv_off[q], size_t(h.recv_cnt[q]),
+                               ncclFloat64, q, ctx->comm, st));
+          if (h.send_cnt[q] > 0)
+            RKMF_NCCL(ncclRecv(back.as<double>() + h.send_off[q], size_t(h.send_cnt[q]),
+                               ncclFloat64, q, ctx->comm, st));
+        }
+        RKMF_NCCL(ncclGroupEnd());
+        if (h.send_total > 0)
+          scatter_add_kernel<<<blocks_for(h.send_total), 256, 0, st>>>(h.send_total, h.send_idx,
+                                                                        back.as<double>(),
+                                                                        cs.as<double>());
+        if (n_local > 0)
+          max_abs_kernel<<<blocks_for(n_local), 256, 0, st>>>(n_local, cs.as<double>(),
+                                                              mx.as<double>());
+        RKMF_CUDA(cudaGetLastError());
+        RKMF_NCCL(ncclAllReduce(mx.p, mx.p, 1, ncclFloat64, ncclMax, ctx->comm, st));
+        RKMF_CUDA(cudaMemcpyAsync(&M->norm1, mx.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+        ctx->launches += 3;
+      }
+    } catch (...) {
+      rkmf_matrix_destroy(M);
+      throw;
+    }
+    *out = M;
+  });
+}
+
+}  // extern "C"

@@ -39,121 +39,7 @@ bool pdl_enabled() {  // RKMF_PDL=0 launches the step kernels without PDL
 }
 }  // namespace rkmf_b200
 
-namespace {
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  void* ensure(size_t bytes) {
-    if (bytes <= cap && p) return p;
-    if (p) RKMF_CUDA(cudaFree(p));
-    p = nullptr;
-    cap = 0;
-    RKMF_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
-    cap = std::max<size_t>(bytes, 256);
-    return p;
-  }
-  template <class T>
-  T* as() const { return static_cast<T*>(p); }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-};
-
-int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
-
-}  // namespace
-
-struct rkmf_context {
-  int device = 0;
-  cudaStream_t own_stream = nullptr;
-  cudaStream_t stream = nullptr;
-  std::string last_error;
-  int64_t launches = 0;
-  SolveState* st_dev = nullptr;
-  SolveState* st_host = nullptr;  // pinned
-  DevBuf z, pacc, sacc, W, U, Rbar, Racc, ws, u, g, fhat, ref, partial, qshift, qweight, qpi,
-      qemx, scratch;
-  int64_t racc_ld = 0;
-  std::vector<double> last_R;
-  int64_t last_M = 0;
-  std::vector<cudaEvent_t> events;
-  cudaEvent_t event(size_t i) {
-    while (events.size() <= i) {
-      cudaEvent_t e;
-      RKMF_CUDA(cudaEventCreate(&e));
-      events.push_back(e);
-    }
-    return events[i];
-  }
-  void sync_state() {
-    RKMF_CUDA(cudaMemcpyAsync(st_host, st_dev, sizeof(SolveState), cudaMemcpyDeviceToHost, stream));
-    RKMF_CUDA(cudaStreamSynchronize(stream));
-  }
-  // ---- optional per-kernel-class timing (rkmf_context_kernel_timing) ----
-  bool ktime = false;
-  std::vector<cudaEvent_t> kpool;
-  std::vector<std::pair<int, size_t>> kpend;  // (class, index of the start event)
-  double kms[RKMF_KCLASS_COUNT] = {0};
-  int64_t kcnt[RKMF_KCLASS_COUNT] = {0};
-  template <class F>
-  void timed(int cls, F&& launch) {
-    if (!ktime) { launch(); return; }
-    const size_t i = 2 * kpend.size();
-    while (kpool.size() < i + 2) {
-      cudaEvent_t e;
-      RKMF_CUDA(cudaEventCreate(&e));
-      kpool.push_back(e);
-    }
-    RKMF_CUDA(cudaEventRecord(kpool[i], stream));
-    launch();
-    RKMF_CUDA(cudaEventRecord(kpool[i + 1], stream));
-    kpend.push_back({cls, i});
-  }
-  void collect_ktimes() {  // call after a stream synchronize
-    for (auto& p : kpend) {
-      float ms = 0.f;
-      RKMF_CUDA(cudaEventElapsedTime(&ms, kpool[p.second], kpool[p.second + 1]));
-      kms[p.first] += ms;
-      kcnt[p.first] += 1;
-    }
-    kpend.clear();
-  }
-};
-
-struct rkmf_matrix {
-  rkmf_context* ctx = nullptr;
-  int device = 0;
-  CsrView view{};
-  void* rp = nullptr;
-  int32_t* col = nullptr;
-  double* val = nullptr;
-  double norm1 = 0.0;
-};
-
-struct rkmf_sketch {
-  rkmf_context* ctx = nullptr;
-  int device = 0;
-  int64_t d = 0, n = 0, zeta = 0;
-  uint64_t seed = 0;
-  double scale = 1.0;
-  uint16_t* rows = nullptr;
-  int8_t* signs = nullptr;
-  uint16_t* tile_off = nullptr;
-  uint8_t* tile_ent = nullptr;
-  SketchView view() const {
-    SketchView v;
-    v.d = d;
-    v.n = n;
-    v.zeta = zeta;
-    v.tile_off = tile_off;
-    v.tile_ent = tile_ent;
-    v.scale = scale;
-    return v;
-  }
-};
+#include "engine_types.cuh"
 
 namespace {
 
@@ -183,7 +69,7 @@ int choose_cap(const std::vector<int64_t>& tile_nnz_max) {
 // ---- matrix construction helpers ----
 // Validates the CSR on device (sparse.cpp:61-81) and caches norm1
 // (sparse.cpp:97-102): once per matrix instead of every cycle (basis.cpp:15,118).
-void finish_matrix(rkmf_matrix* M, int64_t max_tile_nnz) {
+void finish_matrix(rkmf_matrix* M, int64_t max_tile_nnz, bool require_sorted) {
   rkmf_context* ctx = M->ctx;
   M->view.cap = choose_cap({max_tile_nnz});
   M->view.row_ptr = M->rp;
@@ -194,7 +80,7 @@ void finish_matrix(rkmf_matrix* M, int64_t max_tile_nnz) {
   double* out = reinterpret_cast<double*>(scr + 16);
   DevBuf colsum;
   colsum.ensure(sizeof(double) * size_t(M->view.n_cols + 1));
-  launch_matrix_check(&M->view, flags, ctx->stream);
+  launch_matrix_check(&M->view, flags, require_sorted, ctx->stream);
   launch_matrix_norm1(&M->view, colsum.as<double>(), out, ctx->stream);
   ctx->launches += 3;
   int32_t hf[2] = {0, 0};
@@ -225,7 +111,7 @@ __global__ void tile_nnz_max_kernel(int64_t n, const int64_t* __restrict__ rp,
 rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
                                      int64_t nnz, const int64_t* rp64_dev,
                                      const int32_t* col_dev, const double* val_dev,
-                                     bool copy_colval) {
+                                     bool copy_colval, bool require_sorted = true) {
   auto* M = new rkmf_matrix();
   M->ctx = ctx;
   M->device = ctx->device;
@@ -275,7 +161,7 @@ rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t 
     RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
     M->view.max_tile_nnz = int64_t(hmx);
     M->view.padded = true;
-    finish_matrix(M, int64_t(hmx));
+    finish_matrix(M, int64_t(hmx), require_sorted);
   } catch (...) {
     if (M->rp) cudaFree(M->rp);
     if (copy_colval && M->col) cudaFree(M->col);
@@ -293,16 +179,20 @@ double host_norm(const double* x, int64_t n) {
 }
 
 struct SolveBuffers {
-  int64_t n, d, m_eff, ldw, ldr;
+  int64_t n, n_global, d, m_eff, ldw, ldr;
   double *W, *U, *Rbar, *z, *pacc, *sacc;
 };
 
-SolveBuffers prepare(rkmf_context* ctx, int64_t n, int64_t d, int64_t m_eff) {
+// n: local rows; n_ext: local rows + halo columns (W columns carry the halo
+// tail the partitioned SpMV reads); n_global: rows of the whole problem.
+SolveBuffers prepare(rkmf_context* ctx, int64_t n, int64_t n_ext, int64_t n_global, int64_t d,
+                     int64_t m_eff) {
   SolveBuffers b;
   b.n = n;
+  b.n_global = n_global;
   b.d = d;
   b.m_eff = m_eff;
-  b.ldw = round_up(std::max<int64_t>(n, 1), 32);
+  b.ldw = round_up(std::max<int64_t>(n_ext, 1), 32);
   b.ldr = m_eff + 1;
   b.W = static_cast<double*>(ctx->W.ensure(sizeof(double) * size_t(b.ldw) * size_t(m_eff + 1)));
   b.U = static_cast<double*>(ctx->U.ensure(sizeof(double) * size_t(d) * size_t(m_eff + 1)));
@@ -318,12 +208,16 @@ SolveBuffers prepare(rkmf_context* ctx, int64_t n, int64_t d, int64_t m_eff) {
 }
 
 void check_builder_args(const rkmf_matrix* A, const rkmf_sketch* S, int64_t m) {
-  // basis.cpp:14-23, 96-101
-  if (A->view.n_rows != A->view.n_cols) shape_error("arnoldi: matrix must be square");
+  // basis.cpp:14-23, 96-101 (dimensions of the global problem when partitioned)
+  const int64_t ng = A->n_rows_global();
+  if (!A->partitioned && A->view.n_rows != A->view.n_cols)
+    shape_error("arnoldi: matrix must be square");
   if (m < 1) param_error("arnoldi: m must be >= 1");
-  if (m > A->view.n_rows) param_error("arnoldi: m exceeds matrix dimension");
-  if (S->n != A->view.n_rows) shape_error("randomized_arnoldi: sketch width mismatch");
-  const int64_t need = (m == A->view.n_rows) ? m : m + 1;
+  if (m > ng) param_error("arnoldi: m exceeds matrix dimension");
+  if (S->n != A->view.n_rows || (A->partitioned && (S->n_global != ng ||
+                                                     S->col_begin != A->halo.row_begin)))
+    shape_error("randomized_arnoldi: sketch width mismatch");
+  const int64_t need = (m == ng) ? m : m + 1;
   if (S->d < need) param_error("randomized_arnoldi: sketch dimension d too small for m");
 }
 
@@ -335,13 +229,16 @@ void run_steps(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
   const int grid = spmv_sketch_grid(&A->view, &sv, 1);
   int32_t* stop = &ctx->st_dev->stopped;
   for (int64_t k = 0; k < b.m_eff; ++k) {
-    const double* x = b.W + k * b.ldw;
+    double* x = b.W + k * b.ldw;
+    comm_halo_exchange(ctx, A, x);  // multi-GPU: off-rank x entries into the halo tail
     ctx->timed(0, [&] {
       launch_spmv_sketch(&A->view, &sv, 1, x, k == 0 ? &ctx->st_dev->sigma : nullptr, b.z,
                          b.pacc, stop, int(k), grid, ctx->stream);
     });
+    comm_allreduce_sum(ctx, b.pacc, size_t(b.d));  // sum of the ranks' sketch partials
     ctx->timed(1, [&] {
-      launch_rgs_step(b.d, int(k), b.ldr, b.n, tol, b.pacc, b.U, b.Rbar, ctx->st_dev, ctx->stream);
+      launch_rgs_step(b.d, int(k), b.ldr, b.n_global, tol, b.pacc, b.U, b.Rbar, ctx->st_dev,
+                      ctx->stream);
     });
     ctx->launches += 2;
     if (!(fuse_last && k == b.m_eff - 1)) {
@@ -360,6 +257,7 @@ void start_sketch(rkmf_context* ctx, const rkmf_sketch* S, const SolveBuffers& b
                        ctx->stream);
   });
   ctx->launches++;
+  comm_allreduce_sum(ctx, b.sacc, size_t(b.d));
 }
 
 void copy_in(rkmf_context* ctx, double* dst, const double* src, int64_t n, bool on_device) {
@@ -406,6 +304,8 @@ int rkmf_context_destroy(rkmf_context* ctx) {
                     &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch})
     b->release();
   for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->kpool) cudaEventDestroy(e);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->st_dev) cudaFree(ctx->st_dev);
   if (ctx->st_host) cudaFreeHost(ctx->st_host);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -459,6 +359,19 @@ int rkmf_matrix_create_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
                             const int64_t* h_rp, const int32_t* h_ci, const double* h_v,
                             rkmf_matrix** out) {
   return guarded(ctx, [&] {
+    *out = rkmf_b200::create_matrix_host(ctx, n_rows, n_cols, h_rp, h_ci, h_v, true);
+  });
+}
+
+}  // extern "C"
+
+rkmf_matrix* rkmf_b200::create_matrix_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
+                                           const int64_t* h_rp, const int32_t* h_ci,
+                                           const double* h_v, bool require_sorted) {
+  rkmf_matrix** out = nullptr;
+  rkmf_matrix* result = nullptr;
+  out = &result;
+  {
     set_device(ctx);
     if (n_rows < 0 || n_cols < 0) shape_error("negative dimension");
     if (h_rp[0] != 0) shape_error("row_ptr[0] != 0");
@@ -481,7 +394,8 @@ int rkmf_matrix_create_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
     }
     rkmf_matrix* M = nullptr;
     try {
-      M = create_from_device_rp64(ctx, n_rows, n_cols, nnz, rp_dev, col, val, false);
+      M = create_from_device_rp64(ctx, n_rows, n_cols, nnz, rp_dev, col, val, false,
+                                  require_sorted);
     } catch (...) {
       cudaFree(rp_dev);
       cudaFree(col);
@@ -491,8 +405,11 @@ int rkmf_matrix_create_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
     RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
     RKMF_CUDA(cudaFree(rp_dev));
     *out = M;
-  });
+  }
+  return result;
 }
+
+extern "C" {
 
 int rkmf_matrix_create_device(rkmf_context* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
                               const int64_t* d_rp, const int32_t* d_ci, const double* d_v,
@@ -509,6 +426,8 @@ int rkmf_matrix_destroy(rkmf_matrix* M) {
   // does not touch M->ctx: a matrix may be released after its context
   // (cudaFree synchronises the device itself)
   cudaSetDevice(M->device);
+  if (M->halo.send_idx) cudaFree(M->halo.send_idx);
+  if (M->halo.sendbuf) cudaFree(M->halo.sendbuf);
   if (M->rp) cudaFree(M->rp);
   if (M->col) cudaFree(M->col);
   if (M->val) cudaFree(M->val);
@@ -528,11 +447,19 @@ int rkmf_matrix_info(const rkmf_matrix* M, int64_t* n_rows, int64_t* n_cols, int
 
 int rkmf_sketch_create(rkmf_context* ctx, int64_t d, int64_t n, int64_t zeta, uint64_t seed,
                        rkmf_sketch** out) {
+  return rkmf_sketch_create_partitioned(ctx, d, n, zeta, seed, 0, n, out);
+}
+
+int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_global, int64_t zeta,
+                                   uint64_t seed, int64_t col_begin, int64_t n,
+                                   rkmf_sketch** out) {
   return guarded(ctx, [&] {
     set_device(ctx);
     if (zeta < 1) param_error("sketch: zeta must be >= 1");  // sketch.cpp:14-16
     if (zeta > d) param_error("sketch: zeta must not exceed d");
-    if (d > n) param_error("sketch: d must not exceed n");
+    if (d > n_global) param_error("sketch: d must not exceed n");
+    if (col_begin < 0 || n < 0 || col_begin + n > n_global)
+      shape_error("sketch: column range outside [0, n)");
     auto* S = new rkmf_sketch();
     S->ctx = ctx;
     S->device = ctx->device;
@@ -540,6 +467,8 @@ int rkmf_sketch_create(rkmf_context* ctx, int64_t d, int64_t n, int64_t zeta, ui
     S->n = n;
     S->zeta = zeta;
     S->seed = seed;
+    S->n_global = n_global;
+    S->col_begin = col_begin;
     S->scale = 1.0 / std::sqrt(double(zeta));  // sketch.cpp:23
     try {
       const int64_t tiles = (n + kTileRows - 1) / kTileRows;
@@ -548,7 +477,7 @@ int rkmf_sketch_create(rkmf_context* ctx, int64_t d, int64_t n, int64_t zeta, ui
       RKMF_CUDA(cudaMalloc(&S->signs, size_t(std::max<int64_t>(n * zeta, 1))));
       RKMF_CUDA(cudaMalloc(&S->tile_off, sizeof(uint16_t) * size_t(std::max<int64_t>(tiles * off_stride, 1))));
       RKMF_CUDA(cudaMalloc(&S->tile_ent, size_t(std::max<int64_t>(tiles * kTileRows * zeta, 16))));
-      launch_sketch_generate(d, n, zeta, seed, S->rows, S->signs, ctx->stream);
+      launch_sketch_generate(d, n, col_begin, zeta, seed, S->rows, S->signs, ctx->stream);
       launch_sketch_tiles(d, n, zeta, S->rows, S->signs, S->tile_off, S->tile_ent, ctx->stream);
       ctx->launches += 2;
       RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -647,7 +576,7 @@ int rkmf_randomized_arnoldi(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_
     check_builder_args(A, S, m);
     const int64_t n = A->view.n_rows;
     if (ldw < n) param_error("randomized_arnoldi: ldw < n");
-    SolveBuffers b = prepare(ctx, n, S->d, m);
+    SolveBuffers b = prepare(ctx, n, A->view.n_cols, A->n_rows_global(), S->d, m);
     copy_in(ctx, b.W, d_b, n, true);
     start_sketch(ctx, S, b);
     launch_start_init_m(b.d, b.sacc, b.U, ctx->st_dev, true, int(m), ctx->stream);
@@ -709,14 +638,14 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       param_error("rkmf_b200: FULL dense f is implemented for exp_neg only");
     if (dense == RKMF_DENSE_QUADRATURE && fn_kind != RKMF_FN_INV_SQRT)
       param_error("rkmf_b200: quadrature restart is implemented for inv_sqrt only");
-    const int64_t n = A->view.n_rows;
-    const int64_t m_eff = std::min(opts.m_r, n);  // restart.cpp:38
+    const int64_t n = A->view.n_rows;  // local rows when partitioned
+    const int64_t m_eff = std::min(opts.m_r, A->n_rows_global());  // restart.cpp:38
     check_builder_args(A, S, m_eff);
     std::memset(res, 0, sizeof(*res));
     ctx->kpend.clear();
 
     cudaStream_t st = ctx->stream;
-    SolveBuffers bb = prepare(ctx, n, S->d, m_eff);
+    SolveBuffers bb = prepare(ctx, n, A->view.n_cols, A->n_rows_global(), S->d, m_eff);
     double* g = static_cast<double*>(ctx->g.ensure(sizeof(double) * size_t(m_eff)));
     double* fhat = f_on_device ? f_out : static_cast<double*>(ctx->fhat.ensure(sizeof(double) * size_t(std::max<int64_t>(n, 1))));
     RKMF_CUDA(cudaMemsetAsync(fhat, 0, sizeof(double) * size_t(n), st));
@@ -735,6 +664,15 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
         copy_in(ctx, rd, reference, n, false);
         ref_dev = rd;
         ref_norm = host_norm(reference, n);
+      }
+      if (ctx->comm && ctx->nranks > 1) {  // global ||reference||
+        double* sc = reinterpret_cast<double*>(static_cast<char*>(ctx->scratch.ensure(64)) + 32);
+        double r2 = ref_norm * ref_norm;
+        RKMF_CUDA(cudaMemcpyAsync(sc, &r2, sizeof(double), cudaMemcpyHostToDevice, st));
+        comm_allreduce_sum(ctx, sc, 1);
+        RKMF_CUDA(cudaMemcpyAsync(&r2, sc, sizeof(double), cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+        ref_norm = std::sqrt(r2);
       }
     }
     copy_in(ctx, bb.W, b_in, n, b_on_device != 0);  // start = b (restart.cpp:45)
@@ -852,6 +790,7 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
                             ctx->st_dev, st);
       });
       ctx->launches++;
+      comm_allreduce_sum(ctx, &ctx->st_dev->yn2, 2);  // global ||y||^2, ||f - ref||^2
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e3), st));
       ctx->sync_state();
       const SolveState& h = *ctx->st_host;
@@ -862,7 +801,8 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       dot_d += mk * (mk + 1) / 2;
       updates += next ? m_eff : mk - 1;
       peak = std::max<long long>(peak, next ? m_eff + 1 : mk);
-      if (h.nonfinite) numerical_error("restart divergence (cycle " + std::to_string(k) + ")");
+      if (h.nonfinite || !std::isfinite(h.yn2))  // restart.cpp:82-83
+        numerical_error("restart divergence (cycle " + std::to_string(k) + ")");
       const double yn = std::sqrt(h.yn2);
       rkmf_cycle_record rec;
       rec.cycle = k;

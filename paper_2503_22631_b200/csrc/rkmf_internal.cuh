@@ -78,15 +78,16 @@ struct SolveState {
   double sigma;        // 1 / alpha_k (folded into column 0)
   double alpha1;       // cycle-1 start norm (global scale)
   double coupling;     // previous cycle's subdiagonal r_{m+1,m}
-  double yn2;          // ||y_k||^2 accumulator
+  double yn2;          // ||y_k||^2 accumulator        } adjacent: one allreduce
+  double err2;         // ||f_hat - reference||^2      }   of 2 doubles (multi-GPU)
   double rnorm1;       // ||R_accum||_1 (full dense-f path)
-  double err2;         // ||f_hat - reference||^2
 };
 
 // ---- kernels (definitions in *.cu) ----
 // sketch.cu
-void launch_sketch_generate(int64_t d, int64_t n, int64_t zeta, uint64_t seed, uint16_t* rows,
-                            int8_t* signs, cudaStream_t st);
+// columns [j0, j0 + n) of the global operator (j0 = 0 for a whole sketch)
+void launch_sketch_generate(int64_t d, int64_t n, int64_t j0, int64_t zeta, uint64_t seed,
+                            uint16_t* rows, int8_t* signs, cudaStream_t st);
 void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
                          const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
                          cudaStream_t st);
@@ -124,7 +125,7 @@ bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double
                              const double* xscale_dev, double* z, double* pacc,
                              const int32_t* stop_flag, int step, cudaStream_t st);
 void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st);
-void launch_matrix_check(const CsrView* A, int32_t* flags, cudaStream_t st);
+void launch_matrix_check(const CsrView* A, int32_t* flags, bool require_sorted, cudaStream_t st);
 
 // krylov.cu
 void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev, bool first,

@@ -41,12 +41,12 @@ __device__ __forceinline__ uint64_t sm64_derive(uint64_t seed, uint64_t tag) {  
 // limits[i - (d - zeta)] = bound * (UINT64_MAX / bound) for bound = i + 1
 // (rng.hpp:35), precomputed on the host: the 64-bit division runs once per
 // distinct bound instead of once per draw.
-__global__ void sketch_generate_kernel(int64_t d, int64_t n, int zeta, uint64_t seed,
+__global__ void sketch_generate_kernel(int64_t d, int64_t n, int64_t j0, int zeta, uint64_t seed,
                                        const uint64_t* __restrict__ limits,
                                        uint16_t* __restrict__ rows, int8_t* __restrict__ signs) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  uint64_t s = sm64_derive(seed, uint64_t(j));
+  uint64_t s = sm64_derive(seed, uint64_t(j0 + j));  // global column j0 + j
   uint16_t chosen[kMaxZeta];
   int cnt = 0;
   for (int64_t i = d - zeta; i < d; ++i) {  // Floyd: sketch.cpp:33-40
@@ -142,7 +142,8 @@ __global__ void sketch_export_kernel(int64_t count, const uint16_t* __restrict__
 
 }  // namespace
 
-void launch_sketch_generate(int64_t d, int64_t n, int64_t zeta, uint64_t seed, uint16_t* rows,
+void launch_sketch_generate(int64_t d, int64_t n, int64_t j0, int64_t zeta, uint64_t seed,
+                            uint16_t* rows,
                             int8_t* signs, cudaStream_t st) {
   if (zeta > kMaxZeta) param_error("sketch: zeta > 64 is not supported on device");
   if (d > 65535) param_error("sketch: d > 65535 is not supported on device");
@@ -157,7 +158,7 @@ void launch_sketch_generate(int64_t d, int64_t n, int64_t zeta, uint64_t seed, u
                             cudaMemcpyHostToDevice, st));
   const int threads = 128;
   const int64_t blocks = (n + threads - 1) / threads;
-  sketch_generate_kernel<<<unsigned(blocks), threads, 0, st>>>(d, n, int(zeta), seed, dl, rows,
+  sketch_generate_kernel<<<unsigned(blocks), threads, 0, st>>>(d, n, j0, int(zeta), seed, dl, rows,
                                                                signs);
   RKMF_CUDA(cudaGetLastError());
   RKMF_CUDA(cudaFreeAsync(dl, st));

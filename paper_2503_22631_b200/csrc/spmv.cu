@@ -238,14 +238,14 @@ __global__ void max_kernel(int64_t n, const double* __restrict__ v, double* out)
 template <typename RP>
 __global__ void check_kernel(int64_t n_rows, int64_t n_cols, const RP* __restrict__ rp,
                              const int32_t* __restrict__ ci, const double* __restrict__ val,
-                             int32_t* flags) {
+                             int32_t* flags, int sorted) {
   for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
        r += int64_t(gridDim.x) * blockDim.x) {
     const int64_t lo = rp[r], hi = rp[r + 1];
     if (hi < lo) { flags[0] = 1; continue; }
     for (int64_t k = lo; k < hi; ++k) {
       const int64_t c = ci[k];
-      if (c < 0 || c >= n_cols || (k > lo && c <= ci[k - 1])) flags[0] = 1;
+      if (c < 0 || c >= n_cols || (sorted && k > lo && c <= ci[k - 1])) flags[0] = 1;
       if (!isfinite(val[k])) flags[1] = 1;
     }
   }
@@ -262,18 +262,18 @@ void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStre
   RKMF_CUDA(cudaGetLastError());
 }
 
-void launch_matrix_check(const CsrView* A, int32_t* flags, cudaStream_t st) {
+void launch_matrix_check(const CsrView* A, int32_t* flags, bool require_sorted, cudaStream_t st) {
   RKMF_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), st));
   const int g = 4 * num_sms();
   if (A->n_rows == 0) return;
   if (A->rp64)
     check_kernel<int64_t><<<g, 256, 0, st>>>(A->n_rows, A->n_cols,
                                              static_cast<const int64_t*>(A->row_ptr), A->col,
-                                             A->val, flags);
+                                             A->val, flags, require_sorted ? 1 : 0);
   else
     check_kernel<int32_t><<<g, 256, 0, st>>>(A->n_rows, A->n_cols,
                                              static_cast<const int32_t*>(A->row_ptr), A->col,
-                                             A->val, flags);
+                                             A->val, flags, require_sorted ? 1 : 0);
   RKMF_CUDA(cudaGetLastError());
 }
 
