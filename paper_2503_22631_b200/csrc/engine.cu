@@ -472,7 +472,7 @@ int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_globa
     S->scale = 1.0 / std::sqrt(double(zeta));  // sketch.cpp:23
     try {
       const int64_t tiles = (n + kTileRows - 1) / kTileRows;
-      const int64_t off_stride = (d + 1 + 7) / 8 * 8;
+      const int64_t off_stride = tile_off_stride(d);
       RKMF_CUDA(cudaMalloc(&S->rows, sizeof(uint16_t) * size_t(std::max<int64_t>(n * zeta, 1))));
       RKMF_CUDA(cudaMalloc(&S->signs, size_t(std::max<int64_t>(n * zeta, 1))));
       RKMF_CUDA(cudaMalloc(&S->tile_off, sizeof(uint16_t) * size_t(std::max<int64_t>(tiles * off_stride, 1))));

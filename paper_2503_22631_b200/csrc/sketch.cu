@@ -9,11 +9,13 @@
 // Two device layouts are produced:
 //   rows/signs  [n][zeta]  uint16 / int8   the operator itself (export, tests)
 //   tile layout            per 128-column tile, the d x 128 block of S in CSR
-//                          by sketch row ("bin"): tile_off[tile][d+1] uint16
-//                          offsets and tile_ent[tile][128*zeta] uint8 entries
-//                          (local column | sign << 7), entries of a bin sorted
-//                          by local column. This is what the fused SpMV epilogue
-//                          reads: each thread owns a bin and gathers its ~zeta*128/d
+//                          by sketch row ("bin"), bins renumbered into slots by
+//                          length: tile_off[tile][tile_off_stride(d)] uint16 =
+//                          slot offsets [d+1] + slot bins [d], and
+//                          tile_ent[tile][128*zeta] uint8 entries (local column |
+//                          sign << 7), entries of a bin sorted by local column.
+//                          This is what the fused SpMV epilogue reads: each
+//                          thread owns slots and gathers their ~zeta*128/d
 //                          contributions from shared memory, so the scatter-add of
 //                          sketch.cpp:55-61 becomes a deterministic gather with no
 //                          shared-memory atomics (fp64 smem atomics are CAS loops
@@ -73,17 +75,23 @@ __global__ void sketch_generate_kernel(int64_t d, int64_t n, int64_t j0, int zet
 }
 
 // One block per 128-column tile: counting sort of the tile's n_tile*zeta
-// entries by sketch row, then a per-bin insertion sort by local column so the
-// layout (and hence every sketch sum) is deterministic.
+// entries by sketch row ("bin"), a per-bin insertion sort by local column so
+// the layout (and hence every sketch sum) is deterministic, then the bins are
+// renumbered into "slots" ordered by entry count (descending, ties by bin id).
+// Consumers hand slots to threads in snake order (sketch_tile_gather), so the
+// 32 bins a warp walks have near-equal lengths and the gather loop does not
+// diverge. Output per tile (see tile_off_stride): off[slot 0..d] uint16
+// offsets, bin[slot 0..d-1] uint16 sketch rows, and the entries in slot order.
 __global__ void sketch_tiles_kernel(int64_t d, int64_t n, int zeta, int64_t off_stride,
                                     const uint16_t* __restrict__ rows,
                                     const int8_t* __restrict__ signs,
                                     uint16_t* __restrict__ tile_off,
                                     uint8_t* __restrict__ tile_ent) {
   extern __shared__ int sh[];
-  int* cnt = sh;                   // d + 1
-  int* cur = sh + (d + 1);         // d
-  uint8_t* ent = reinterpret_cast<uint8_t*>(cur + d);  // kTileRows * zeta
+  int* cnt = sh;                   // d + 1: bin offsets
+  int* cur = sh + (d + 1);         // d: insertion cursors, then slot of each bin
+  int* soff = cur + d;             // d + 1: slot offsets
+  uint8_t* ent = reinterpret_cast<uint8_t*>(soff + d + 1);  // kTileRows * zeta
   __shared__ int chunk_sum[kBlock];
   const int64_t tile = blockIdx.x;
   const int t = threadIdx.x;
@@ -126,12 +134,37 @@ __global__ void sketch_tiles_kernel(int64_t d, int64_t n, int zeta, int64_t off_
       ent[q + 1] = key;
     }
   }
+  // slot of bin b = #bins that are longer, or as long with a smaller id
+  for (int64_t b = t; b < d; b += blockDim.x) {
+    const int cb = cnt[b + 1] - cnt[b];
+    int rank = 0;
+    for (int64_t q = 0; q < d; ++q) {
+      const int cq = cnt[q + 1] - cnt[q];
+      rank += (cq > cb) || (cq == cb && q < b);
+    }
+    cur[b] = rank;
+  }
   __syncthreads();
   uint16_t* toff = tile_off + tile * off_stride;
-  for (int64_t b = t; b <= d; b += blockDim.x) toff[b] = uint16_t(cnt[b]);
+  for (int64_t b = t; b < d; b += blockDim.x) {
+    soff[cur[b] + 1] = cnt[b + 1] - cnt[b];
+    toff[d + 1 + cur[b]] = uint16_t(b);
+  }
+  __syncthreads();
+  if (t == 0) {
+    soff[0] = 0;
+    for (int64_t q = 1; q <= d; ++q) soff[q] += soff[q - 1];
+  }
+  __syncthreads();
+  for (int64_t q = t; q <= d; q += blockDim.x) toff[q] = uint16_t(soff[q]);
+  for (int64_t q = 2 * d + 1 + t; q < off_stride; q += blockDim.x) toff[q] = 0;
   uint8_t* tent = tile_ent + tile * int64_t(kTileRows) * zeta;
   const int total = cnt[d];
-  for (int e = t; e < kTileRows * zeta; e += blockDim.x) tent[e] = e < total ? ent[e] : 0;
+  for (int64_t b = t; b < d; b += blockDim.x) {
+    const int src = cnt[b], c = cnt[b + 1] - cnt[b], dst = soff[cur[b]];
+    for (int e = 0; e < c; ++e) tent[dst + e] = ent[src + e];
+  }
+  for (int e = total + t; e < kTileRows * zeta; e += blockDim.x) tent[e] = 0;
 }
 
 __global__ void sketch_export_kernel(int64_t count, const uint16_t* __restrict__ rows,
@@ -168,8 +201,8 @@ void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* row
                          const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
                          cudaStream_t st) {
   const int64_t tiles = (n + kTileRows - 1) / kTileRows;
-  const int64_t off_stride = (d + 1 + 7) / 8 * 8;
-  const size_t smem = sizeof(int) * size_t(2 * d + 1) + size_t(kTileRows * zeta) + 16;
+  const int64_t off_stride = tile_off_stride(d);
+  const size_t smem = sizeof(int) * size_t(3 * d + 2) + size_t(kTileRows * zeta) + 16;
   if (smem > 200 * 1024) param_error("sketch: d too large for the device tile layout");
   if (smem > 48 * 1024)
     RKMF_CUDA(cudaFuncSetAttribute(sketch_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -12,9 +12,10 @@
 //    fully coalesced loads into shared memory as products val*x[col] (chunks
 //    of `cap` products for long rows), then thread t reduces row t from shared
 //    memory in column order — the reference's row-sequential order.
-//  * Sketch epilogue: z_t*scale goes to shared memory; each thread owns sketch
-//    rows ("bins") b = t, t+128, ... and gathers the tile's contributions from
-//    the per-tile transposed layout (see sketch.cu). No atomics except one
+//  * Sketch epilogue: z_t*scale goes to shared memory; each thread owns a
+//    length-balanced set of sketch rows ("bins") and gathers the tile's
+//    contributions from the per-tile transposed layout (sketch_tile_gather,
+//    sketch.cu). No atomics except one
 //    fp64 RED per bin per block at kernel end.
 #include <cuda_runtime.h>
 
@@ -94,16 +95,7 @@ __global__ void __launch_bounds__(kBlock)
       uint4* se = reinterpret_cast<uint4*>(ent);
       for (int q = t; q < 8 * zeta; q += kBlock) se[q] = __ldcs(ge + q);
       __syncthreads();
-      for (int b = t; b < d; b += kBlock) {
-        const int e0 = off[b], e1 = off[b + 1];
-        double s = 0.0;
-        for (int e = e0; e < e1; ++e) {
-          const unsigned u = ent[e];
-          const double v = zs[u & 0x7f];
-          s += (u & 0x80) ? -v : v;
-        }
-        acc[b] += s;
-      }
+      sketch_tile_gather(t, d, off, ent, zs, acc);
       __syncthreads();
     }
   }
@@ -163,7 +155,7 @@ int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode) {
   const int64_t tiles = (n + kTileRows - 1) / kTileRows;
   const int cap = A ? A->cap : 0;
   const int64_t d = S ? S->d : 0, zeta = S ? S->zeta : 0;
-  const int64_t off_stride = S ? (d + 1 + 7) / 8 * 8 : 0;
+  const int64_t off_stride = S ? tile_off_stride(d) : 0;
   const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
   void* fn = pick(A ? A->rp64 : false, mode);
   if (smem > 48 * 1024)
@@ -182,7 +174,7 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
   const int64_t tiles = (n + kTileRows - 1) / kTileRows;
   const int cap = A ? A->cap : 0;
   const int d = S ? int(S->d) : 0, zeta = S ? int(S->zeta) : 0;
-  const int64_t off_stride = S ? (S->d + 1 + 7) / 8 * 8 : 0;
+  const int64_t off_stride = S ? tile_off_stride(S->d) : 0;
   const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
   if (mode == 1 && A && S && use_pipe() &&
       launch_spmv_sketch_pipe(A, S, x, xscale_dev, z, pacc, stop_flag, step, st))

@@ -30,6 +30,9 @@ namespace {
 constexpr int kConsumers = 128;  // = kTileRows, one row per consumer thread
 constexpr int kPipeThreads = kConsumers + 32;
 constexpr int kStages = 4;
+// try_wait may suspend the warp until the phase completes or this many ns
+// pass: fewer re-polls, so the spinning warps stop eating issue slots.
+constexpr uint32_t kSuspendHintNs = 20000;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -49,9 +52,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra LAB_WAIT;\n}\n" ::"r"(su32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(kSuspendHintNs)
       : "memory");
 }
 // Streamed operands (values, columns, sketch metadata) are read exactly once
@@ -147,15 +150,16 @@ __global__ void __launch_bounds__(kPipeThreads)
       nrs = (long long)rp[r0];
       nre = (long long)rp[min(n, r0 + kTileRows)];
     }
+    int s = 0;
+    uint32_t eph = 0;  // parity of the empty barrier round being waited for
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int s = it % nstages;
       const long long rs = nrs, re = nre;
       const int64_t nt = tile + gridDim.x;
       if (nt < num_tiles) {
         nrs = (long long)rp[nt * kTileRows];
         nre = (long long)rp[min(n, nt * kTileRows + kTileRows)];
       }
-      if (it >= nstages) mbar_wait(&empty[s], ((it / nstages) - 1) & 1);
+      if (it >= nstages) mbar_wait(&empty[s], eph);
       unsigned char* st = smem + s * L.stride;
       const int64_t r0 = tile * kTileRows;
       const long long vs0 = rs & ~1LL, cs0 = rs & ~3LL;
@@ -177,57 +181,59 @@ __global__ void __launch_bounds__(kPipeThreads)
       }
       bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], pol);
       bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], pol);
+      if (++s == nstages) {
+        s = 0;
+        if (it >= nstages) eph ^= 1u;  // rounds 1, 2, ... of each stage
+      }
     }
     return;
   }
 
   // ---------------- consumer warps: one row per thread ----------------
   const double xs = xscale ? *xscale : 1.0;
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-    const int s = it % nstages;
-    mbar_wait(&full[s], (it / nstages) & 1);
+  int s = 0;
+  uint32_t fph = 0;  // parity of the full barrier round being waited for
+  for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    mbar_wait(&full[s], fph);
     unsigned char* st = smem + s * L.stride;
     const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
-    const double* vals = reinterpret_cast<const double*>(st + L.val);
-    const int32_t* cols = reinterpret_cast<const int32_t*>(st + L.col);
     const uint16_t* off = reinterpret_cast<const uint16_t*>(st + L.off);
     const uint8_t* ent = st + L.ent;
     double* zs = reinterpret_cast<double*>(st + L.zs);
     const TileMeta meta = *reinterpret_cast<const TileMeta*>(st + L.meta);
+    const double* vals = reinterpret_cast<const double*>(st + L.val) + meta.vshift;
+    const int32_t* cols = reinterpret_cast<const int32_t*>(st + L.col) + meta.cshift;
     const int64_t row = tile * kTileRows + t;
     double sum = 0.0;
     if (row < n) {
       const int lo = int((long long)rps[t] - meta.rs), hi = int((long long)rps[t + 1] - meta.rs);
+      // 8 gathers in flight per thread, issued before the first FMA. Lanes
+      // past the row end re-read the row's last column (always a valid index,
+      // and one the row already uses) and contribute a zero product.
       for (int e = lo; e < hi; e += 8) {
         double v[8], xv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const bool ok = e + q < hi;
-          v[q] = ok ? vals[meta.vshift + e + q] : 0.0;
-          xv[q] = ok ? __ldg(x + cols[meta.cshift + e + q]) : 0.0;
+          const int ee = min(e + q, hi - 1);
+          v[q] = vals[ee];
+          xv[q] = __ldg(x + cols[ee]);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (e + q < hi) sum += v[q] * xv[q];
+        for (int q = 0; q < 8; ++q) sum += (e + q < hi ? v[q] : 0.0) * xv[q];
       }
       sum *= xs;
       z[row] = sum;
     }
     zs[t] = row < n ? sum * sscale : 0.0;
     named_sync();
-    for (int b = t; b < d; b += kConsumers) {
-      const int e0 = off[b], e1 = off[b + 1];
-      double a = 0.0;
-      for (int e = e0; e < e1; ++e) {
-        const unsigned u = ent[e];
-        const double w = zs[u & 0x7f];
-        a += (u & 0x80) ? -w : w;
-      }
-      acc[b] += a;
-    }
+    sketch_tile_gather(t, d, off, ent, zs, acc);
     mbar_arrive(&empty[s]);
+    if (++s == nstages) {
+      s = 0;
+      fph ^= 1u;
+    }
   }
+  named_sync();  // acc[b] may have been written by another consumer thread
   for (int b = t; b < d; b += kConsumers) atomicAdd(pacc + b, acc[b]);
 }
 
@@ -271,7 +277,7 @@ template <typename RP>
 bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
                    int step, cudaStream_t st) {
-  const int off_stride = int((S->d + 1 + 7) / 8 * 8);
+  const int off_stride = int(tile_off_stride(S->d));
   auto fn = spmv_sketch_pipe_kernel<RP>;
   // Pick the stage count that maximises consumer warps per SM while keeping
   // at least one tile in flight ahead of the consumers (cached per shape).
