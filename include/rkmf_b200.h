@@ -152,6 +152,11 @@ int rkmf_sketch_apply(rkmf_context* ctx, const rkmf_sketch* S, const double* d_x
 /* z = A x and p = S z in one pass (the fused K2 kernel) */
 int rkmf_spmv_sketch(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
                      const double* d_x, double* d_z, double* d_p);
+/* Measurement only: average device time of `reps` back-to-back launches of the
+ * step kernel on the context stream (CUDA events), mode 1 = fused SpMV+sketch
+ * (K2), 0 = SpMV alone, 2 = sketch of x alone. pacc accumulates over the reps. */
+int rkmf_kernel_bench(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S, int32_t mode,
+                      const double* d_x, double* d_z, double* d_p, int32_t reps, double* avg_ms);
 
 /* ---- one randomized Arnoldi decomposition: basis.cpp:92-142 ----
  * d_W: n x (m+1) column-major with leading dimension ldw >= n (device);

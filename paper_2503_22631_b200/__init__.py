@@ -113,6 +113,7 @@ SYMBOLS = [
     ("rkmf_spmv", C.c_int, [_P, _P, _P, _P]),
     ("rkmf_sketch_apply", C.c_int, [_P, _P, _P, _P]),
     ("rkmf_spmv_sketch", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("rkmf_kernel_bench", C.c_int, [_P, _P, _P, _I32, _P, _P, _P, _I32, _P]),
     ("rkmf_randomized_arnoldi", C.c_int,
      [_P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     ("rkmf_restarted_krylov", C.c_int,
@@ -356,6 +357,21 @@ def spmv_sketch(A: SparseMatrix, S: SketchOperator, x):
     A.ctx.check(lib().rkmf_spmv_sketch(A.ctx.h, A.h, S.h, xd.data_ptr(), z.data_ptr(),
                                        p.data_ptr()))
     return z, p
+
+
+def kernel_bench(A: SparseMatrix, S: Optional[SketchOperator], x, mode: int = 1,
+                 reps: int = 50) -> float:
+    """Average device ms of one step-kernel launch (measurement only): mode 1 =
+    fused SpMV+sketch (K2), 0 = SpMV alone, 2 = sketch of x alone."""
+    import torch
+    xd = _dev(x, A.ctx)
+    z = torch.empty(A.n_rows, dtype=torch.float64, device=xd.device)
+    p = torch.empty(S.d if S is not None else 1, dtype=torch.float64, device=xd.device)
+    ms = C.c_double()
+    A.ctx.check(lib().rkmf_kernel_bench(A.ctx.h, A.h, S.h if S is not None else None, mode,
+                                        xd.data_ptr(), z.data_ptr(), p.data_ptr(), reps,
+                                        C.byref(ms)))
+    return ms.value
 
 
 @dataclass

@@ -567,6 +567,34 @@ int rkmf_spmv_sketch(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch*
   });
 }
 
+int rkmf_kernel_bench(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S, int32_t mode,
+                      const double* d_x, double* d_z, double* d_p, int32_t reps, double* avg_ms) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    if (mode < 0 || mode > 2 || reps < 1) param_error("kernel_bench: bad mode or reps");
+    if (mode != 0 && (!S || S->n != A->view.n_rows))
+      shape_error("kernel_bench: sketch width mismatch");
+    SketchView sv{};
+    if (S) sv = S->view();
+    const SketchView* svp = mode == 0 ? nullptr : &sv;
+    const int grid = spmv_sketch_grid(mode == 2 ? nullptr : &A->view, svp, mode);
+    if (mode != 0) RKMF_CUDA(cudaMemsetAsync(d_p, 0, sizeof(double) * size_t(S->d), ctx->stream));
+    auto launch = [&] {
+      launch_spmv_sketch(mode == 2 ? nullptr : &A->view, svp, mode, d_x, nullptr, d_z, d_p,
+                         nullptr, 0, grid, ctx->stream);
+    };
+    launch();  // warm-up
+    RKMF_CUDA(cudaEventRecord(ctx->event(0), ctx->stream));
+    for (int i = 0; i < reps; ++i) launch();
+    RKMF_CUDA(cudaEventRecord(ctx->event(1), ctx->stream));
+    RKMF_CUDA(cudaEventSynchronize(ctx->event(1)));
+    float ms = 0.f;
+    RKMF_CUDA(cudaEventElapsedTime(&ms, ctx->event(0), ctx->event(1)));
+    *avg_ms = double(ms) / reps;
+    ctx->launches += reps + 1;
+  });
+}
+
 int rkmf_randomized_arnoldi(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
                             const double* d_b, int64_t m, double* d_W, int64_t ldw, double* d_U,
                             double* h_Rbar, double* start_norm, int64_t* mk,

@@ -119,21 +119,17 @@ struct SketchView {
 // sketch row of each slot), padded to 16 bytes.
 __host__ __device__ inline int64_t tile_off_stride(int64_t d) { return (2 * d + 1 + 7) / 8 * 8; }
 
-// v with its sign flipped when bit 7 of the entry byte u is set
-__device__ __forceinline__ double with_sign(double v, unsigned u) {
-  const unsigned long long m = static_cast<unsigned long long>(u & 0x80u) << 56;
-  return __longlong_as_double(static_cast<long long>(
-      static_cast<unsigned long long>(__double_as_longlong(v)) ^ m));
-}
-
 // Sketch epilogue of one 128-row tile (sketch.cpp:51-63 as a gather): thread t
 // of 128 sums the tile's contributions to the slots it owns and adds them to
 // acc[bin]. Slots are sorted by length, and thread t takes slots t, 255-t,
 // 256+t, 511-t, ... (snake), so each warp walks 32 slots of near-equal length
-// and every thread gets about the same number of entries. zs[r] holds the
-// scaled z of local row r; an entry is (local row | sign << 7).
+// and every thread gets about the same number of entries. zs2 holds the scaled
+// z of the tile's rows twice, zs2[r] = +z_r and zs2[128 + r] = -z_r, so an
+// entry byte (local row | sign << 7) indexes its signed value directly. Reading
+// one entry past a slot's end stays inside shared memory (the stage layouts
+// place zs2 after the entries) and is masked.
 __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t* off,
-                                                   const uint8_t* ent, const double* zs,
+                                                   const uint8_t* ent, const double* zs2,
                                                    double* acc) {
   const uint16_t* bins = off + d + 1;
   for (int j = 0; 128 * j < d; ++j) {
@@ -141,17 +137,12 @@ __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t*
     if (s >= d) continue;
     const int e0 = off[s], e1 = off[s + 1];
     double a0 = 0.0, a1 = 0.0;
-    int e = e0;
-    for (; e + 1 < e1; e += 2) {
-      const unsigned u0 = ent[e], u1 = ent[e + 1];
-      const double v0 = zs[u0 & 0x7fu], v1 = zs[u1 & 0x7fu];
-      a0 += with_sign(v0, u0);
-      a1 += with_sign(v1, u1);
-    }
-    if (e < e1) {
-      const unsigned u0 = ent[e];
-      const double v0 = zs[u0 & 0x7fu];
-      a0 += with_sign(v0, u0);
+#pragma unroll 1
+    for (int e = e0; e < e1; e += 2) {
+      const double v0 = zs2[ent[e]];
+      const double v1 = zs2[ent[e + 1]];
+      a0 += v0;
+      a1 += e + 1 < e1 ? v1 : 0.0;
     }
     acc[bins[s]] += a0 + a1;
   }

@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(kBlock)
   constexpr bool kSpmv = MODE <= 1;
   constexpr bool kSketch = MODE >= 1;
   double* acc = reinterpret_cast<double*>(smem_raw);       // [d rounded up to even]
-  double* zs = acc + (kSketch ? (d + 1) / 2 * 2 : 0);      // [128], 16-byte aligned
-  double* prod = zs + (kSketch ? kTileRows : 0);           // [cap]
+  double* zs = acc + (kSketch ? (d + 1) / 2 * 2 : 0);      // [2*128] (+z, -z), 16-byte aligned
+  double* prod = zs + (kSketch ? 2 * kTileRows : 0);       // [cap]
   uint16_t* off = reinterpret_cast<uint16_t*>(prod + (kSpmv ? cap : 0));  // [off_stride]
   uint8_t* ent = reinterpret_cast<uint8_t*>(off + (kSketch ? off_stride : 0));  // [128*zeta]
 
@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kBlock)
     }
     if (kSketch) {
       zs[t] = live ? zrow * sscale : 0.0;
+      zs[kTileRows + t] = -zs[t];
       const uint16_t* go = toff + tile * off_stride;
       for (int q = t; q < off_stride; q += kBlock) off[q] = go[q];
       const uint4* ge = reinterpret_cast<const uint4*>(tent + tile * int64_t(kTileRows) * zeta);
@@ -105,9 +106,9 @@ __global__ void __launch_bounds__(kBlock)
 
 size_t smem_bytes(int mode, int cap, int64_t d, int64_t zeta, int64_t off_stride) {
   size_t s = 0;
-  if (mode >= 1) s += sizeof(double) * size_t((d + 1) / 2 * 2 + kTileRows);
+  if (mode >= 1) s += sizeof(double) * size_t((d + 1) / 2 * 2 + 2 * kTileRows);
   if (mode <= 1) s += sizeof(double) * size_t(cap);
-  if (mode >= 1) s += sizeof(uint16_t) * size_t(off_stride) + size_t(kTileRows * zeta);
+  if (mode >= 1) s += sizeof(uint16_t) * size_t(off_stride) + size_t(kTileRows * zeta) + 16;
   return (s + 15) / 16 * 16;
 }
 

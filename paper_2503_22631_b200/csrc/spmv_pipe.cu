@@ -60,10 +60,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Streamed operands (values, columns, sketch metadata) are read exactly once
 // per step: copy them with an L2 evict-first policy so they do not evict the
 // x vector being gathered or the z vector the basis update reads next.
-__device__ __forceinline__ uint64_t l2_policy(int evict_first) {
+// kind: 0 evict_normal, 1 evict_first, 2 evict_last
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
   uint64_t pol;
-  if (evict_first)
+  if (kind == 1)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   else
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
   return pol;
@@ -99,8 +102,8 @@ __host__ __device__ inline StageLayout stage_layout(int rp_bytes, int cap, int o
   o += r16(uint32_t(off_stride) * 2u);
   L.ent = o;
   o += r16(uint32_t(kTileRows * zeta));
-  L.zs = o;
-  o += kTileRows * 8u;
+  L.zs = o;  // zs2: +z then -z of the tile's rows (sketch_tile_gather)
+  o += 2 * kTileRows * 8u;
   L.meta = o;
   o += 16u;
   L.stride = (o + 127u) & ~127u;
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(kPipeThreads)
                             int cap, int d, int zeta, int off_stride,
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
                             double sscale, double* pacc, const int32_t* stop, int step,
-                            int nstages, int evict_first) {
+                            int nstages, int l2_hints, int debug) {
   extern __shared__ __align__(128) unsigned char smem[];
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -140,7 +143,9 @@ __global__ void __launch_bounds__(kPipeThreads)
 
   if (t >= kConsumers) {  // ---------------- producer warp ----------------
     if (t != kConsumers) return;
-    const uint64_t pol = l2_policy(evict_first);
+    const uint64_t pol = l2_policy(l2_hints >= 1 ? 1 : 0);
+    // the sketch tile layout is re-read every step: ask L2 to keep it
+    const uint64_t mpol = l2_policy(l2_hints);
     int it = 0;
     // row-pointer pair of the next tile, prefetched one iteration ahead so the
     // bulk copies of a tile are issued without a dependent global round trip
@@ -179,8 +184,8 @@ __global__ void __launch_bounds__(kPipeThreads)
         bulk_g2s(st + L.val, val + vs0, vbytes, &full[s], pol);
         bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s], pol);
       }
-      bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], pol);
-      bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], pol);
+      bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], mpol);
+      bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], mpol);
       if (++s == nstages) {
         s = 0;
         if (it >= nstages) eph ^= 1u;  // rounds 1, 2, ... of each stage
@@ -190,49 +195,82 @@ __global__ void __launch_bounds__(kPipeThreads)
   }
 
   // ---------------- consumer warps: one row per thread ----------------
+  // Software-pipelined by one tile: the x gathers of tile i are issued, then
+  // the sketch gather of tile i-1 runs from shared memory while they are in
+  // flight, then tile i's row sums finish. The consumers therefore hold two
+  // stages (i-1 until its sketch is gathered, and i).
   const double xs = xscale ? *xscale : 1.0;
-  int s = 0;
-  uint32_t fph = 0;  // parity of the full barrier round being waited for
+  int s = 0, ps = -1;  // current stage; stage of the tile whose sketch is pending
+  uint32_t fph = 0;    // parity of the full barrier round being waited for
+  auto gather_prev = [&] {
+    if (ps < 0) return;
+    unsigned char* pst = smem + ps * L.stride;
+    if (!(debug & 1))
+      sketch_tile_gather(t, d, reinterpret_cast<const uint16_t*>(pst + L.off), pst + L.ent,
+                         reinterpret_cast<const double*>(pst + L.zs), acc);
+    mbar_arrive(&empty[ps]);
+  };
   for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
     mbar_wait(&full[s], fph);
     unsigned char* st = smem + s * L.stride;
+    if (debug & 4) {  // ablation: stream only
+      mbar_arrive(&empty[s]);
+      if (++s == nstages) { s = 0; fph ^= 1u; }
+      continue;
+    }
     const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
-    const uint16_t* off = reinterpret_cast<const uint16_t*>(st + L.off);
-    const uint8_t* ent = st + L.ent;
     double* zs = reinterpret_cast<double*>(st + L.zs);
     const TileMeta meta = *reinterpret_cast<const TileMeta*>(st + L.meta);
     const double* vals = reinterpret_cast<const double*>(st + L.val) + meta.vshift;
     const int32_t* cols = reinterpret_cast<const int32_t*>(st + L.col) + meta.cshift;
     const int64_t row = tile * kTileRows + t;
+    const bool live = row < n;
+    int lo = 0, hi = 0;
+    if (live) {
+      lo = int((long long)rps[t] - meta.rs);
+      hi = int((long long)rps[t + 1] - meta.rs);
+    }
+    // first 8 nonzeros: gathers in flight across the previous tile's sketch.
+    // Lanes past the row end re-read the row's last column (a valid index the
+    // row already uses) and contribute a zero product.
+    double v[8], xv[8];
+    if (lo < hi) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int ee = min(lo + q, hi - 1);
+        v[q] = vals[ee];
+        xv[q] = (debug & 2) ? double(cols[ee]) : __ldg(x + cols[ee]);
+      }
+    }
+    gather_prev();
     double sum = 0.0;
-    if (row < n) {
-      const int lo = int((long long)rps[t] - meta.rs), hi = int((long long)rps[t + 1] - meta.rs);
-      // 8 gathers in flight per thread, issued before the first FMA. Lanes
-      // past the row end re-read the row's last column (always a valid index,
-      // and one the row already uses) and contribute a zero product.
-      for (int e = lo; e < hi; e += 8) {
-        double v[8], xv[8];
+    if (lo < hi) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sum += (lo + q < hi ? v[q] : 0.0) * xv[q];
+      for (int e = lo + 8; e < hi; e += 8) {  // long rows (27-point stencils)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int ee = min(e + q, hi - 1);
           v[q] = vals[ee];
-          xv[q] = __ldg(x + cols[ee]);
+          xv[q] = (debug & 2) ? double(cols[ee]) : __ldg(x + cols[ee]);
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) sum += (e + q < hi ? v[q] : 0.0) * xv[q];
       }
-      sum *= xs;
-      z[row] = sum;
     }
-    zs[t] = row < n ? sum * sscale : 0.0;
-    named_sync();
-    sketch_tile_gather(t, d, off, ent, zs, acc);
-    mbar_arrive(&empty[s]);
+    sum *= xs;
+    if (live) z[row] = sum;
+    const double zt = live ? sum * sscale : 0.0;
+    zs[t] = zt;
+    zs[kConsumers + t] = -zt;
+    named_sync();  // zs2 of this tile complete; orders acc updates across threads
+    ps = s;
     if (++s == nstages) {
       s = 0;
       fph ^= 1u;
     }
   }
+  gather_prev();
   named_sync();  // acc[b] may have been written by another consumer thread
   for (int b = t; b < d; b += kConsumers) atomicAdd(pacc + b, acc[b]);
 }
@@ -243,11 +281,24 @@ size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages) {
   return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
 }
 
-int env_evict_first() {  // RKMF_EVICT_FIRST=0 disables the streaming L2 hint
+// RKMF_L2_HINTS: 0 no L2 hints, 1 evict_first on the matrix and sketch
+// streams, 2 (default) evict_first on the matrix and evict_last on the sketch
+// tile layout, which every step re-reads.
+int env_l2_hints() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_EVICT_FIRST");
-    v = (e && e[0] == '0') ? 0 : 1;
+    const char* e = getenv("RKMF_L2_HINTS");
+    v = e ? atoi(e) : 2;
+    if (v < 0 || v > 2) v = 2;
+  }
+  return v;
+}
+
+int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather, 4 stream only)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_PIPE_DEBUG");
+    v = e ? atoi(e) : 0;
   }
   return v;
 }
@@ -287,7 +338,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   if (key != key_c) {
     best_s = 0;
     best_per = 0;
-    for (int s = 2; s <= kStages; ++s) {
+    for (int s = 3; s <= kStages; ++s) {  // consumers hold 2 stages (pipelined)
       if (env_stages() && s != env_stages()) continue;
       const size_t sm = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta), s);
       if (sm > 220 * 1024) continue;
@@ -311,7 +362,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   launch_maybe_pdl(fn, dim3(grid), dim3(kPipeThreads), smem, st, A->n_rows,
                    static_cast<const RP*>(A->row_ptr), A->col, A->val, x, xscale_dev, z, tiles,
                    A->cap, int(S->d), int(S->zeta), off_stride, S->tile_off, S->tile_ent,
-                   S->scale, pacc, stop, step, stages, env_evict_first());
+                   S->scale, pacc, stop, step, stages, env_l2_hints(), env_debug());
   return true;
 }
 
