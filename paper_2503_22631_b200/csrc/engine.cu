@@ -180,7 +180,7 @@ double host_norm(const double* x, int64_t n) {
 
 struct SolveBuffers {
   int64_t n, n_global, d, m_eff, ldw, ldr;
-  double *W, *U, *Rbar, *z, *pacc, *sacc;
+  double *W, *U, *Rbar, *G, *z, *pacc, *sacc;
 };
 
 // n: local rows; n_ext: local rows + halo columns (W columns carry the halo
@@ -195,8 +195,10 @@ SolveBuffers prepare(rkmf_context* ctx, int64_t n, int64_t n_ext, int64_t n_glob
   b.ldw = round_up(std::max<int64_t>(n_ext, 1), 32);
   b.ldr = m_eff + 1;
   b.W = static_cast<double*>(ctx->W.ensure(sizeof(double) * size_t(b.ldw) * size_t(m_eff + 1)));
-  b.U = static_cast<double*>(ctx->U.ensure(sizeof(double) * size_t(d) * size_t(m_eff + 1)));
+  // +2: the Gram-form K3 bulk-copies U[:,0..k] rounded up to 16 bytes
+  b.U = static_cast<double*>(ctx->U.ensure(sizeof(double) * (size_t(d) * size_t(m_eff + 1) + 2)));
   b.Rbar = static_cast<double*>(ctx->Rbar.ensure(sizeof(double) * size_t(b.ldr) * size_t(m_eff)));
+  b.G = static_cast<double*>(ctx->gram.ensure(sizeof(double) * size_t(b.ldr) * size_t(b.ldr)));
   b.z = static_cast<double*>(ctx->z.ensure(sizeof(double) * size_t(b.ldw)));
   b.pacc = static_cast<double*>(ctx->pacc.ensure(sizeof(double) * size_t(d)));
   b.sacc = static_cast<double*>(ctx->sacc.ensure(sizeof(double) * size_t(d)));
@@ -237,7 +239,8 @@ void run_steps(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
     });
     comm_allreduce_sum(ctx, b.pacc, size_t(b.d));  // sum of the ranks' sketch partials
     ctx->timed(1, [&] {
-      launch_rgs_step(b.d, int(k), b.ldr, b.n_global, tol, b.pacc, b.U, b.Rbar, ctx->st_dev,
+      launch_rgs_step(b.d, int(k), b.ldr, b.n_global, tol, b.pacc, b.U, b.Rbar, b.G, b.ldr,
+                      ctx->st_dev,
                       ctx->stream);
     });
     ctx->launches += 2;
@@ -301,7 +304,7 @@ int rkmf_context_destroy(rkmf_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->z, &ctx->pacc, &ctx->sacc, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
                     &ctx->ws, &ctx->u, &ctx->g, &ctx->fhat, &ctx->ref, &ctx->partial,
-                    &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch})
+                    &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch, &ctx->gram})
     b->release();
   for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->kpool) cudaEventDestroy(e);

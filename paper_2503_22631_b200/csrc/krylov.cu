@@ -8,7 +8,10 @@
 // start copy (restart.cpp:118) never touch HBM.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "rkmf_internal.cuh"
+#include "tma.cuh"
 
 namespace rkmf_b200 {
 
@@ -152,6 +155,137 @@ __global__ void __launch_bounds__(kRgsThreads)
     const int64_t b = t + int64_t(j) * kRgsThreads;
     if (b < d) U[int64_t(k + 1) * d + b] = p[j] / rkk;
   }
+  if (t == 0) Rbar[int64_t(k) * ldr + k + 1] = rkk;
+}
+
+// K3, Gram form (used when U[:,0..k] and the Gram rows fit in shared memory).
+// MGS (basis.cpp:123-134) computes r_i = <u_i, p - sum_{j<i} r_j u_j>, i.e.
+//   r_i = c_i - sum_{j<i} G_ij r_j,   c = U^T p,   G_ij = <u_i, u_j>,
+// exactly in exact arithmetic. The dots c and the new Gram row G_k,0..k-1
+// (u_k arrived in the previous step; earlier rows are kept in global memory)
+// are 2k+1 independent reductions spread over the 8 warps; only the unit
+// lower-triangular solve for r is sequential, and it is scalar: one warp
+// holds c in registers and broadcasts each r_i with a shuffle. Then
+// p -= U r, r_kk = ||p||, U[:,k+1] = p / r_kk. With U sketch-orthonormal to
+// rounding, r agrees with the sequential sweep to O(eps ||p||).
+__global__ void __launch_bounds__(kRgsThreads)
+    rgs_gram_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
+                    double* U, double* Rbar, double* G, SolveState* st) {
+  extern __shared__ __align__(16) double sm[];
+  const int kk = k + 1;
+  const int64_t ucnt = (int64_t(kk) * d + 1) / 2 * 2;  // U[:,0..k], rounded to 16 B
+  double* Us = sm;                                     // [kk][d]
+  double* Gs = Us + ucnt;                  // packed rows 1..k: G_ij (j < i) at i(i-1)/2 + j
+  double* ps = Gs + (int64_t(kk) * k / 2 + 1) / 2 * 2;  // [d]
+  double* cs = ps + d;                                  // [kk]: c, then r
+  __shared__ double red[kRgsThreads / 32];
+  __shared__ __align__(8) uint64_t bar;
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  // Prologue (overlaps the SpMV's tail under PDL): U[:,0..k] and Gram rows
+  // 1..k-1 (packed lower triangle) are final; one bulk copy each (TMA) into
+  // shared memory. The 16-byte round-up reads at most one double past either
+  // range, inside the allocations (engine.cu pads U; G holds (m+1)^2).
+  const uint32_t ubytes = uint32_t(ucnt * 8);
+  const uint32_t gbytes = uint32_t((int64_t(k) * (k - 1) / 2 + 1) / 2 * 2 * 8);
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar, ubytes + (k >= 2 ? gbytes : 0u));
+    bulk_g2s(Us, U, ubytes, &bar);
+    if (k >= 2) bulk_g2s(Gs, G, gbytes, &bar);
+  }
+  pdl_wait_then_trigger();
+  if (st->stopped <= k) return;
+  for (int64_t b = t; b < d; b += kRgsThreads) {
+    ps[b] = pacc[b];
+    pacc[b] = 0.0;
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  // 2k+1 dots: task q < kk is c_q = <u_q, p>; task kk + j is G_kj = <u_k, u_j>
+  const double* uk = Us + int64_t(k) * d;
+  constexpr int kW = kRgsThreads / 32;
+  auto task = [&](int q, const double*& a, const double*& bv) {
+    a = q < kk ? Us + int64_t(q) * d : Us + int64_t(q - kk) * d;
+    bv = q < kk ? ps : uk;
+  };
+  auto put = [&](int q, double v) {
+    if (q < kk) {
+      cs[q] = v;
+    } else {
+      Gs[int64_t(k) * (k - 1) / 2 + (q - kk)] = v;
+      G[int64_t(k) * (k - 1) / 2 + (q - kk)] = v;
+    }
+  };
+  const int ntask = 2 * k + 1;
+  for (int q = w; q < ntask; q += 2 * kW) {  // two reductions in flight per warp
+    const int q2 = q + kW;
+    const double *a0, *b0, *a1 = nullptr, *b1 = nullptr;
+    task(q, a0, b0);
+    if (q2 < ntask) task(q2, a1, b1);
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t b = l; b < d; b += 32) {
+      s0 += a0[b] * b0[b];
+      if (q2 < ntask) s1 += a1[b] * b1[b];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (l == 0) {
+      put(q, s0);
+      if (q2 < ntask) put(q2, s1);
+    }
+  }
+  __syncthreads();
+  if (w == 0) {  // unit lower-triangular solve (I + L) r = c, column by column
+    if (kk <= 64) {  // c in registers (lanes l, l+32); r_i broadcast by shuffle
+      const int m0 = l, m1 = l + 32;
+      const int64_t g0 = int64_t(m0) * (m0 - 1) / 2, g1 = int64_t(m1) * (m1 - 1) / 2;
+      double c0 = m0 < kk ? cs[m0] : 0.0, c1 = m1 < kk ? cs[m1] : 0.0;
+      for (int i = 0; i < kk; ++i) {
+        const double a0 = (m0 > i && m0 < kk) ? Gs[g0 + i] : 0.0;
+        const double a1 = (m1 > i && m1 < kk) ? Gs[g1 + i] : 0.0;
+        const double ri = __shfl_sync(0xffffffffu, i < 32 ? c0 : c1, i & 31);
+        if (m0 > i) c0 -= a0 * ri;
+        if (m1 > i) c1 -= a1 * ri;
+      }
+      if (m0 < kk) cs[m0] = c0;
+      if (m1 < kk) cs[m1] = c1;
+    } else {
+      for (int i = 0; i < kk; ++i) {
+        const double ri = cs[i];  // final: every earlier column has updated it
+        __syncwarp();
+        for (int m = i + 1 + l; m < kk; m += 32) cs[m] -= Gs[int64_t(m) * (m - 1) / 2 + i] * ri;
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  double ss = 0.0;
+  for (int64_t b = t; b < d; b += kRgsThreads) {
+    double v = ps[b];
+    for (int i = 0; i < kk; ++i) v -= cs[i] * Us[int64_t(i) * d + b];
+    ps[b] = v;
+    ss += v * v;
+  }
+  ss = warp_sum(ss);
+  if (l == 0) red[w] = ss;
+  __syncthreads();
+  double tot = 0.0;
+#pragma unroll
+  for (int q = 0; q < kRgsThreads / 32; ++q) tot += red[q];
+  const double rkk = sqrt(tot);
+  for (int i = t; i <= k; i += kRgsThreads) Rbar[int64_t(k) * ldr + i] = cs[i];
+  if (rkk <= tol || int64_t(k) + 1 == n) {  // basis.cpp:131-134
+    if (t == 0) {
+      st->stopped = k + 1;
+      st->breakdown = k + 1;
+    }
+    return;
+  }
+  for (int64_t b = t; b < d; b += kRgsThreads) U[int64_t(k + 1) * d + b] = ps[b] / rkk;
   if (t == 0) Rbar[int64_t(k) * ldr + k + 1] = rkk;
 }
 
@@ -311,9 +445,28 @@ void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev,
   RKMF_CUDA(cudaGetLastError());
 }
 
+bool rgs_use_gram() {  // RKMF_RGS=mgs selects the sequential sweep (A/B runs)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_RGS");
+    v = (e && e[0] == 'm') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
-                     double* U, double* Rbar, SolveState* st_dev, cudaStream_t st) {
+                     double* U, double* Rbar, double* G, int64_t ldg, SolveState* st_dev,
+                     cudaStream_t st) {
   if (k >= 1024) param_error("randomized_arnoldi: m > 1024 is not supported on device");
+  const size_t gbytes = sizeof(double) * (size_t(k + 1) * size_t(d) + size_t(k + 1) * size_t(k) / 2 +
+                                          size_t(d) + size_t(k + 1) + 4);
+  if (G != nullptr && rgs_use_gram() && gbytes <= 200 * 1024) {
+    RKMF_CUDA(cudaFuncSetAttribute(rgs_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
+    launch_maybe_pdl(rgs_gram_kernel, dim3(1), dim3(kRgsThreads), gbytes, st, d, k, ldr, n, tol,
+                     pacc, U, Rbar, G, st_dev);
+    return;
+  }
   const int64_t pt = (d + kRgsThreads - 1) / kRgsThreads;
   const size_t ubytes = sizeof(double) * size_t(k + 1) * size_t(d);
   const int staged = ubytes <= 160 * 1024 ? 1 : 0;

@@ -162,8 +162,10 @@ void launch_matrix_check(const CsrView* A, int32_t* flags, bool require_sorted, 
 // krylov.cu
 void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev, bool first,
                          int m_eff, cudaStream_t st);
+// G: (m+1) x (m+1) scratch for the Gram rows of U (row i at i*ldg), or null
+// for the sequential MGS sweep.
 void launch_rgs_step(int64_t d, int k, int64_t m, int64_t n, double tol, double* pacc, double* U,
-                     double* Rbar, SolveState* st_dev, cudaStream_t st);
+                     double* Rbar, double* G, int64_t ldg, SolveState* st_dev, cudaStream_t st);
 void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double* z,
                          const double* Rbar, int64_t ldr, const SolveState* st_dev,
                          cudaStream_t st);
