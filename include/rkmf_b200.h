@@ -190,6 +190,20 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
 int rkmf_nccl_unique_id(void* out128);
 int rkmf_context_init_comm(rkmf_context* ctx, int32_t nranks, int32_t rank,
                            const void* unique_id128);
+/* The same collectives through caller callbacks on pinned host buffers (an MPI
+ * or gloo host stack; tests with fewer GPUs than ranks). Each returns 0 on
+ * success. alltoallv_b64: send holds one segment per rank in rank order
+ * (send_counts[q] 8-byte elements for rank q), recv receives rank q's segment
+ * (recv_counts[q] elements) in rank order; own-rank counts are 0. */
+typedef struct rkmf_host_comm {
+  void* user;
+  int (*allreduce_sum_f64)(void* user, double* buf, int64_t count);
+  int (*allreduce_max_f64)(void* user, double* buf, int64_t count);
+  int (*alltoallv_b64)(void* user, const void* send, const int64_t* send_counts, void* recv,
+                       const int64_t* recv_counts);
+} rkmf_host_comm;
+int rkmf_context_init_host_comm(rkmf_context* ctx, int32_t nranks, int32_t rank,
+                                const rkmf_host_comm* callbacks);
 int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const int64_t* row_starts,
                                    const int64_t* h_row_ptr_local, const int32_t* h_col_global,
                                    const double* h_values, rkmf_matrix** out);

@@ -121,6 +121,7 @@ SYMBOLS = [
     ("rkmf_last_r_accum", C.c_int, [_P, _P, _I64, _P]),
     ("rkmf_nccl_unique_id", C.c_int, [_P]),
     ("rkmf_context_init_comm", C.c_int, [_P, _I32, _I32, _P]),
+    ("rkmf_context_init_host_comm", C.c_int, [_P, _I32, _I32, _P]),
     ("rkmf_matrix_create_partitioned", C.c_int, [_P, _I64, _P, _P, _P, _P, _PP]),
     ("rkmf_sketch_create_partitioned", C.c_int, [_P, _I64, _I64, _I64, _U64, _I64, _I64, _PP]),
     ("rkmf_partition_rows", C.c_int, [_I64, _P, _I32, _P]),
@@ -561,6 +562,54 @@ def init_comm(ctx: Context, nranks: int, rank: int, unique_id: bytes) -> None:
     """One NCCL communicator per context (one process per GPU)."""
     buf = C.create_string_buffer(unique_id, 128)
     ctx.check(lib().rkmf_context_init_comm(ctx.h, nranks, rank, buf))
+    ctx.nranks, ctx.rank = nranks, rank
+
+
+_REDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+_A2A_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                      C.POINTER(C.c_int64))
+
+
+class _HostComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum_f64", _REDUCE_CB),
+                ("allreduce_max_f64", _REDUCE_CB), ("alltoallv_b64", _A2A_CB)]
+
+
+def init_host_comm(ctx: Context, nranks: int, rank: int, allreduce, alltoallv) -> None:
+    """Drive the partitioned solve through host callbacks (rkmf_host_comm).
+
+    allreduce(buf: np.ndarray[float64], op: "sum" | "max") reduces in place;
+    alltoallv(send: np.ndarray[int8], send_counts, recv: np.ndarray[int8],
+    recv_counts) moves per-rank segments of 8-byte elements in rank order."""
+    def red(op):
+        def cb(_u, buf, count):
+            try:
+                allreduce(np.ctypeslib.as_array(buf, shape=(count,)), op)
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a status code
+                import traceback
+                traceback.print_exc()
+                return 1
+        return _REDUCE_CB(cb)
+
+    def a2a(_u, send, scnt, recv, rcnt):
+        try:
+            sc = np.ctypeslib.as_array(scnt, shape=(nranks,)).copy()
+            rc = np.ctypeslib.as_array(rcnt, shape=(nranks,)).copy()
+            sb = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_int8)),
+                                       shape=(8 * max(int(sc.sum()), 1),))
+            rb = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_int8)),
+                                       shape=(8 * max(int(rc.sum()), 1),))
+            alltoallv(sb, sc, rb, rc)
+            return 0
+        except Exception:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    hc = _HostComm(None, red("sum"), red("max"), _A2A_CB(a2a))
+    ctx._host_comm = hc  # the callbacks must outlive the context's use of them
+    ctx.check(lib().rkmf_context_init_host_comm(ctx.h, nranks, rank, C.byref(hc)))
     ctx.nranks, ctx.rank = nranks, rank
 
 

@@ -1,19 +1,26 @@
-// Multi-GPU plumbing: NCCL communicator, row-partitioned matrices and sketches,
-// the per-step halo exchange and the sketch allreduce.
+// Multi-GPU plumbing: transports, row-partitioned matrices and sketches, the
+// per-step halo exchange and the sketch allreduce.
 //
 // One process per GPU. Rank r owns rows [row_starts[r], row_starts[r+1]) of A,
 // the same rows of every basis vector, of z and of f; its sketch is the same
 // column range of the global S (bit-identical to make_sketch on n_global).
 // Per Krylov step:
-//   halo exchange   pack the owned x entries other ranks reference, then
-//                   ncclSend/ncclRecv with every neighbour in one group; the
-//                   received values land directly in the halo tail of the x
-//                   column (W is allocated with ld >= n_local + n_halo)
+//   halo exchange   pack the owned x entries other ranks reference, then one
+//                   personalised exchange; the received values land directly
+//                   in the halo tail of the x column (W is allocated with
+//                   ld >= n_local + n_halo)
 //   local K2        SpMV over [owned | halo] columns + local sketch partial
-//   allreduce       ncclAllReduce(sum) of the d sketch doubles, in place
+//   allreduce       sum of the d sketch doubles, in place
 //   K3              replicated (every rank holds the same p, hence the same r)
 //   K4              local
 // Per cycle: allreduce of the start sketch (d) and of ||y||^2, ||f-ref||^2 (2).
+//
+// Transports: NcclTransport (ncclAllReduce, grouped ncclSend/ncclRecv over
+// NVLink/NVSwitch) is the product path. HostTransport stages the same
+// collectives through pinned host memory into caller callbacks
+// (rkmf_host_comm), so an MPI or gloo host stack can drive the partitioned
+// solve, and the multi-rank path can be exercised where fewer GPUs than ranks
+// exist: its ranks never wait on each other inside a kernel.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -39,6 +46,106 @@ namespace rkmf_b200 {
   } while (0)
 
 namespace {
+
+class NcclTransport final : public Transport {
+ public:
+  NcclTransport(int nranks, int rank, const ncclUniqueId& id) : me_(rank), p_(nranks) {
+    RKMF_NCCL(ncclCommInitRank(&comm_, nranks, id, rank));
+  }
+  ~NcclTransport() override {
+    if (comm_) ncclCommDestroy(comm_);
+  }
+  void allreduce(double* dev, size_t count, bool max, cudaStream_t st) override {
+    RKMF_NCCL(ncclAllReduce(dev, dev, count, ncclFloat64, max ? ncclMax : ncclSum, comm_, st));
+  }
+  void alltoallv(const void* send, const std::vector<int64_t>& soff,
+                 const std::vector<int64_t>& scnt, void* recv, const std::vector<int64_t>& roff,
+                 const std::vector<int64_t>& rcnt, bool is_double, cudaStream_t st) override {
+    const ncclDataType_t ty = is_double ? ncclFloat64 : ncclInt64;
+    const char* s = static_cast<const char*>(send);
+    char* r = static_cast<char*>(recv);
+    RKMF_NCCL(ncclGroupStart());
+    for (int q = 0; q < p_; ++q) {
+      if (q == me_) continue;
+      if (scnt[q] > 0) RKMF_NCCL(ncclSend(s + 8 * soff[q], size_t(scnt[q]), ty, q, comm_, st));
+      if (rcnt[q] > 0) RKMF_NCCL(ncclRecv(r + 8 * roff[q], size_t(rcnt[q]), ty, q, comm_, st));
+    }
+    RKMF_NCCL(ncclGroupEnd());
+  }
+
+ private:
+  ncclComm_t comm_ = nullptr;
+  int me_, p_;
+};
+
+class HostTransport final : public Transport {
+ public:
+  HostTransport(int nranks, int rank, const rkmf_host_comm& cb) : me_(rank), p_(nranks), cb_(cb) {}
+  ~HostTransport() override {
+    if (stage_) cudaFreeHost(stage_);
+  }
+  void allreduce(double* dev, size_t count, bool max, cudaStream_t st) override {
+    double* h = static_cast<double*>(host(8 * count));
+    RKMF_CUDA(cudaMemcpyAsync(h, dev, 8 * count, cudaMemcpyDeviceToHost, st));
+    RKMF_CUDA(cudaStreamSynchronize(st));
+    const int rc = max ? cb_.allreduce_max_f64(cb_.user, h, int64_t(count))
+                       : cb_.allreduce_sum_f64(cb_.user, h, int64_t(count));
+    if (rc != 0) throw Error(RKMF_DEVICE_ERROR, "host comm: allreduce callback failed");
+    RKMF_CUDA(cudaMemcpyAsync(dev, h, 8 * count, cudaMemcpyHostToDevice, st));
+    RKMF_CUDA(cudaStreamSynchronize(st));  // h is reused by the next call
+  }
+  void alltoallv(const void* send, const std::vector<int64_t>& soff,
+                 const std::vector<int64_t>& scnt, void* recv, const std::vector<int64_t>& roff,
+                 const std::vector<int64_t>& rcnt, bool /*is_double*/, cudaStream_t st) override {
+    // the callback sees contiguous per-rank segments in rank order
+    std::vector<int64_t> sc(scnt), rc(rcnt);
+    sc[me_] = 0;
+    rc[me_] = 0;
+    int64_t stot = 0, rtot = 0;
+    for (int q = 0; q < p_; ++q) {
+      stot += sc[q];
+      rtot += rc[q];
+    }
+    char* h = static_cast<char*>(host(8 * size_t(stot + rtot)));
+    char* hs = h;
+    char* hr = h + 8 * stot;
+    const char* s = static_cast<const char*>(send);
+    char* r = static_cast<char*>(recv);
+    int64_t o = 0;
+    for (int q = 0; q < p_; ++q) {
+      if (sc[q] > 0)
+        RKMF_CUDA(cudaMemcpyAsync(hs + 8 * o, s + 8 * soff[q], 8 * size_t(sc[q]),
+                                  cudaMemcpyDeviceToHost, st));
+      o += sc[q];
+    }
+    RKMF_CUDA(cudaStreamSynchronize(st));
+    if (cb_.alltoallv_b64(cb_.user, hs, sc.data(), hr, rc.data()) != 0)
+      throw Error(RKMF_DEVICE_ERROR, "host comm: alltoallv callback failed");
+    o = 0;
+    for (int q = 0; q < p_; ++q) {
+      if (rc[q] > 0)
+        RKMF_CUDA(cudaMemcpyAsync(r + 8 * roff[q], hr + 8 * o, 8 * size_t(rc[q]),
+                                  cudaMemcpyHostToDevice, st));
+      o += rc[q];
+    }
+    RKMF_CUDA(cudaStreamSynchronize(st));
+  }
+
+ private:
+  void* host(size_t bytes) {
+    if (bytes > cap_) {
+      if (stage_) RKMF_CUDA(cudaFreeHost(stage_));
+      stage_ = nullptr;
+      cap_ = std::max<size_t>(bytes, 4096);
+      RKMF_CUDA(cudaMallocHost(&stage_, cap_));
+    }
+    return stage_;
+  }
+  int me_, p_;
+  rkmf_host_comm cb_;
+  void* stage_ = nullptr;
+  size_t cap_ = 0;
+};
 
 __global__ void pack_kernel(int64_t cnt, const int32_t* __restrict__ idx,
                             const double* __restrict__ x, double* __restrict__ out) {
@@ -67,7 +174,7 @@ __global__ void max_abs_kernel(int64_t n, const double* __restrict__ v, double* 
        i += int64_t(gridDim.x) * blockDim.x)
     m = fmax(m, v[i]);
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0)
+  if ((threadIdx.x & 31) == 0)  // non-negative doubles order like their bit patterns
     atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(m));
 }
 
@@ -77,7 +184,7 @@ int blocks_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n
 
 void comm_allreduce_sum(rkmf_context* ctx, double* buf, size_t count) {
   if (!ctx->comm || ctx->nranks <= 1 || count == 0) return;
-  RKMF_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+  ctx->comm->allreduce(buf, count, false, ctx->stream);
 }
 
 void comm_halo_exchange(rkmf_context* ctx, const rkmf_matrix* A, double* x) {
@@ -89,17 +196,8 @@ void comm_halo_exchange(rkmf_context* ctx, const rkmf_matrix* A, double* x) {
     RKMF_CUDA(cudaGetLastError());
     ctx->launches++;
   }
-  RKMF_NCCL(ncclGroupStart());
-  for (int q = 0; q < ctx->nranks; ++q) {
-    if (q == ctx->rank) continue;
-    if (h.send_cnt[q] > 0)
-      RKMF_NCCL(ncclSend(h.sendbuf + h.send_off[q], size_t(h.send_cnt[q]), ncclFloat64, q,
-                         ctx->comm, ctx->stream));
-    if (h.recv_cnt[q] > 0)
-      RKMF_NCCL(ncclRecv(x + h.n_local + h.recv_off[q], size_t(h.recv_cnt[q]), ncclFloat64, q,
-                         ctx->comm, ctx->stream));
-  }
-  RKMF_NCCL(ncclGroupEnd());
+  ctx->comm->alltoallv(h.sendbuf, h.send_off, h.send_cnt, x + h.n_local, h.recv_off, h.recv_cnt,
+                       true, ctx->stream);
 }
 
 }  // namespace rkmf_b200
@@ -123,21 +221,8 @@ int guarded_c(rkmf_context* ctx, F&& fn) {
   }
 }
 
-// int64 all-to-all of per-rank segments through grouped send/recv
-void exchange_i64(rkmf_context* ctx, const int64_t* send_dev, const std::vector<int64_t>& soff,
-                  const std::vector<int64_t>& scnt, int64_t* recv_dev,
-                  const std::vector<int64_t>& roff, const std::vector<int64_t>& rcnt) {
-  RKMF_NCCL(ncclGroupStart());
-  for (int q = 0; q < ctx->nranks; ++q) {
-    if (q == ctx->rank) continue;
-    if (scnt[q] > 0)
-      RKMF_NCCL(ncclSend(send_dev + soff[q], size_t(scnt[q]), ncclInt64, q, ctx->comm,
-                         ctx->stream));
-    if (rcnt[q] > 0)
-      RKMF_NCCL(ncclRecv(recv_dev + roff[q], size_t(rcnt[q]), ncclInt64, q, ctx->comm,
-                         ctx->stream));
-  }
-  RKMF_NCCL(ncclGroupEnd());
+void check_ranks(int32_t nranks, int32_t rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) param_error("comm: invalid rank/nranks");
 }
 
 }  // namespace
@@ -154,18 +239,32 @@ int rkmf_nccl_unique_id(void* out128) {
 int rkmf_context_init_comm(rkmf_context* ctx, int32_t nranks, int32_t rank,
                            const void* unique_id128) {
   return guarded_c(ctx, [&] {
-    if (nranks < 1 || rank < 0 || rank >= nranks) param_error("comm: invalid rank/nranks");
+    check_ranks(nranks, rank);
     RKMF_CUDA(cudaSetDevice(ctx->device));
-    if (ctx->comm) {
-      ncclCommDestroy(ctx->comm);
-      ctx->comm = nullptr;
-    }
+    delete ctx->comm;
+    ctx->comm = nullptr;
     ctx->nranks = nranks;
     ctx->rank = rank;
     if (nranks == 1) return;
     ncclUniqueId id;
     std::memcpy(&id, unique_id128, sizeof(id));
-    RKMF_NCCL(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+    ctx->comm = new NcclTransport(nranks, rank, id);
+  });
+}
+
+int rkmf_context_init_host_comm(rkmf_context* ctx, int32_t nranks, int32_t rank,
+                                const rkmf_host_comm* callbacks) {
+  return guarded_c(ctx, [&] {
+    check_ranks(nranks, rank);
+    if (nranks > 1 && (!callbacks || !callbacks->allreduce_sum_f64 ||
+                       !callbacks->allreduce_max_f64 || !callbacks->alltoallv_b64))
+      param_error("host comm: all three callbacks are required");
+    delete ctx->comm;
+    ctx->comm = nullptr;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    if (nranks == 1) return;
+    ctx->comm = new HostTransport(nranks, rank, *callbacks);
   });
 }
 
@@ -175,10 +274,11 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
   return guarded_c(ctx, [&] {
     RKMF_CUDA(cudaSetDevice(ctx->device));
     const int P = ctx->nranks, me = ctx->rank;
-    if (P > 1 && !ctx->comm) param_error("partitioned matrix: call rkmf_context_init_comm first");
+    if (P > 1 && !ctx->comm) param_error("partitioned matrix: initialise the communicator first");
     const int64_t rb = row_starts[me], re = row_starts[me + 1];
     const int64_t n_local = re - rb;
-    if (rb < 0 || re < rb || row_starts[P] != n_global) shape_error("partition: bad row_starts");
+    if (row_starts[0] != 0 || rb < 0 || re < rb || row_starts[P] != n_global)
+      shape_error("partition: bad row_starts");
     if (h_row_ptr_local[0] != 0) shape_error("row_ptr[0] != 0");
     const int64_t nnz = h_row_ptr_local[n_local];
     // validate the rows in global numbering (sparse.cpp:61-81)
@@ -216,6 +316,9 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
       h.send_off.assign(size_t(P), 0);
       cudaStream_t st = ctx->stream;
       if (P > 1) {
+        Transport& T = *ctx->comm;
+        std::vector<int64_t> one(static_cast<size_t>(P), 1), idx(static_cast<size_t>(P));
+        for (int q = 0; q < P; ++q) idx[q] = q;
         // 1) counts: what each rank needs from me
         DevBuf rc, sc;
         rc.ensure(sizeof(int64_t) * size_t(P));
@@ -223,9 +326,7 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
         RKMF_CUDA(cudaMemcpyAsync(rc.p, h.recv_cnt.data(), sizeof(int64_t) * size_t(P),
                                   cudaMemcpyHostToDevice, st));
         RKMF_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(int64_t) * size_t(P), st));
-        std::vector<int64_t> one(static_cast<size_t>(P), 1), idx(static_cast<size_t>(P));
-        for (int q = 0; q < P; ++q) idx[q] = q;
-        exchange_i64(ctx, rc.as<int64_t>(), idx, one, sc.as<int64_t>(), idx, one);
+        T.alltoallv(rc.p, idx, one, sc.p, idx, one, false, st);
         RKMF_CUDA(cudaMemcpyAsync(h.send_cnt.data(), sc.p, sizeof(int64_t) * size_t(P),
                                   cudaMemcpyDeviceToHost, st));
         RKMF_CUDA(cudaStreamSynchronize(st));
@@ -239,8 +340,7 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
         if (n_halo > 0)
           RKMF_CUDA(cudaMemcpyAsync(req.p, halo.data(), sizeof(int64_t) * size_t(n_halo),
                                     cudaMemcpyHostToDevice, st));
-        exchange_i64(ctx, req.as<int64_t>(), h.recv_off, h.recv_cnt, got.as<int64_t>(), h.send_off,
-                     h.send_cnt);
+        T.alltoallv(req.p, h.recv_off, h.recv_cnt, got.p, h.send_off, h.send_cnt, false, st);
         std::vector<int64_t> sg(static_cast<size_t>(h.send_total));
         if (h.send_total > 0)
           RKMF_CUDA(cudaMemcpyAsync(sg.data(), got.p, sizeof(int64_t) * size_t(h.send_total),
@@ -257,7 +357,8 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
           RKMF_CUDA(cudaMemcpyAsync(h.send_idx, sl.data(), sizeof(int32_t) * size_t(h.send_total),
                                     cudaMemcpyHostToDevice, st));
         // 3) global norm1 = max column abs-sum (sparse.cpp:97-102): local column
-        //    sums, halo parts returned to their owners, max, allreduce(max)
+        //    sums, the halo parts returned to their owners (the reverse of the
+        //    halo exchange), max, allreduce(max)
         DevBuf cs, back, mx;
         cs.ensure(sizeof(double) * size_t(n_local + n_halo + 1));
         back.ensure(sizeof(double) * size_t(std::max<int64_t>(h.send_total, 1)));
@@ -266,17 +367,8 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
         RKMF_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(double), st));
         if (nnz > 0)
           colsum_abs_kernel<<<blocks_for(nnz), 256, 0, st>>>(nnz, M->col, M->val, cs.as<double>());
-        RKMF_NCCL(ncclGroupStart());
-        for (int q = 0; q < P; ++q) {
-          if (q == me) continue;
-          if (h.recv_cnt[q] > 0)
-            RKMF_NCCL(ncclSend(cs.as<double>() + n_local + h.recv_off[q], size_t(h.recv_cnt[q]),
-                               ncclFloat64, q, ctx->comm, st));
-          if (h.send_cnt[q] > 0)
-            RKMF_NCCL(ncclRecv(back.as<double>() + h.send_off[q], size_t(h.send_cnt[q]),
-                               ncclFloat64, q, ctx->comm, st));
-        }
-        RKMF_NCCL(ncclGroupEnd());
+        T.alltoallv(cs.as<double>() + n_local, h.recv_off, h.recv_cnt, back.p, h.send_off,
+                    h.send_cnt, true, st);
         if (h.send_total > 0)
           scatter_add_kernel<<<blocks_for(h.send_total), 256, 0, st>>>(h.send_total, h.send_idx,
                                                                         back.as<double>(),
@@ -285,7 +377,7 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
           max_abs_kernel<<<blocks_for(n_local), 256, 0, st>>>(n_local, cs.as<double>(),
                                                               mx.as<double>());
         RKMF_CUDA(cudaGetLastError());
-        RKMF_NCCL(ncclAllReduce(mx.p, mx.p, 1, ncclFloat64, ncclMax, ctx->comm, st));
+        T.allreduce(mx.as<double>(), 1, true, st);
         RKMF_CUDA(cudaMemcpyAsync(&M->norm1, mx.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         RKMF_CUDA(cudaStreamSynchronize(st));
         ctx->launches += 3;

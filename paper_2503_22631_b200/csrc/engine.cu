@@ -308,7 +308,7 @@ int rkmf_context_destroy(rkmf_context* ctx) {
     b->release();
   for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->kpool) cudaEventDestroy(e);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  delete ctx->comm;
   if (ctx->st_dev) cudaFree(ctx->st_dev);
   if (ctx->st_host) cudaFreeHost(ctx->st_host);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

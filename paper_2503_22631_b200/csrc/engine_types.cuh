@@ -2,8 +2,6 @@
 // sketch objects behind the opaque C-ABI handles).
 #pragma once
 
-#include <nccl.h>
-
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -36,12 +34,32 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 }  // namespace rkmf_b200
 
+namespace rkmf_b200 {
+// Collectives of the row-partitioned solve, on device buffers and the
+// context stream. NcclTransport (comm.cu) is the product path, one process
+// per GPU over NVLink/NVSwitch; HostTransport stages through pinned host
+// memory into caller callbacks (rkmf_host_comm: MPI, gloo, tests).
+struct Transport {
+  virtual ~Transport() {}
+  // in-place elementwise sum (or max) of count doubles over all ranks
+  virtual void allreduce(double* dev, size_t count, bool max, cudaStream_t st) = 0;
+  // personalised exchange of 8-byte elements: segment q of the send buffer
+  // (scnt[q] elements at soff[q]) goes to rank q; what rank q sends here lands
+  // at roff[q] (rcnt[q] elements). Counts are agreed beforehand; the own-rank
+  // segment is not moved.
+  virtual void alltoallv(const void* send, const std::vector<int64_t>& soff,
+                         const std::vector<int64_t>& scnt, void* recv,
+                         const std::vector<int64_t>& roff, const std::vector<int64_t>& rcnt,
+                         bool is_double, cudaStream_t st) = 0;
+};
+}  // namespace rkmf_b200
+
 using namespace rkmf_b200;
 
 struct rkmf_context {
   int device = 0;
-  // multi-GPU: one rank per process/GPU (rkmf_context_init_comm)
-  ncclComm_t comm = nullptr;
+  // multi-GPU: one rank per process/GPU (rkmf_context_init_comm / _host_comm)
+  Transport* comm = nullptr;
   int nranks = 1, rank = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;

@@ -19,15 +19,15 @@
 extern "C" {
 
 // row_starts[0..nranks]: contiguous blocks whose nonzero counts are as equal
-// as the row granularity allows (each boundary is the first row whose prefix
-// nnz reaches r/nranks of the total).
+// as the row granularity allows (boundary r is the first row whose prefix
+// nnz reaches floor(r * nnz / nranks)).
 int rkmf_partition_rows(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* row_starts) {
   if (nranks < 1 || n < 0) return RKMF_PARAMETER_ERROR;
   const int64_t nnz = row_ptr[n];
   row_starts[0] = 0;
   for (int32_t r = 1; r < nranks; ++r) {
-    const long double target = (long double)nnz * r / nranks;
-    const int64_t* it = std::lower_bound(row_ptr, row_ptr + n + 1, (int64_t)target);
+    const int64_t target = int64_t((__int128)nnz * r / nranks);
+    const int64_t* it = std::lower_bound(row_ptr, row_ptr + n + 1, target);
     int64_t row = int64_t(it - row_ptr);
     row = std::max(row, row_starts[r - 1]);
     row = std::min(row, n);
@@ -39,7 +39,8 @@ int rkmf_partition_rows(int64_t n, const int64_t* row_ptr, int32_t nranks, int64
 
 // Halo plan of `rank`. Inputs: the rank's rows [row_starts[rank],
 // row_starts[rank+1]) as CSR with local row pointers (row_ptr_local[0] == 0)
-// and GLOBAL column indices. Outputs (pass NULL arrays first to get *n_halo):
+// and GLOBAL column indices. Outputs (pass NULL arrays first to get *n_halo;
+// each non-NULL array is filled):
 //   halo_global[n_halo]  sorted distinct off-rank columns (grouped by owner)
 //   recv_counts[nranks]  how many halo entries each rank owns
 //   col_local[nnz]       owned column c -> c - row_begin; halo column -> n_local + position
@@ -59,13 +60,16 @@ int rkmf_partition_halo(int32_t nranks, int32_t rank, const int64_t* row_starts,
   std::sort(halo.begin(), halo.end());
   halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
   *n_halo = int64_t(halo.size());
-  if (!halo_global) return RKMF_OK;
-  std::copy(halo.begin(), halo.end(), halo_global);
-  for (int32_t q = 0; q < nranks; ++q) recv_counts[q] = 0;
-  int32_t owner = 0;
-  for (int64_t c : halo) {  // halo is sorted and blocks are contiguous
-    while (c >= row_starts[owner + 1]) ++owner;
-    ++recv_counts[owner];
+  // each output is filled when its pointer is given (an empty halo may come
+  // with a null halo_global)
+  if (halo_global) std::copy(halo.begin(), halo.end(), halo_global);
+  if (recv_counts) {
+    for (int32_t q = 0; q < nranks; ++q) recv_counts[q] = 0;
+    int32_t owner = 0;
+    for (int64_t c : halo) {  // halo is sorted and blocks are contiguous
+      while (c >= row_starts[owner + 1]) ++owner;
+      ++recv_counts[owner];
+    }
   }
   if (col_local) {
     for (int64_t k = 0; k < nnz; ++k) {
