@@ -9,8 +9,9 @@ vectors per second (sum of m_k over cycles / solve time), whole job.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config cfg1..cfg5]
 
-N > 1 (torchrun, one rank per GPU): independent replicas of the workload per
-rank (weak scaling); the row-partitioned NCCL path is not in this round.
+N > 1 (torchrun, one rank per GPU): one row-partitioned solve over all ranks
+(weak scaling: each rank owns a cfg2-sized x-slab of a 128N x 128 x 128 grid;
+halo send/recv + sketch allreduce over NCCL every Krylov step).
 `--impl reference` times the CPU restatement of the reference solver (the
 reference itself cannot be built here: Eigen3 is absent) on the host cores.
 """
@@ -105,9 +106,10 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def class_bytes(P, total_m, cycles):
-    """Algorithmic bytes per solve for each kernel class (SURVEY.md §8(d) terms)."""
-    n, nnz, m = P.n, P.nnz, P.m
+def class_bytes(w, total_m, cycles):
+    """Algorithmic bytes per solve (per rank) for each kernel class (SURVEY.md
+    §8(d) terms)."""
+    n, nnz, m = w.n, w.nnz, w.m
     rp = 4 if nnz < 2**31 - 1 else 8
     steps = total_m
     spmv = steps * (12 * nnz + rp * (n + 1) + 8 * n + 8 * n)
@@ -172,28 +174,86 @@ def run_reference(args):
     return 0
 
 
+class Workload:
+    """What one rank solves: the device objects plus the sizes the byte model
+    and the JSON line need."""
+
+
+def setup_single(args, ctx, dev):
+    import torch
+
+    import paper_2503_22631_b200 as rk
+    from paper_2503_22631_b200 import configs
+    P = configs.build(args.config)
+    w = Workload()
+    w.P, w.n, w.nnz, w.m = P, P.n, P.nnz, P.m
+    w.A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values, ctx=ctx)
+    w.S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, ctx=ctx)
+    w.f = rk.FunctionSpec.exp_neg(P.t) if P.fn == "exp_neg" else rk.FunctionSpec.inv_sqrt()
+    w.opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
+    w.b_host = P.b
+    w.b_dev = torch.tensor(P.b, device=dev)
+    w.config = dict(workload_desc(P, args.config), parallelism="single")
+    return w
+
+
+def setup_partitioned(args, ctx_device, world, rank, dev):
+    """Weak scaling: rank r owns an x-slab of cfg2's size (configs.build_slab);
+    one distributed solve over all ranks (halo exchange + sketch allreduce)."""
+    import torch
+
+    import paper_2503_22631_b200 as rk
+    from paper_2503_22631_b200 import configs
+    from paper_2503_22631_b200 import distributed as D
+    transport = os.environ.get("RKMF_BENCH_TRANSPORT", "nccl")
+    ctx = D.make_context(ctx_device, world, rank, transport)
+    Sl = configs.build_slab(world, rank)
+    part = D.partition_local(ctx, Sl.n_global, Sl.row_starts, Sl.row_ptr, Sl.col_idx, Sl.values,
+                             Sl.b, Sl.d, Sl.zeta, configs.SKETCH_SEED, rank)
+    w = Workload()
+    w.ctx, w.P, w.n, w.nnz, w.m = ctx, None, part.n_local, Sl.nnz, Sl.m
+    w.A, w.S = part.A, part.S
+    w.f = rk.FunctionSpec.exp_neg(Sl.t)
+    w.opts = rk.RestartOptions(m_r=Sl.m, tol=Sl.tol, k_max=Sl.k_max)
+    w.b_host = part.b
+    w.b_dev = torch.tensor(part.b, device=dev)
+    w.config = {"workload": f"cfg2 weak-scaled: 3D 7-point Laplacian {128 * world}x128x128, "
+                            f"one {128}^3 x-slab (cfg2's rows) per GPU",
+                "matrix_rows": Sl.n_global, "nnz": Sl.nnz_global, "rows_per_gpu": part.n_local,
+                "function": "exp_neg", "t": Sl.t, "m": Sl.m, "sketch_d": Sl.d, "zeta": Sl.zeta,
+                "tol_abs": Sl.tol, "k_max": Sl.k_max, "b_seed": 1, "sketch_seed": 1,
+                "l2_policy": "inputs larger than L2 (CSR + basis W exceed 126 MB)",
+                "parallelism": f"row-partitioned x{world} ({transport}: halo send/recv + "
+                               f"sketch allreduce per Krylov step)",
+                "unit_note": "basis vectors counted per rank slab (value = world x m_k / s)"}
+    return w
+
+
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2503_22631_b200 as rk
-    from paper_2503_22631_b200 import configs
 
     rank, world, local = env_rank()
+    if os.environ.get("RKMF_BENCH_ONE_GPU"):  # functional runs of N ranks on one GPU
+        local = 0                             # (with RKMF_BENCH_TRANSPORT=host); not timing
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if world > 1 and os.environ.get("RKMF_BENCH_ONE_GPU"):
+        dist.init_process_group("gloo")  # NCCL refuses two ranks on one device
+    elif world > 1:
+        # CPU tensors (host transport, timing reductions) over gloo, CUDA over NCCL
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
-    P = configs.build(args.config)
-    ctx = rk.Context.default(local)
+    if world > 1:
+        w = setup_partitioned(args, local, world, rank, dev)
+        ctx = w.ctx
+    else:
+        ctx = rk.Context.default(local)
+        w = setup_single(args, ctx, dev)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream)
-    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values, ctx=ctx)
-    S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, ctx=ctx)
-    f = rk.FunctionSpec.exp_neg(P.t) if P.fn == "exp_neg" else rk.FunctionSpec.inv_sqrt()
-    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
-    b_dev = torch.tensor(P.b, device=dev)
+    A, S, f, opts, b_dev = w.A, w.S, w.f, w.opts, w.b_dev
 
     for _ in range(args.warmup):
         res = rk.restarted_krylov(A, b_dev, f, opts, S)
@@ -218,7 +278,7 @@ def run_ours(args):
         barrier()
     gpu_launches = ctx.launch_count - launches0
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    t = torch.tensor([ms], dtype=torch.float64)  # max over ranks (CPU tensor: gloo)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
@@ -226,24 +286,30 @@ def run_ours(args):
 
     # ---- setup (once per matrix, outside both timed regions, reported):
     #      CSR upload from pinned host memory + validation, device sketch ----
-    rp_h = torch.from_numpy(P.row_ptr).pin_memory()
-    ci_h = torch.from_numpy(P.col_idx).pin_memory()
-    v_h = torch.from_numpy(P.values).pin_memory()
-    torch.cuda.synchronize()
-    s0 = time.perf_counter()
-    A2 = rk.SparseMatrix.from_csr(rp_h.numpy(), ci_h.numpy(), v_h.numpy(), ctx=ctx)
-    s1 = time.perf_counter()
-    S2 = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, ctx=ctx)
-    torch.cuda.synchronize()
-    s2 = time.perf_counter()
-    setup = {"matrix_upload_validate_s": s1 - s0, "sketch_generate_s": s2 - s1,
-             "h2d_bytes": 8 * (P.n + 1) + 12 * P.nnz}
+    setup = None
+    A2, S2 = A, S
+    if world == 1:
+        from paper_2503_22631_b200 import configs
+        P = w.P
+        rp_h = torch.from_numpy(P.row_ptr).pin_memory()
+        ci_h = torch.from_numpy(P.col_idx).pin_memory()
+        v_h = torch.from_numpy(P.values).pin_memory()
+        torch.cuda.synchronize()
+        s0 = time.perf_counter()
+        A2 = rk.SparseMatrix.from_csr(rp_h.numpy(), ci_h.numpy(), v_h.numpy(), ctx=ctx)
+        s1 = time.perf_counter()
+        S2 = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, ctx=ctx)
+        torch.cuda.synchronize()
+        s2 = time.perf_counter()
+        setup = {"matrix_upload_validate_s": s1 - s0, "sketch_generate_s": s2 - s1,
+                 "h2d_bytes": 8 * (P.n + 1) + 12 * P.nnz}
 
     # ---- e2e: the reference-facing call with HOST vectors: every step copies
     #      b host->device (pinned) and f device->host inside the timed region ----
-    b_h = torch.from_numpy(P.b).pin_memory()
-    f_h = torch.empty(P.n, dtype=torch.float64).pin_memory()
+    b_h = torch.from_numpy(w.b_host).pin_memory()
+    f_h = torch.empty(w.n, dtype=torch.float64).pin_memory()
     e2e_steps = max(1, args.steps)
+    rk.restarted_krylov(A2, b_h.numpy(), f, opts, S2, out=f_h.numpy())  # warm-up
     barrier()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
@@ -254,22 +320,22 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
     del A2, S2
-    et = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    et = torch.tensor([e2e_s], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_value = world * e2e_m / float(et.item())
-    h2d = 8 * P.n
-    d2h = 8 * P.n
+    h2d = 8 * w.n
+    d2h = 8 * w.n
 
-    out = None
+    # ---- per-kernel breakdown (separate diagnostic solve, events per launch;
+    #      every rank runs it so the collectives match) ----
+    ctx.kernel_timing(True)
+    ctx.kernel_times(reset=True)
+    rb = rk.restarted_krylov(A, b_dev, f, opts, S)
+    kt = ctx.kernel_times(reset=True)
+    ctx.kernel_timing(False)
     if rank == 0:
-        # ---- per-kernel breakdown (separate diagnostic solve, events per launch) ----
-        ctx.kernel_timing(True)
-        ctx.kernel_times(reset=True)
-        rb = rk.restarted_krylov(A, b_dev, f, opts, S)
-        kt = ctx.kernel_times(reset=True)
-        ctx.kernel_timing(False)
-        cb = class_bytes(P, rb.total_m, rb.cycles)
+        cb = class_bytes(w, rb.total_m, rb.cycles)
         peak, peak_src = measured_peaks()
         kernels = {}
         for cls, (kms, cnt) in kt.items():
@@ -283,9 +349,9 @@ def run_ours(args):
         cyc_bytes = sum(cb.values())
         traffic = None  # per-launch DRAM bytes of the committed ncu --set full capture
         try:
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
                 tj = json.load(fh)
-            if args.config == "cfg2" and dom in tj:
+            if world == 1 and args.config == "cfg2" and dom in tj:
                 traffic = tj[dom]["bytes"]
         except Exception:
             pass
@@ -293,19 +359,20 @@ def run_ours(args):
                     "peak": peak, "unit": "GB/s", "frac": dk["frac"],
                     "traffic": traffic, "alg_bytes_per_launch": dk["alg_bytes"] / dk["launches"],
                     "avg_launch_ms": dk["ms"] / dk["launches"], "peak_source": peak_src,
-                    "whole_solve_gbs": cyc_bytes / (max_ms / args.steps / 1e3) / 1e9}
+                    "whole_solve_gbs": cyc_bytes / (max_ms / args.steps / 1e3) / 1e9,
+                    "per_kernel_frac": {c: kernels[c]["frac"] for c in cb
+                                        if "frac" in kernels[c]}}
         cpu = None
         if world == 1:
-            cv, cdt, cr = cpu_baseline_sample(P, 1, 1)
+            cv, cdt, cr = cpu_baseline_sample(w.P, 1, 1)
             cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"one restart cycle (m={P.m}) of {args.config}, single thread, "
+                   "sample": f"one restart cycle (m={w.m}) of {args.config}, single thread, "
                              f"{cdt:.1f} s"}
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generators, BASELINE.json shapes)",
-               "config": dict(workload_desc(P, args.config),
-                              parallelism="replicas" if world > 1 else "single"),
+               "config": w.config,
                "solve": {"cycles": res.cycles, "total_m": res.total_m,
                          "converged": res.converged,
                          "solve_ms": max_ms / args.steps,

@@ -234,6 +234,8 @@ int rkmf_gen_convdiff_upwind(int64_t N, double peclet, double vx, double vy, dou
                              double* h_values);
 /* b[i] = first N(0,1) draw of SplitMix64(derive(seed, i)) (rng.hpp:47-59). */
 int rkmf_gen_gaussian(uint64_t seed, int64_t n, double* h_out);
+/* entries [i0, i0 + n) of the same vector (one rank's slice of b) */
+int rkmf_gen_gaussian_range(uint64_t seed, int64_t i0, int64_t n, double* out);
 
 #ifdef __cplusplus
 }

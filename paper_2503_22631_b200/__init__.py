@@ -130,6 +130,7 @@ SYMBOLS = [
     ("rkmf_gen_q1_hex", C.c_int, [_I64, _I32, _U64, _I32, _P, _P, _P, _P, _P]),
     ("rkmf_gen_convdiff_upwind", C.c_int, [_I64, _D, _D, _D, _D, _P, _P, _P, _P, _P]),
     ("rkmf_gen_gaussian", C.c_int, [_U64, _I64, _P]),
+    ("rkmf_gen_gaussian_range", C.c_int, [_U64, _I64, _I64, _P]),
 ]
 
 _lib = None
@@ -694,6 +695,14 @@ def gen_convdiff_upwind(N: int, peclet: float = 10.0, v=(1.0, 0.5, 0.25)):
     """3D upwind convection-diffusion, 7-point (CSR arrays)."""
     return _gen(lib().rkmf_gen_convdiff_upwind, N, float(peclet), float(v[0]), float(v[1]),
                 float(v[2]))
+
+
+def gen_gaussian_range(seed: int, i0: int, n: int) -> np.ndarray:
+    """Entries [i0, i0 + n) of gen_gaussian(seed, .) (one rank's slice of b)."""
+    out = np.empty(n, np.float64)
+    if lib().rkmf_gen_gaussian_range(C.c_uint64(seed), i0, n, _ptr(out)) != RKMF_OK:
+        raise ParameterError("gen_gaussian_range: bad range")
+    return out
 
 
 def gen_gaussian(seed: int, n: int) -> np.ndarray:

@@ -120,3 +120,68 @@ def algorithmic_bytes_per_cycle(n: int, nnz: int, m: int, rp_bytes: int = 4) -> 
         total += 12 * nnz + rp_bytes * (n + 1) + 8 * n * 4 + 8 * n * (k + 1)
     total += 8 * n + 16 * n + 8 * n * (m + 2)
     return total
+
+
+@dataclass
+class Slab:
+    """One rank's rows of the weak-scaling problem (bench.py --gpus N)."""
+    name: str
+    n_global: int
+    row_starts: np.ndarray
+    row_ptr: np.ndarray   # local row pointers
+    col_idx: np.ndarray   # GLOBAL column indices (int32)
+    values: np.ndarray
+    b: np.ndarray         # local slice
+    nnz: int              # local
+    nnz_global: int
+    fn: str
+    t: float
+    m: int
+    d: int
+    zeta: int
+    tol: float
+    k_max: int
+
+
+def build_slab(world: int, rank: int, N: int = 128) -> Slab:
+    """cfg2 weak-scaled: the 7-point Laplacian on an (N*world) x N x N interior
+    grid (spacing h = 1/(N+1) in every direction, Dirichlet boundary
+    eliminated, scaled by h^-2), lexicographic order (ix*N + iy)*N + iz, so
+    rank r owns the x-slab ix in [rN, (r+1)N): exactly cfg2's rows and stencil
+    per rank, with one N^2 halo plane to each neighbour. Only the rank's rows
+    are generated. f = exp(-tA), t = 500 / lambda_max, m = 50, d = 200."""
+    cfg = CONFIGS["cfg2"]
+    Nx, plane = N * world, N * N
+    n_global = Nx * plane
+    h = 1.0 / (N + 1)
+    s = 1.0 / (h * h)
+    r0, r1 = rank * N * plane, (rank + 1) * N * plane
+    rows = np.arange(r0, r1, dtype=np.int64)
+    ix, iy, iz = rows // plane, (rows // N) % N, rows % N
+    # neighbours in increasing column order: -x, -y, -z, self, +z, +y, +x
+    offs = [-plane, -N, -1, 0, 1, N, plane]
+    ok = [ix > 0, iy > 0, iz > 0, np.ones_like(ix, bool), iz < N - 1, iy < N - 1, ix < Nx - 1]
+    cols = np.stack([rows + o for o in offs], axis=1)
+    vals = np.where(np.arange(7) == 3, 6.0 * s, -s)[None, :].repeat(len(rows), 0)
+    mask = np.stack(ok, axis=1)
+    row_ptr = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(mask.sum(1), out=row_ptr[1:])
+    col_idx = cols[mask].astype(np.int32)
+    values = vals[mask].astype(np.float64)
+    lam = lap_lambda_max(3, N) if world == 1 else (4.0 / (h * h)) * (
+        math.sin(Nx * math.pi / (2 * Nx + 2)) ** 2 + 2 * math.sin(N * math.pi / (2 * N + 2)) ** 2)
+    from . import gen_gaussian_range
+    b = gen_gaussian_range(B_SEED, r0, r1 - r0)
+    # ||b||_2 of the global vector without materialising it: sum of squares of
+    # every rank's slice is deterministic, so compute it slab by slab
+    ss = 0.0
+    for q in range(world):
+        ss += float(np.dot(*(2 * [gen_gaussian_range(B_SEED, q * N * plane, N * plane)])))
+    # 7 per row minus one per missing neighbour: two boundary faces per axis
+    nnz_global = 7 * n_global - 2 * (N * N + Nx * N + Nx * N)
+    row_starts = np.arange(world + 1, dtype=np.int64) * N * plane
+    return Slab(name="cfg2-slab", n_global=n_global, row_starts=row_starts, row_ptr=row_ptr,
+                col_idx=col_idx, values=values, b=b, nnz=int(row_ptr[-1]),
+                nnz_global=int(nnz_global), fn="exp_neg", t=cfg["c"] / lam, m=cfg["m"],
+                d=cfg["d"], zeta=cfg["zeta"], tol=cfg["tol_rel"] * math.sqrt(ss),
+                k_max=BUDGET_TOTAL_M // cfg["m"])

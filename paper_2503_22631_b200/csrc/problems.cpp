@@ -55,8 +55,14 @@ double gaussian_at(uint64_t seed, uint64_t i) {  // next_gaussian(0,1), rng.hpp:
 extern "C" {
 
 int rkmf_gen_gaussian(uint64_t seed, int64_t n, double* out) {
+  return rkmf_gen_gaussian_range(seed, 0, n, out);
+}
+
+// entries [i0, i0 + n) of the same vector: one rank's slice of b
+int rkmf_gen_gaussian_range(uint64_t seed, int64_t i0, int64_t n, double* out) {
+  if (i0 < 0 || n < 0) return RKMF_PARAMETER_ERROR;
   par_rows(n, [&](int64_t lo, int64_t hi) {
-    for (int64_t i = lo; i < hi; ++i) out[i] = gaussian_at(seed, uint64_t(i));
+    for (int64_t i = lo; i < hi; ++i) out[i] = gaussian_at(seed, uint64_t(i0 + i));
   });
   return RKMF_OK;
 }

@@ -68,8 +68,10 @@ def make_context(device: int, nranks: int, rank: int, transport: str) -> Context
         import torch.distributed as dist
         uid = nccl_unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(np.frombuffer(uid, np.uint8).copy())
+        if dist.get_backend() == "nccl":  # a pure-NCCL group moves CUDA tensors only
+            t = t.cuda(device)
         dist.broadcast(t, src=0)
-        init_comm(ctx, nranks, rank, bytes(t.numpy().tobytes()))
+        init_comm(ctx, nranks, rank, bytes(t.cpu().numpy().tobytes()))
     elif transport == "host":
         init_host_comm(ctx, nranks, rank, gloo_allreduce, gloo_alltoallv)
     else:
@@ -100,6 +102,17 @@ def partition(ctx: Context, row_ptr, col_idx, values, b, d: int, zeta: int, seed
     S = partitioned_sketch(ctx, d, n, zeta, seed, rb, re - rb)
     return RankPart(ctx=ctx, row_starts=rs, row_begin=rb, n_local=re - rb, A=A, S=S,
                     b=np.ascontiguousarray(b[rb:re]))
+
+
+def partition_local(ctx: Context, n_global: int, row_starts, row_ptr_local, col_global,
+                    values_local, b_local, d: int, zeta: int, seed: int, rank: int) -> RankPart:
+    """This rank's objects from rows generated locally (global column ids)."""
+    rs = np.asarray(row_starts, np.int64)
+    A = partitioned_matrix(ctx, n_global, rs, row_ptr_local, col_global, values_local)
+    rb, re = int(rs[rank]), int(rs[rank + 1])
+    S = partitioned_sketch(ctx, d, n_global, zeta, seed, rb, re - rb)
+    return RankPart(ctx=ctx, row_starts=rs, row_begin=rb, n_local=re - rb, A=A, S=S,
+                    b=np.ascontiguousarray(b_local, np.float64))
 
 
 def solve(part: RankPart, f: FunctionSpec, opts: RestartOptions, b_local=None,
