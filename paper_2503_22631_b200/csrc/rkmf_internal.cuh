@@ -120,20 +120,21 @@ struct SketchView {
 __host__ __device__ inline int64_t tile_off_stride(int64_t d) { return (2 * d + 1 + 7) / 8 * 8; }
 
 // Sketch epilogue of one 128-row tile (sketch.cpp:51-63 as a gather): thread t
-// of 128 sums the tile's contributions to the slots it owns and adds them to
-// acc[bin]. Slots are sorted by length, and thread t takes slots t, 255-t,
-// 256+t, 511-t, ... (snake), so each warp walks 32 slots of near-equal length
-// and every thread gets about the same number of entries. zs2 holds the scaled
+// of NT sums the tile's contributions to the slots it owns and adds them to
+// acc[bin]. Slots are sorted by length, and thread t takes slots t,
+// 2NT-1-t, 2NT+t, 4NT-1-t, ... (snake), so each warp walks 32 slots of
+// near-equal length and every thread gets about the same number of entries. zs2 holds the scaled
 // z of the tile's rows twice, zs2[r] = +z_r and zs2[128 + r] = -z_r, so an
 // entry byte (local row | sign << 7) indexes its signed value directly. Reading
 // one entry past a slot's end stays inside shared memory (the stage layouts
 // place zs2 after the entries) and is masked.
+template <int NT = 128>
 __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t* off,
                                                    const uint8_t* ent, const double* zs2,
                                                    double* acc) {
   const uint16_t* bins = off + d + 1;
-  for (int j = 0; 128 * j < d; ++j) {
-    const int s = (j & 1) ? 128 * j + 127 - t : 128 * j + t;
+  for (int j = 0; NT * j < d; ++j) {
+    const int s = (j & 1) ? NT * j + NT - 1 - t : NT * j + t;
     if (s >= d) continue;
     const int e0 = off[s], e1 = off[s + 1];
     double a0 = 0.0, a1 = 0.0;

@@ -28,12 +28,9 @@ namespace rkmf_b200 {
 
 namespace {
 
-constexpr int kConsumers = 128;  // = kTileRows, one row per consumer thread
-constexpr int kPipeThreads = kConsumers + 32;
-constexpr int kStages = 4;
-__device__ __forceinline__ void named_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
-}
+
+constexpr int kStages = 8;
+
 
 struct StageLayout {
   uint32_t rp, val, col, off, ent, zs, meta, stride;
@@ -67,8 +64,25 @@ struct TileMeta {
   int vshift, cshift;
 };
 
-template <typename RP>
-__global__ void __launch_bounds__(kPipeThreads)
+// Thread roles of one block (warp-specialised):
+//   [0, G*128*TPR)        SpMV threads: G groups, group g takes the block's
+//                         tiles it = g, g+G, ...; TPR threads per row
+//   next kSketchThreads   sketch threads: every tile in order, from shared memory
+//   last warp             producer: one elected lane issues the bulk copies
+// Per stage s (ring of NS >= G + 2): full[s] (producer tx bytes) -> the SpMV
+// group writes z and the signed z table into the stage and arrives on zsr[s]
+// -> the sketch threads gather the tile's bins and arrive on empty[s] -> the
+// producer refills. The SpMV groups never wait for the sketch, so G tiles'
+// x gathers are in flight per block while the sketch of an older tile runs.
+constexpr int kSketchThreads = 128;
+
+template <int TPR, int G>
+constexpr int spmv_threads() { return G * kTileRows * TPR; }
+template <int TPR, int G>
+constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads + 32; }
+
+template <typename RP, int TPR, int G>
+__global__ void __launch_bounds__(block_threads<TPR, G>())
     spmv_sketch_pipe_kernel(int64_t n, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ val, const double* __restrict__ x,
                             const double* xscale, double* __restrict__ z, int64_t num_tiles,
@@ -76,29 +90,31 @@ __global__ void __launch_bounds__(kPipeThreads)
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
                             double sscale, double* pacc, const int32_t* stop, int step,
                             int nstages, int l2_hints, int debug) {
+  constexpr int kSpmv = spmv_threads<TPR, G>();
+  constexpr int kGroup = kTileRows * TPR;
   extern __shared__ __align__(128) unsigned char smem[];
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d]
+  __shared__ __align__(8) uint64_t full[kStages], zsr[kStages], empty[kStages];
+  double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d], sketch threads
   const int t = threadIdx.x;
   if (t == 0) {
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
+      mbar_init(&zsr[s], kGroup);
+      mbar_init(&empty[s], kSketchThreads);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int b = t; b < d; b += kPipeThreads) acc[b] = 0.0;
+  for (int b = t; b < d; b += block_threads<TPR, G>()) acc[b] = 0.0;
   __syncthreads();
   pdl_wait_then_trigger();  // x, pacc and the stop flag come from earlier kernels
   if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
 
-  if (t >= kConsumers) {  // ---------------- producer warp ----------------
-    if (t != kConsumers) return;
+  if (t >= kSpmv + kSketchThreads) {  // ---------------- producer warp ----------------
+    if (t != kSpmv + kSketchThreads) return;
     const uint64_t pol = l2_policy(l2_hints >= 1 ? 1 : 0);
     // the sketch tile layout is re-read every step: ask L2 to keep it
     const uint64_t mpol = l2_policy(l2_hints);
-    int it = 0;
     // row-pointer pair of the next tile, prefetched one iteration ahead so the
     // bulk copies of a tile are issued without a dependent global round trip
     long long nrs = 0, nre = 0;
@@ -107,7 +123,7 @@ __global__ void __launch_bounds__(kPipeThreads)
       nrs = (long long)rp[r0];
       nre = (long long)rp[min(n, r0 + kTileRows)];
     }
-    int s = 0;
+    int s = 0, it = 0;
     uint32_t eph = 0;  // parity of the empty barrier round being waited for
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const long long rs = nrs, re = nre;
@@ -146,85 +162,85 @@ __global__ void __launch_bounds__(kPipeThreads)
     return;
   }
 
-  // ---------------- consumer warps: one row per thread ----------------
-  // Software-pipelined by one tile: the x gathers of tile i are issued, then
-  // the sketch gather of tile i-1 runs from shared memory while they are in
-  // flight, then tile i's row sums finish. The consumers therefore hold two
-  // stages (i-1 until its sketch is gathered, and i).
-  const double xs = xscale ? *xscale : 1.0;
-  int s = 0, ps = -1;  // current stage; stage of the tile whose sketch is pending
-  uint32_t fph = 0;    // parity of the full barrier round being waited for
-  auto gather_prev = [&] {
-    if (ps < 0) return;
-    unsigned char* pst = smem + ps * L.stride;
-    if (!(debug & 1))
-      sketch_tile_gather(t, d, reinterpret_cast<const uint16_t*>(pst + L.off), pst + L.ent,
-                         reinterpret_cast<const double*>(pst + L.zs), acc);
-    mbar_arrive(&empty[ps]);
-  };
-  for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-    mbar_wait(&full[s], fph);
-    unsigned char* st = smem + s * L.stride;
-    if (debug & 4) {  // ablation: stream only
+  if (t >= kSpmv) {  // ---------------- sketch threads ----------------
+    const int u = t - kSpmv;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&zsr[s], ph);
+      mbar_wait(&full[s], ph);  // completed already (the SpMV group waited on it)
+      unsigned char* st = smem + s * L.stride;
+      if (!(debug & 1))
+        sketch_tile_gather<kSketchThreads>(u, d, reinterpret_cast<const uint16_t*>(st + L.off),
+                                           st + L.ent,
+                                           reinterpret_cast<const double*>(st + L.zs), acc);
+      // orders this tile's acc updates before the next tile's (slot -> bin
+      // ownership changes per tile)
+      asm volatile("bar.sync 2, %0;" ::"n"(kSketchThreads) : "memory");
       mbar_arrive(&empty[s]);
-      if (++s == nstages) { s = 0; fph ^= 1u; }
-      continue;
-    }
-    const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
-    double* zs = reinterpret_cast<double*>(st + L.zs);
-    const TileMeta meta = *reinterpret_cast<const TileMeta*>(st + L.meta);
-    const double* vals = reinterpret_cast<const double*>(st + L.val) + meta.vshift;
-    const int32_t* cols = reinterpret_cast<const int32_t*>(st + L.col) + meta.cshift;
-    const int64_t row = tile * kTileRows + t;
-    const bool live = row < n;
-    int lo = 0, hi = 0;
-    if (live) {
-      lo = int((long long)rps[t] - meta.rs);
-      hi = int((long long)rps[t + 1] - meta.rs);
-    }
-    // first 8 nonzeros: gathers in flight across the previous tile's sketch.
-    // Lanes past the row end re-read the row's last column (a valid index the
-    // row already uses) and contribute a zero product.
-    double v[8], xv[8];
-    if (lo < hi) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int ee = min(lo + q, hi - 1);
-        v[q] = vals[ee];
-        xv[q] = (debug & 2) ? double(cols[ee]) : __ldg(x + cols[ee]);
+      if (++s == nstages) {
+        s = 0;
+        ph ^= 1u;
       }
     }
-    gather_prev();
-    double sum = 0.0;
-    if (lo < hi) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) sum += (lo + q < hi ? v[q] : 0.0) * xv[q];
-      for (int e = lo + 8; e < hi; e += 8) {  // long rows (27-point stencils)
+    for (int b = u; b < d; b += kSketchThreads) atomicAdd(pacc + b, acc[b]);
+    return;
+  }
+
+  // ---------------- SpMV threads: group g, TPR threads per row ----------------
+  // Adjacent lanes of a row take its nonzeros round-robin and combine their
+  // partial sums with a fixed butterfly (deterministic). 8 gathers per thread
+  // are in flight before the first FMA; lanes past the row end re-read the
+  // row's last column (a valid index the row already uses) and contribute a
+  // zero product.
+  const double xs = xscale ? *xscale : 1.0;
+  const int g = t / kGroup, gt = t % kGroup;
+  const int rl = gt / TPR, part = gt % TPR;
+  int it = g;
+  int s = g % nstages;
+  for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
+       tile += int64_t(G) * gridDim.x, it += G) {
+    mbar_wait(&full[s], uint32_t(it / nstages) & 1u);
+    unsigned char* st = smem + s * L.stride;
+    if (!(debug & 4)) {
+      const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
+      double* zs = reinterpret_cast<double*>(st + L.zs);
+      const TileMeta meta = *reinterpret_cast<const TileMeta*>(st + L.meta);
+      const double* vals = reinterpret_cast<const double*>(st + L.val) + meta.vshift;
+      const int32_t* cols = reinterpret_cast<const int32_t*>(st + L.col) + meta.cshift;
+      const int64_t row = tile * kTileRows + rl;
+      const bool live = row < n;
+      int lo = 0, hi = 0;
+      if (live) {
+        lo = int((long long)rps[rl] - meta.rs);
+        hi = int((long long)rps[rl + 1] - meta.rs);
+      }
+      double sum = 0.0;
+      for (int e = lo + part; e < hi; e += 8 * TPR) {
+        double v[8], xv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const int ee = min(e + q, hi - 1);
+          const int ee = min(e + TPR * q, hi - 1);
           v[q] = vals[ee];
           xv[q] = (debug & 2) ? double(cols[ee]) : __ldg(x + cols[ee]);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) sum += (e + q < hi ? v[q] : 0.0) * xv[q];
+        for (int q = 0; q < 8; ++q) sum += (e + TPR * q < hi ? v[q] : 0.0) * xv[q];
+      }
+#pragma unroll
+      for (int o = 1; o < TPR; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      sum *= xs;
+      if (part == 0) {
+        if (live) z[row] = sum;
+        const double zt = live ? sum * sscale : 0.0;
+        zs[rl] = zt;
+        zs[kTileRows + rl] = -zt;
       }
     }
-    sum *= xs;
-    if (live) z[row] = sum;
-    const double zt = live ? sum * sscale : 0.0;
-    zs[t] = zt;
-    zs[kConsumers + t] = -zt;
-    named_sync();  // zs2 of this tile complete; orders acc updates across threads
-    ps = s;
-    if (++s == nstages) {
-      s = 0;
-      fph ^= 1u;
-    }
+    mbar_arrive(&zsr[s]);
+    s += G;
+    while (s >= nstages) s -= nstages;
   }
-  gather_prev();
-  named_sync();  // acc[b] may have been written by another consumer thread
-  for (int b = t; b < d; b += kConsumers) atomicAdd(pacc + b, acc[b]);
 }
 
 template <typename RP>
@@ -276,29 +292,39 @@ int sms() {
   return v;
 }
 
-template <typename RP>
+template <typename RP, int TPR, int G>
 bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
                    int step, cudaStream_t st) {
+  constexpr int kThreads = block_threads<TPR, G>();
   const int off_stride = int(tile_off_stride(S->d));
-  auto fn = spmv_sketch_pipe_kernel<RP>;
-  // Pick the stage count that maximises consumer warps per SM while keeping
-  // at least one tile in flight ahead of the consumers (cached per shape).
+  auto fn = spmv_sketch_pipe_kernel<RP, TPR, G>;
+  // Pick the stage count. G stages feed the SpMV groups and one the sketch,
+  // so (stages - G - 1) x resident blocks x stage bytes are in flight ahead
+  // of them: take the configuration that keeps >= 64 KB per SM ahead (HBM
+  // latency x per-SM bandwidth), then the one with more resident blocks, then
+  // more stages. Cached per shape.
   static thread_local int64_t key_c = -1;
   static thread_local int best_s = 0, best_per = 0;
   const int64_t key = (int64_t(A->cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP);
   if (key != key_c) {
     best_s = 0;
     best_per = 0;
-    for (int s = 3; s <= kStages; ++s) {  // consumers hold 2 stages (pipelined)
+    int64_t best_ahead = -1;
+    const int64_t stride = int64_t(stage_layout(int(sizeof(RP)), A->cap, off_stride,
+                                                int(S->zeta)).stride);
+    for (int s = G + 2; s <= kStages; ++s) {
       if (env_stages() && s != env_stages()) continue;
       const size_t sm = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta), s);
       if (sm > 220 * 1024) continue;
       RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
       int per = 0;
-      RKMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kPipeThreads, sm));
-      // prefer more resident blocks; on a tie, more stages
-      if (per > 0 && (per > best_per || (per == best_per && s > best_s))) {
+      RKMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, sm));
+      if (per <= 0) continue;
+      const int64_t ahead = std::min<int64_t>(int64_t(per) * (s - G - 1) * stride, 64 * 1024);
+      if (ahead > best_ahead || (ahead == best_ahead && per > best_per) ||
+          (ahead == best_ahead && per == best_per && s > best_s)) {
+        best_ahead = ahead;
         best_per = per;
         best_s = s;
       }
@@ -311,11 +337,63 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
-  launch_maybe_pdl(fn, dim3(grid), dim3(kPipeThreads), smem, st, A->n_rows,
+  launch_maybe_pdl(fn, dim3(grid), dim3(kThreads), smem, st, A->n_rows,
                    static_cast<const RP*>(A->row_ptr), A->col, A->val, x, xscale_dev, z, tiles,
                    A->cap, int(S->d), int(S->zeta), off_stride, S->tile_off, S->tile_ent,
                    S->scale, pacc, stop, step, stages, env_l2_hints(), env_debug());
   return true;
+}
+
+// Threads per row: enough that each thread's first 8 gathers cover an average
+// row (RKMF_PIPE_TPR=1|2|4 overrides).
+int pick_tpr(const CsrView* A) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("RKMF_PIPE_TPR");
+    env = e ? atoi(e) : 0;
+  }
+  if (env == 1 || env == 2 || env == 4) return env;
+  const double avg = A->n_rows ? double(A->nnz) / double(A->n_rows) : 0.0;
+  return avg <= 10.0 ? 1 : (avg <= 40.0 ? 2 : 4);
+}
+
+// SpMV groups per block: one for short rows (its tiles are small, several
+// blocks fit per SM), two for long rows (one block per SM; two tiles' gathers
+// in flight). RKMF_PIPE_GROUPS=1|2|3 overrides.
+int pick_groups(const CsrView* A) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("RKMF_PIPE_GROUPS");
+    env = e ? atoi(e) : 0;
+  }
+  if (env >= 1 && env <= 3) return env;
+  const double avg = A->n_rows ? double(A->nnz) / double(A->n_rows) : 0.0;
+  return avg <= 10.0 ? 1 : 2;
+}
+
+template <typename RP, int TPR>
+bool launch_pipe_g(const CsrView* A, const SketchView* S, const double* x,
+                   const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
+                   int step, cudaStream_t st) {
+  // at most 1024 threads per block: TPR 4 runs one group, TPR 2 up to three
+  int g = pick_groups(A);
+  while (g > 1 && g * kTileRows * TPR + kSketchThreads + 32 > 1024) --g;
+  if (g >= 3 && TPR <= 2)
+    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 3 : 1)>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+  if (g == 2 && TPR <= 2)
+    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 2 : 1)>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+  return launch_pipe_t<RP, TPR, 1>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+}
+
+template <typename RP>
+bool launch_pipe_rp(const CsrView* A, const SketchView* S, const double* x,
+                    const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
+                    int step, cudaStream_t st) {
+  switch (pick_tpr(A)) {
+    case 4: return launch_pipe_g<RP, 4>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+    case 2: return launch_pipe_g<RP, 2>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+    default: return launch_pipe_g<RP, 1>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+  }
 }
 
 }  // namespace
@@ -324,8 +402,8 @@ bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double
                              const double* xscale_dev, double* z, double* pacc,
                              const int32_t* stop_flag, int step, cudaStream_t st) {
   if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
-  return A->rp64 ? launch_pipe_t<int64_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
-                 : launch_pipe_t<int32_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
+  return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
+                 : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
 }
 
 }  // namespace rkmf_b200
