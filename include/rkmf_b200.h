@@ -217,6 +217,15 @@ int rkmf_partition_halo(int32_t nranks, int32_t rank, const int64_t* row_starts,
                         const int64_t* row_ptr_local, const int32_t* col_global, int64_t* n_halo,
                         int64_t* halo_global, int64_t* recv_counts, int32_t* col_local);
 
+/* ---- on-device generators of the BASELINE matrices (same entries as the
+ * host rkmf_gen_* below; cfg5's 3.6e9 nonzeros never touch the host) ---- */
+int rkmf_matrix_gen_q1_hex(rkmf_context* ctx, int64_t N, int32_t lognormal, uint64_t coef_seed,
+                           int32_t dirichlet, rkmf_matrix** out);
+int rkmf_matrix_gen_laplacian(rkmf_context* ctx, int32_t dim, int64_t N, rkmf_matrix** out);
+/* d_out[i] = gaussian(seed, i0 + i) on the device (rng.hpp:47-59) */
+int rkmf_gen_gaussian_device(rkmf_context* ctx, uint64_t seed, int64_t i0, int64_t n,
+                             double* d_out);
+
 /* R_accum of the last solve on this context (total_m x total_m, column-major,
  * host); n_cap is the caller's capacity in rows. */
 int rkmf_last_r_accum(rkmf_context* ctx, double* h_R, int64_t n_cap, int64_t* total_m);

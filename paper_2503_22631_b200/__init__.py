@@ -131,6 +131,9 @@ SYMBOLS = [
     ("rkmf_gen_convdiff_upwind", C.c_int, [_I64, _D, _D, _D, _D, _P, _P, _P, _P, _P]),
     ("rkmf_gen_gaussian", C.c_int, [_U64, _I64, _P]),
     ("rkmf_gen_gaussian_range", C.c_int, [_U64, _I64, _I64, _P]),
+    ("rkmf_matrix_gen_q1_hex", C.c_int, [_P, _I64, _I32, _U64, _I32, _PP]),
+    ("rkmf_matrix_gen_laplacian", C.c_int, [_P, _I32, _I64, _PP]),
+    ("rkmf_gen_gaussian_device", C.c_int, [_P, _U64, _I64, _I64, _P]),
 ]
 
 _lib = None
@@ -264,6 +267,24 @@ class SparseMatrix:
         h = C.c_void_p()
         ctx.check(lib().rkmf_matrix_create_host(ctx.h, n, n if n_cols is None else n_cols,
                                                 _ptr(rp), _ptr(ci), _ptr(v), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def q1_hex(cls, N: int, lognormal: bool = False, coef_seed: int = 1, dirichlet: bool = False,
+               ctx: Optional[Context] = None) -> "SparseMatrix":
+        """Q1 hexahedral stiffness on N^3 nodes, generated in HBM (cfg3, cfg5)."""
+        ctx = ctx or Context.default()
+        h = C.c_void_p()
+        ctx.check(lib().rkmf_matrix_gen_q1_hex(ctx.h, N, int(lognormal), C.c_uint64(coef_seed),
+                                               int(dirichlet), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def laplacian(cls, dim: int, N: int, ctx: Optional[Context] = None) -> "SparseMatrix":
+        """5/7-point Dirichlet Laplacian (h^-2 scaled), generated in HBM (cfg1, cfg2)."""
+        ctx = ctx or Context.default()
+        h = C.c_void_p()
+        ctx.check(lib().rkmf_matrix_gen_laplacian(ctx.h, dim, N, C.byref(h)))
         return cls(ctx, h)
 
     @classmethod
@@ -695,6 +716,15 @@ def gen_convdiff_upwind(N: int, peclet: float = 10.0, v=(1.0, 0.5, 0.25)):
     """3D upwind convection-diffusion, 7-point (CSR arrays)."""
     return _gen(lib().rkmf_gen_convdiff_upwind, N, float(peclet), float(v[0]), float(v[1]),
                 float(v[2]))
+
+
+def gen_gaussian_device(seed: int, i0: int, n: int, ctx: Optional[Context] = None):
+    """gen_gaussian_range on the device: a float64 CUDA tensor."""
+    import torch
+    ctx = ctx or Context.default()
+    out = torch.empty(n, dtype=torch.float64, device=f"cuda:{ctx.device}")
+    ctx.check(lib().rkmf_gen_gaussian_device(ctx.h, C.c_uint64(seed), i0, n, out.data_ptr()))
+    return out
 
 
 def gen_gaussian_range(seed: int, i0: int, n: int) -> np.ndarray:

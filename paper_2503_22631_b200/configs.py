@@ -185,3 +185,63 @@ def build_slab(world: int, rank: int, N: int = 128) -> Slab:
                 nnz_global=int(nnz_global), fn="exp_neg", t=cfg["c"] / lam, m=cfg["m"],
                 d=cfg["d"], zeta=cfg["zeta"], tol=cfg["tol_rel"] * math.sqrt(ss),
                 k_max=BUDGET_TOTAL_M // cfg["m"])
+
+
+@dataclass
+class DeviceProblem:
+    """A BASELINE config generated in HBM (cfg5's 3.6e9 nonzeros never touch
+    the host): the device matrix, the device b, and the solver parameters."""
+    name: str
+    n: int
+    nnz: int
+    A: object   # SparseMatrix
+    b: object   # float64 CUDA tensor
+    fn: str
+    t: float
+    m: int
+    d: int
+    zeta: int
+    tol: float
+    k_max: int
+    norm2: float
+
+
+def device_power_norm2(A, iters: int = 60, seed: int = 7) -> float:
+    """||A||_2 of a symmetric device matrix by a fixed-seed power iteration
+    (the host power_norm2 on the device: same start vector, same count)."""
+    from . import gen_gaussian_device, spmv
+    x = gen_gaussian_device(seed, 0, A.n_rows, A.ctx)
+    x /= x.norm()
+    lam = 0.0
+    for _ in range(iters):
+        y = spmv(A, x)
+        lam = float(y.norm())
+        x = y / lam
+    return lam
+
+
+def build_device(name: str, N: Optional[int] = None, ctx=None) -> DeviceProblem:
+    """Config `name` generated on the device (Laplacians and Q1; cfg4's
+    upwind operator has no device generator and uses build())."""
+    from . import Context, SparseMatrix, gen_gaussian_device
+    cfg = dict(CONFIGS[name])
+    N = int(N or cfg["N"])
+    ctx = ctx or Context.default()
+    kind = cfg["kind"]
+    if kind == "lap2d":
+        A = SparseMatrix.laplacian(2, N, ctx)
+        norm2 = lap_lambda_max(2, N)
+    elif kind == "lap3d":
+        A = SparseMatrix.laplacian(3, N, ctx)
+        norm2 = lap_lambda_max(3, N)
+    elif kind == "q1":
+        A = SparseMatrix.q1_hex(N, cfg["lognormal"], COEF_SEED, cfg["dirichlet"], ctx)
+        norm2 = device_power_norm2(A) if cfg["fn"] == "exp_neg" else 0.0
+    else:
+        raise ValueError(f"{name}: no device generator for {kind}")
+    b = gen_gaussian_device(B_SEED, 0, A.n_rows, ctx)
+    t = cfg["c"] / norm2 if cfg["fn"] == "exp_neg" else 1.0
+    return DeviceProblem(name=name, n=A.n_rows, nnz=A.nnz, A=A, b=b, fn=cfg["fn"], t=t,
+                         m=cfg["m"], d=cfg["d"], zeta=cfg["zeta"],
+                         tol=cfg["tol_rel"] * float(b.norm()), k_max=BUDGET_TOTAL_M // cfg["m"],
+                         norm2=norm2)

@@ -108,70 +108,6 @@ __global__ void tile_nnz_max_kernel(int64_t n, const int64_t* __restrict__ rp,
   }
 }
 
-rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
-                                     int64_t nnz, const int64_t* rp64_dev,
-                                     const int32_t* col_dev, const double* val_dev,
-                                     bool copy_colval, bool require_sorted = true) {
-  auto* M = new rkmf_matrix();
-  M->ctx = ctx;
-  M->device = ctx->device;
-  M->view.n_rows = n_rows;
-  M->view.n_cols = n_cols;
-  M->view.nnz = nnz;
-  try {
-    const bool rp64 = nnz >= (int64_t(1) << 31) - 1;
-    M->view.rp64 = rp64;
-    // tail padding: the TMA-pipelined SpMV rounds its bulk copies up to 16 B
-    const size_t rp_elems = size_t(n_rows + 1 + kRpPad);
-    if (rp64) {
-      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int64_t) * rp_elems));
-      RKMF_CUDA(cudaMemsetAsync(M->rp, 0, sizeof(int64_t) * rp_elems, ctx->stream));
-      RKMF_CUDA(cudaMemcpyAsync(M->rp, rp64_dev, sizeof(int64_t) * size_t(n_rows + 1),
-                                cudaMemcpyDeviceToDevice, ctx->stream));
-    } else {
-      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int32_t) * rp_elems));
-      RKMF_CUDA(cudaMemsetAsync(M->rp, 0, sizeof(int32_t) * rp_elems, ctx->stream));
-      rp_narrow_kernel<<<256, 256, 0, ctx->stream>>>(n_rows, rp64_dev,
-                                                     static_cast<int32_t*>(M->rp));
-      RKMF_CUDA(cudaGetLastError());
-      ctx->launches++;
-    }
-    if (!copy_colval) {  // caller-allocated with kNnzPad elements of padding
-      M->col = const_cast<int32_t*>(col_dev);
-      M->val = const_cast<double*>(val_dev);
-    } else {
-      RKMF_CUDA(cudaMalloc(&M->col, sizeof(int32_t) * size_t(nnz + kNnzPad)));
-      RKMF_CUDA(cudaMalloc(&M->val, sizeof(double) * size_t(nnz + kNnzPad)));
-      RKMF_CUDA(cudaMemsetAsync(M->col, 0, sizeof(int32_t) * size_t(nnz + kNnzPad), ctx->stream));
-      RKMF_CUDA(cudaMemsetAsync(M->val, 0, sizeof(double) * size_t(nnz + kNnzPad), ctx->stream));
-      if (nnz > 0) {
-        RKMF_CUDA(cudaMemcpyAsync(M->col, col_dev, sizeof(int32_t) * size_t(nnz),
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
-        RKMF_CUDA(cudaMemcpyAsync(M->val, val_dev, sizeof(double) * size_t(nnz),
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
-      }
-    }
-    unsigned long long* mx = reinterpret_cast<unsigned long long*>(ctx->scratch.ensure(64));
-    RKMF_CUDA(cudaMemsetAsync(mx, 0, 8, ctx->stream));
-    tile_nnz_max_kernel<<<256, 256, 0, ctx->stream>>>(n_rows, rp64_dev, mx);
-    RKMF_CUDA(cudaGetLastError());
-    ctx->launches++;
-    unsigned long long hmx = 0;
-    RKMF_CUDA(cudaMemcpyAsync(&hmx, mx, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
-    M->view.max_tile_nnz = int64_t(hmx);
-    M->view.padded = true;
-    finish_matrix(M, int64_t(hmx), require_sorted);
-  } catch (...) {
-    if (M->rp) cudaFree(M->rp);
-    if (copy_colval && M->col) cudaFree(M->col);
-    if (copy_colval && M->val) cudaFree(M->val);
-    delete M;
-    throw;
-  }
-  return M;
-}
-
 double host_norm(const double* x, int64_t n) {
   double s = 0.0;
   for (int64_t i = 0; i < n; ++i) s += x[i] * x[i];
@@ -271,6 +207,72 @@ void copy_in(rkmf_context* ctx, double* dst, const double* src, int64_t n, bool 
 }
 
 }  // namespace
+
+// host/device CSR -> validated device matrix (also used by gen.cu)
+rkmf_matrix* rkmf_b200::create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
+                                     int64_t nnz, const int64_t* rp64_dev,
+                                     const int32_t* col_dev, const double* val_dev,
+                                     bool copy_colval, bool require_sorted) {
+  auto* M = new rkmf_matrix();
+  M->ctx = ctx;
+  M->device = ctx->device;
+  M->view.n_rows = n_rows;
+  M->view.n_cols = n_cols;
+  M->view.nnz = nnz;
+  try {
+    const bool rp64 = nnz >= (int64_t(1) << 31) - 1;
+    M->view.rp64 = rp64;
+    // tail padding: the TMA-pipelined SpMV rounds its bulk copies up to 16 B
+    const size_t rp_elems = size_t(n_rows + 1 + kRpPad);
+    if (rp64) {
+      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int64_t) * rp_elems));
+      RKMF_CUDA(cudaMemsetAsync(M->rp, 0, sizeof(int64_t) * rp_elems, ctx->stream));
+      RKMF_CUDA(cudaMemcpyAsync(M->rp, rp64_dev, sizeof(int64_t) * size_t(n_rows + 1),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      RKMF_CUDA(cudaMalloc(&M->rp, sizeof(int32_t) * rp_elems));
+      RKMF_CUDA(cudaMemsetAsync(M->rp, 0, sizeof(int32_t) * rp_elems, ctx->stream));
+      rp_narrow_kernel<<<256, 256, 0, ctx->stream>>>(n_rows, rp64_dev,
+                                                     static_cast<int32_t*>(M->rp));
+      RKMF_CUDA(cudaGetLastError());
+      ctx->launches++;
+    }
+    if (!copy_colval) {  // caller-allocated with kNnzPad elements of padding
+      M->col = const_cast<int32_t*>(col_dev);
+      M->val = const_cast<double*>(val_dev);
+    } else {
+      RKMF_CUDA(cudaMalloc(&M->col, sizeof(int32_t) * size_t(nnz + kNnzPad)));
+      RKMF_CUDA(cudaMalloc(&M->val, sizeof(double) * size_t(nnz + kNnzPad)));
+      RKMF_CUDA(cudaMemsetAsync(M->col, 0, sizeof(int32_t) * size_t(nnz + kNnzPad), ctx->stream));
+      RKMF_CUDA(cudaMemsetAsync(M->val, 0, sizeof(double) * size_t(nnz + kNnzPad), ctx->stream));
+      if (nnz > 0) {
+        RKMF_CUDA(cudaMemcpyAsync(M->col, col_dev, sizeof(int32_t) * size_t(nnz),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+        RKMF_CUDA(cudaMemcpyAsync(M->val, val_dev, sizeof(double) * size_t(nnz),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    }
+    unsigned long long* mx = reinterpret_cast<unsigned long long*>(ctx->scratch.ensure(64));
+    RKMF_CUDA(cudaMemsetAsync(mx, 0, 8, ctx->stream));
+    tile_nnz_max_kernel<<<256, 256, 0, ctx->stream>>>(n_rows, rp64_dev, mx);
+    RKMF_CUDA(cudaGetLastError());
+    ctx->launches++;
+    unsigned long long hmx = 0;
+    RKMF_CUDA(cudaMemcpyAsync(&hmx, mx, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    M->view.max_tile_nnz = int64_t(hmx);
+    M->view.padded = true;
+    finish_matrix(M, int64_t(hmx), require_sorted);
+  } catch (...) {
+    if (M->rp) cudaFree(M->rp);
+    if (copy_colval && M->col) cudaFree(M->col);
+    if (copy_colval && M->val) cudaFree(M->val);
+    delete M;
+    throw;
+  }
+  return M;
+}
+
 
 // ============================== C ABI ==============================
 extern "C" {
@@ -420,7 +422,7 @@ int rkmf_matrix_create_device(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
   return guarded(ctx, [&] {
     set_device(ctx);
     if (n_rows < 0 || n_cols < 0) shape_error("negative dimension");
-    *out = create_from_device_rp64(ctx, n_rows, n_cols, nnz, d_rp, d_ci, d_v, true);
+    *out = create_from_device_rp64(ctx, n_rows, n_cols, nnz, d_rp, d_ci, d_v, true, true);
   });
 }
 

@@ -175,4 +175,10 @@ namespace rkmf_b200 {
 rkmf_matrix* create_matrix_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
                                 const int64_t* h_rp, const int32_t* h_ci, const double* h_v,
                                 bool require_sorted);
+// device CSR (int64 row pointers) -> validated matrix; with copy_colval false
+// the matrix takes ownership of col/val (allocated with kNnzPad padding)
+rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
+                                     int64_t nnz, const int64_t* rp64_dev,
+                                     const int32_t* col_dev, const double* val_dev,
+                                     bool copy_colval, bool require_sorted);
 }  // namespace rkmf_b200

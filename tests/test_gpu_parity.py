@@ -293,3 +293,33 @@ def test_cpp_host_api(rk):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "converged=1" in r.stdout
+
+
+# ---------------- on-device generators (cfg5's path) ----------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,args", [("lap", (2, 40)), ("lap", (3, 17)), ("q1", (9, False, 1, False)),
+                                       ("q1", (8, True, 3, True)), ("q1", (2, False, 1, False))])
+def test_device_generators_match_host(rk, torch, kind, args):
+    if kind == "lap":
+        Ad = rk.SparseMatrix.laplacian(*args)
+        rp, ci, v = rk.gen_laplacian(*args)
+    else:
+        Ad = rk.SparseMatrix.q1_hex(*args)
+        rp, ci, v = rk.gen_q1_hex(*args)
+    Ah = rk.SparseMatrix.from_csr(rp, ci, v)
+    assert (Ad.n_rows, Ad.nnz) == (Ah.n_rows, Ah.nnz)
+    lognormal = kind == "q1" and args[1]
+    assert Ad.norm1 == pytest.approx(Ah.norm1, rel=1e-14 if lognormal else 0.0)
+    x = torch.tensor(rk.gen_gaussian(5, Ad.n_rows), device="cuda")
+    zd, zh = rk.spmv(Ad, x), rk.spmv(Ah, x)
+    if lognormal:
+        assert float((zd - zh).norm() / zh.norm()) <= 1e-14
+    else:
+        assert torch.equal(zd, zh)
+
+
+@pytest.mark.gpu
+def test_device_gaussian_matches_host(rk, torch):
+    d = rk.gen_gaussian_device(7, 1000, 5000).cpu().numpy()
+    h = rk.gen_gaussian_range(7, 1000, 5000)
+    assert np.max(np.abs(d - h) / np.maximum(np.abs(h), 1e-300)) <= 1e-14
