@@ -521,7 +521,8 @@ class RestartResult:
 
 def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions = None,
                      S: SketchOperator = None, reference=None, out=None) -> RestartResult:
-    """restart::restarted_krylov (restart.hpp:74-79) with the randomized builder.
+    """restart::restarted_krylov (restart.hpp:74-79): the randomized builder with a
+    SketchOperator S, the classical builder (CGS2 on device) with S = None.
 
     b may be a numpy array (host: the host<->device copies are part of the call)
     or a CUDA tensor (device-resident); f_hat comes back in the same residency
@@ -529,9 +530,7 @@ def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions =
     """
     opts = opts or RestartOptions()
     ctx = A.ctx
-    if S is None:
-        raise ParameterError("rkmf_b200: the classical builder (S == nullptr) is not on the "
-                             "device path")
+    # S is None selects the classical builder (restart.cpp:53-55, basis.cpp:34-77)
     on_dev = _is_torch(b) and b.is_cuda
     n = A.n_rows
     if on_dev:
@@ -553,7 +552,7 @@ def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions =
     cap = int(opts.k_max) + 1
     recs = (CycleRecordC * cap)()
     oc = opts.to_c()
-    ctx.check(lib().rkmf_restarted_krylov(ctx.h, A.h, S.h, bptr, 1 if on_dev else 0, f.kind,
+    ctx.check(lib().rkmf_restarted_krylov(ctx.h, A.h, S.h if S is not None else None, bptr, 1 if on_dev else 0, f.kind,
                                           f.t, C.byref(oc), fptr, 1 if on_dev else 0,
                                           _ptr(ref), C.byref(res), C.cast(recs, C.c_void_p),
                                           cap))

@@ -152,6 +152,7 @@ void check_builder_args(const rkmf_matrix* A, const rkmf_sketch* S, int64_t m) {
     shape_error("arnoldi: matrix must be square");
   if (m < 1) param_error("arnoldi: m must be >= 1");
   if (m > ng) param_error("arnoldi: m exceeds matrix dimension");
+  if (!S) return;  // classical builder (basis.cpp:34-77)
   if (S->n != A->view.n_rows || (A->partitioned && (S->n_global != ng ||
                                                      S->col_begin != A->halo.row_begin)))
     shape_error("randomized_arnoldi: sketch width mismatch");
@@ -187,6 +188,64 @@ void run_steps(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
       ctx->launches++;
     }
   }
+}
+
+// Classical builder steps (S == nullptr; basis.cpp:47-72 via CGS2, classical.cu).
+// cl: [h1 | h2 | nrm2 | rlast (ldr x m_eff)]; fuse_last leaves the last
+// update (z' - W h2)/beta to final_update, with (h2, beta) in rlast.
+void run_steps_classical(rkmf_context* ctx, const rkmf_matrix* A, const SolveBuffers& b,
+                         double tol, bool fuse_last, double* cl) {
+  double* h1 = cl;
+  double* h2 = cl + b.ldr;
+  double* nrm2 = cl + 2 * b.ldr;
+  double* rlast = cl + 2 * b.ldr + 2;
+  const int grid = spmv_sketch_grid(&A->view, nullptr, 0);
+  int32_t* stop = &ctx->st_dev->stopped;
+  cudaStream_t st = ctx->stream;
+  for (int64_t k = 0; k < b.m_eff; ++k) {
+    const bool last = fuse_last && k == b.m_eff - 1;
+    double* x = b.W + k * b.ldw;
+    comm_halo_exchange(ctx, A, x);
+    ctx->timed(0, [&] {
+      launch_spmv_sketch(&A->view, nullptr, 0, x, k == 0 ? &ctx->st_dev->sigma : nullptr, b.z,
+                         nullptr, stop, int(k), grid, st);
+    });
+    ctx->timed(1, [&] { launch_cl_multidot(b.n, int(k), b.ldw, b.W, b.z, h1, ctx->st_dev, st); });
+    comm_allreduce_sum(ctx, h1, size_t(k + 1));
+    ctx->timed(2, [&] {
+      launch_cl_update(b.n, int(k), b.ldw, b.W, b.z, h1, nullptr, true, ctx->st_dev, st);
+    });
+    ctx->timed(1, [&] { launch_cl_multidot(b.n, int(k), b.ldw, b.W, b.z, h2, ctx->st_dev, st); });
+    comm_allreduce_sum(ctx, h2, size_t(k + 1));
+    ctx->timed(2, [&] {
+      launch_cl_update(b.n, int(k), b.ldw, b.W, b.z, h2, nrm2, !last, ctx->st_dev, st);
+    });
+    comm_allreduce_sum(ctx, nrm2, 1);
+    ctx->timed(1, [&] {
+      launch_cl_decide(int(k), b.ldr, b.n_global, tol, h1, h2, nrm2, b.Rbar,
+                       last ? rlast : nullptr, ctx->st_dev, st);
+    });
+    ctx->launches += 6;
+    if (!last) {
+      ctx->timed(2, [&] {
+        launch_cl_scale(b.n, int(k), b.ldw, b.W, b.z, b.Rbar, b.ldr, ctx->st_dev, st);
+      });
+      ctx->launches++;
+    }
+  }
+}
+
+// Classical start (basis.cpp:38-43): ||start||_2 over the (local) rows.
+void start_classical(rkmf_context* ctx, const SolveBuffers& b, double* cl, bool first) {
+  double* nrm2 = cl + 2 * b.ldr;
+  ctx->timed(5, [&] {
+    launch_cl_start(b.n, b.W, nrm2, ctx->st_dev, first, int(b.m_eff), true, ctx->stream);
+  });
+  comm_allreduce_sum(ctx, nrm2, 1);
+  ctx->timed(5, [&] {
+    launch_cl_start(b.n, b.W, nrm2, ctx->st_dev, first, int(b.m_eff), false, ctx->stream);
+  });
+  ctx->launches += 2;
 }
 
 void start_sketch(rkmf_context* ctx, const rkmf_sketch* S, const SolveBuffers& b) {
@@ -306,7 +365,8 @@ int rkmf_context_destroy(rkmf_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->z, &ctx->pacc, &ctx->sacc, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
                     &ctx->ws, &ctx->u, &ctx->g, &ctx->fhat, &ctx->ref, &ctx->partial,
-                    &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch, &ctx->gram})
+                    &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch, &ctx->gram,
+                    &ctx->cl})
     b->release();
   for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->kpool) cudaEventDestroy(e);
@@ -664,7 +724,7 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     if (fn_kind != RKMF_FN_EXP_NEG && fn_kind != RKMF_FN_INV_SQRT)
       param_error("funm: unknown FunctionSpec kind");
     if (fn_kind == RKMF_FN_EXP_NEG && !(fn_t >= 0.0)) param_error("FunctionSpec: t must be >= 0");
-    if (!S) param_error("rkmf_b200: the classical builder (S == nullptr) is not on the device path");
+    const bool classical = S == nullptr;  // restart.cpp:53-55: arnoldi vs randomized_arnoldi
     int dense = opts.dense_f;
     if (dense == RKMF_DENSE_AUTO) dense = fn_kind == RKMF_FN_EXP_NEG ? RKMF_DENSE_FULL : RKMF_DENSE_QUADRATURE;
     if (dense == RKMF_DENSE_FULL && fn_kind != RKMF_FN_EXP_NEG)
@@ -678,7 +738,14 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     ctx->kpend.clear();
 
     cudaStream_t st = ctx->stream;
-    SolveBuffers bb = prepare(ctx, n, A->view.n_cols, A->n_rows_global(), S->d, m_eff);
+    SolveBuffers bb = prepare(ctx, n, A->view.n_cols, A->n_rows_global(), classical ? 1 : S->d,
+                              m_eff);
+    double* cl = nullptr;
+    if (classical) {
+      const size_t cnt = size_t(2 * bb.ldr + 2 + bb.ldr * m_eff);
+      cl = static_cast<double*>(ctx->cl.ensure(sizeof(double) * cnt));
+      RKMF_CUDA(cudaMemsetAsync(cl, 0, sizeof(double) * cnt, ctx->stream));
+    }
     double* g = static_cast<double*>(ctx->g.ensure(sizeof(double) * size_t(m_eff)));
     double* fhat = f_on_device ? f_out : static_cast<double*>(ctx->fhat.ensure(sizeof(double) * size_t(std::max<int64_t>(n, 1))));
     RKMF_CUDA(cudaMemsetAsync(fhat, 0, sizeof(double) * size_t(n), st));
@@ -760,9 +827,9 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     const double tol_break = 1e-14 * A->norm1;  // basis.cpp:118
     int64_t M = 0;
     double first_update = -1.0;
-    long long matvecs = 0, dot_d = 0, updates = 0, peak = 0;
+    long long matvecs = 0, dot_n = 0, dot_d = 0, updates = 0, peak = 0;
     RKMF_CUDA(cudaEventRecord(ctx->event(0), st));
-    start_sketch(ctx, S, bb);
+    if (!classical) start_sketch(ctx, S, bb);
     struct CycleEv { size_t e0, e1, e2, e3; };
     size_t next_ev = 1;
     std::vector<CycleEv> evs;
@@ -773,16 +840,22 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       next_ev += 4;
       CycleEv ce{base, base + 1, base + 2, base + 3};
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e0), st));
-      ctx->timed(5, [&] {
-        launch_start_init_m(bb.d, bb.sacc, bb.U, ctx->st_dev, k == 1, int(m_eff), st);
-      });
-      ctx->launches++;
+      if (classical) {
+        start_classical(ctx, bb, cl, k == 1);
+      } else {
+        ctx->timed(5, [&] {
+          launch_start_init_m(bb.d, bb.sacc, bb.U, ctx->st_dev, k == 1, int(m_eff), st);
+        });
+        ctx->launches++;
+      }
       if (k == 1) {
         ctx->sync_state();
         if (ctx->st_host->zero_start)
-          param_error("randomized_arnoldi: zero start vector after sketching");
+          param_error(classical ? "arnoldi: zero start vector"
+                                : "randomized_arnoldi: zero start vector after sketching");
       }
-      run_steps(ctx, A, S, bb, tol_break, true);
+      if (classical) run_steps_classical(ctx, A, bb, tol_break, true, cl);
+      else run_steps(ctx, A, S, bb, tol_break, true);
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e1), st));
       // ---- dense f ----
       if (dense == RKMF_DENSE_FULL) {
@@ -819,7 +892,9 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       }
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e2), st));
       ctx->timed(4, [&] {
-        launch_final_update(n, int(m_eff), bb.ldw, bb.W, bb.z, bb.Rbar, bb.ldr, g, fhat, ref_dev,
+        // classical: the last step left z' and (h2, beta) in rlast
+        launch_final_update(n, int(m_eff), bb.ldw, bb.W, bb.z,
+                            classical ? cl + 2 * bb.ldr + 2 : bb.Rbar, bb.ldr, g, fhat, ref_dev,
                             ctx->st_dev, st);
       });
       ctx->launches++;
@@ -831,7 +906,7 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       const bool next = h.breakdown == 0;
       if (k == 1) res->alpha = h.alpha1;
       matvecs += mk;
-      dot_d += mk * (mk + 1) / 2;
+      (classical ? dot_n : dot_d) += mk * (mk + 1) / 2;
       updates += next ? m_eff : mk - 1;
       peak = std::max<long long>(peak, next ? m_eff + 1 : mk);
       if (h.nonfinite || !std::isfinite(h.yn2))  // restart.cpp:82-83
@@ -862,7 +937,7 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
         res->converged = 1;
         break;
       }
-      start_sketch(ctx, S, bb);  // next cycle's S * start
+      if (!classical) start_sketch(ctx, S, bb);  // next cycle's S * start
     }
     const size_t e_end = next_ev;
     RKMF_CUDA(cudaEventRecord(ctx->event(e_end), st));
@@ -883,7 +958,7 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       recs[i].funm_ms = c;
     }
     res->matvecs = matvecs;
-    res->dot_n = 0;
+    res->dot_n = dot_n;
     res->dot_d = dot_d;
     res->basis_updates = updates;
     res->peak_basis_cols = peak;

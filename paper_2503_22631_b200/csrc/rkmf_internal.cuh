@@ -177,6 +177,19 @@ void launch_scale_copy(int64_t n, const double* src, double* dst, const SolveSta
                        cudaStream_t st);
 void launch_fill(int64_t n, double v, double* x, cudaStream_t st);
 
+// classical.cu: the classical builder (S == nullptr) via CGS2
+void launch_cl_start(int64_t n, const double* start, double* nrm2_scratch, SolveState* st_dev,
+                     bool first, int m_eff, bool norm_only, cudaStream_t st);
+void launch_cl_multidot(int64_t n, int k, int64_t ldw, const double* W, const double* z,
+                        double* h, const SolveState* st_dev, cudaStream_t st);
+void launch_cl_update(int64_t n, int k, int64_t ldw, const double* W, double* z, const double* h,
+                      double* nrm2, bool store, const SolveState* st_dev, cudaStream_t st);
+void launch_cl_decide(int k, int64_t ldr, int64_t n_global, double tol, double* h1, double* h2,
+                      double* nrm2, double* Rbar, double* rlast, SolveState* st_dev,
+                      cudaStream_t st);
+void launch_cl_scale(int64_t n, int k, int64_t ldw, double* W, const double* z,
+                     const double* Rbar, int64_t ldr, const SolveState* st_dev, cudaStream_t st);
+
 // densef.cu
 void launch_raccum_append(double* R, int64_t ldr_acc, int64_t M, const double* Rbar,
                           int64_t ldr, SolveState* st_dev, cudaStream_t st);

@@ -160,9 +160,46 @@ __global__ void sketch_tiles_kernel(int64_t d, int64_t n, int zeta, int64_t off_
   for (int64_t q = 2 * d + 1 + t; q < off_stride; q += blockDim.x) toff[q] = 0;
   uint8_t* tent = tile_ent + tile * int64_t(kTileRows) * zeta;
   const int total = cnt[d];
-  for (int64_t b = t; b < d; b += blockDim.x) {
-    const int src = cnt[b], c = cnt[b + 1] - cnt[b], dst = soff[cur[b]];
-    for (int e = 0; e < c; ++e) tent[dst + e] = ent[src + e];
+  __syncthreads();  // slot bins (toff) visible to the whole block
+  // Entry order inside each slot, bank-aware: the 32 slots of a group are
+  // walked by one warp in lockstep (sketch_tile_gather: group = slot / 32), and
+  // at position q every lane loads zs2[entry]; the double at index u sits in
+  // bank pair (u mod 16) = (row mod 16). Greedily give each lane, position by
+  // position, its remaining entry in the least-used bank pair, so the warp's
+  // loads spread over the 16 pairs (~2 wavefronts instead of ~4-5). Only the
+  // summation order inside a bin changes; the layout stays deterministic.
+  const int ngroups = int((d + 31) / 32);
+  for (int g = t; g < ngroups; g += blockDim.x) {
+    const int s0 = 32 * g, s1 = int(min(d, int64_t(s0) + 32));
+    int maxc = 0;
+    for (int sl = s0; sl < s1; ++sl) maxc = max(maxc, soff[sl + 1] - soff[sl]);
+    if (maxc > 64) {  // unusually long bins: keep the column order
+      for (int sl = s0; sl < s1; ++sl) {
+        const int b = toff[d + 1 + sl], src = cnt[b], c = soff[sl + 1] - soff[sl];
+        for (int e = 0; e < c; ++e) tent[soff[sl] + e] = ent[src + e];
+      }
+      continue;
+    }
+    uint64_t used[32];
+    for (int l = 0; l < 32; ++l) used[l] = 0;
+    for (int q = 0; q < maxc; ++q) {
+      int load[16];
+      for (int k = 0; k < 16; ++k) load[k] = 0;
+      for (int sl = s0; sl < s1; ++sl) {
+        const int c = soff[sl + 1] - soff[sl];
+        if (q >= c) continue;
+        const int src = cnt[toff[d + 1 + sl]];
+        int best = -1, bl = 1 << 30;
+        for (int e = 0; e < c; ++e) {
+          if ((used[sl - s0] >> e) & 1ull) continue;
+          const int bank = ent[src + e] & 15;
+          if (load[bank] < bl) { bl = load[bank]; best = e; }
+        }
+        used[sl - s0] |= 1ull << best;
+        load[ent[src + best] & 15]++;
+        tent[soff[sl] + q] = ent[src + best];
+      }
+    }
   }
   for (int e = total + t; e < kTileRows * zeta; e += blockDim.x) tent[e] = 0;
 }

@@ -22,6 +22,7 @@ import torch.distributed as dist  # noqa: E402
 def main():
     out, name, N = sys.argv[1], sys.argv[2], int(sys.argv[3])
     transport = sys.argv[4] if len(sys.argv) > 4 else "host"
+    classical = len(sys.argv) > 5 and sys.argv[5] == "classical"
     dist.init_process_group("gloo", timeout=timedelta(seconds=300))
     rank, world = dist.get_rank(), dist.get_world_size()
     import paper_2503_22631_b200 as rk
@@ -33,7 +34,7 @@ def main():
                        configs.SKETCH_SEED, world, rank)
     f = rk.FunctionSpec.exp_neg(P.t) if P.fn == "exp_neg" else rk.FunctionSpec.inv_sqrt()
     opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
-    r = D.solve(part, f, opts)
+    r = rk.restarted_krylov(part.A, part.b, f, opts, None) if classical else D.solve(part, f, opts)
     fg = D.gather_f(r.f_hat, part.row_starts)
     # the partitioned sketch is the global sketch's column range (bit-exact)
     rows, signs, _ = part.S.export()

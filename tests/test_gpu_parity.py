@@ -323,3 +323,45 @@ def test_device_gaussian_matches_host(rk, torch):
     d = rk.gen_gaussian_device(7, 1000, 5000).cpu().numpy()
     h = rk.gen_gaussian_range(7, 1000, 5000)
     assert np.max(np.abs(d - h) / np.maximum(np.abs(h), 1e-300)) <= 1e-14
+
+
+# ---------------- classical restarted Arnoldi (S == nullptr) ----------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N", [("cfg1", 64), ("cfg2", 20), ("cfg4", 16)])
+def test_classical_restart_matches_oracle(rk, oracle, torch, name, N):
+    """restart.cpp:53-55 with the classical builder (basis.cpp:34-77): device
+    CGS2 vs the oracle's MGS, f_hat within 1e-9, cycles within one, the
+    reference's counter formulas (dot_n = sum m_k(m_k+1)/2, dot_d = 0)."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    f = rk.FunctionSpec.exp_neg(P.t)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
+    r = rk.restarted_krylov(A, torch.tensor(P.b, device="cuda"), f, opts, None)
+    o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, oracle.KIND_EXP_NEG, P.t,
+                                m_r=P.m, tol=P.tol, k_max=P.k_max, S=None)
+    fd = r.f_hat.cpu().numpy()
+    assert r.converged and o.converged
+    assert abs(r.cycles - o.cycles) <= 1
+    assert np.linalg.norm(fd - o.f_hat) <= 1e-9 * np.linalg.norm(o.f_hat)
+    assert r.alpha == pytest.approx(np.linalg.norm(P.b), rel=1e-13)  # beta = ||b||_2
+    assert r.counters["dot_d"] == 0
+    assert r.counters["dot_n"] == r.counters["matvecs"] * (P.m + 1) // 2 or r.cycles > 1
+
+
+@pytest.mark.gpu
+def test_classical_breakdown_and_zero_start(rk, oracle, torch):
+    # happy breakdown: b in a 3-dimensional invariant subspace of a diagonal A
+    n = 40
+    d = np.arange(1, n + 1, dtype=np.float64)
+    A = sp.diags(d).tocsr()
+    b = np.zeros(n)
+    b[[2, 7, 11]] = [1.0, -2.0, 0.5]
+    dA = rk.SparseMatrix.from_scipy(A)
+    f = rk.FunctionSpec.exp_neg(0.3)
+    r = rk.restarted_krylov(dA, b, f, rk.RestartOptions(m_r=10, tol=1e-12, k_max=5), None)
+    assert r.converged and r.cycles == 1 and r.total_m == 3
+    ref = np.exp(-0.3 * d) * b
+    assert np.linalg.norm(r.f_hat - ref) <= 1e-12 * np.linalg.norm(ref)
+    with pytest.raises(rk.ParameterError, match="zero start vector"):
+        rk.restarted_krylov(dA, np.zeros(n), f, rk.RestartOptions(m_r=5), None)

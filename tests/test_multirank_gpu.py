@@ -27,11 +27,11 @@ def _port():
     return p
 
 
-def _run(tmp_path, name, N, world, transport="host"):
-    out = str(tmp_path / f"{name}_{N}_{world}.npz")
+def _run(tmp_path, name, N, world, transport="host", builder="randomized"):
+    out = str(tmp_path / f"{name}_{N}_{world}_{builder}.npz")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
-           os.path.join(ROOT, "tests", "mr_worker.py"), out, name, str(N), transport]
+           os.path.join(ROOT, "tests", "mr_worker.py"), out, name, str(N), transport, builder]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
@@ -79,4 +79,18 @@ def test_partitioned_single_rank_nccl_path(tmp_path, oracle):
     S = oracle.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED)
     o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, oracle.KIND_EXP_NEG, P.t,
                                 m_r=P.m, tol=P.tol, k_max=P.k_max, S=S)
+    assert np.linalg.norm(res["f"] - o.f_hat) <= 1e-9 * np.linalg.norm(o.f_hat)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,world", [("cfg2", 20, 2), ("cfg4", 16, 3)])
+def test_partitioned_classical_matches_oracle(tmp_path, oracle, name, N, world):
+    """The classical builder on partitioned rows: the n-length dots and norms
+    of CGS2 are allreduced across ranks."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    res = _run(tmp_path, name, N, world, "host", "classical")
+    o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, oracle.KIND_EXP_NEG, P.t,
+                                m_r=P.m, tol=P.tol, k_max=P.k_max, S=None)
+    assert bool(res["converged"]) and abs(int(res["cycles"]) - o.cycles) <= 1
     assert np.linalg.norm(res["f"] - o.f_hat) <= 1e-9 * np.linalg.norm(o.f_hat)
