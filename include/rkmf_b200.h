@@ -59,12 +59,16 @@ typedef struct {
   double divergence_factor;
   int32_t dense_f;        /* RKMF_DENSE_* */
   int32_t quad_nodes;     /* quadrature nodes (0 = default 512) */
+  int32_t diagnostics;    /* 1: fill CycleRecord kappa_W / leftmost_ritz_re
+                             (restart.cpp:101,103; one Gram pass over W_m per
+                             cycle, m <= 64); 0 (default): NaN */
+  int32_t reserved;
 } rkmf_restart_options;
 
 /* Replaces restart::CycleRecord (restart.hpp:28-40). kappa_W and
- * leftmost_ritz_re are per-cycle diagnostics of the reference
- * (restart.cpp:101,103) that are not on the device hot path: NaN. Times are
- * device times from CUDA events. */
+ * leftmost_ritz_re (restart.cpp:101,103) are filled when
+ * rkmf_restart_options.diagnostics is set, else NaN (not on the hot path).
+ * Times are device times from CUDA events. */
 typedef struct {
   int64_t cycle;
   int64_t total_m;

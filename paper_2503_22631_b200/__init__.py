@@ -71,7 +71,8 @@ _CODE = {1: ParameterError, 2: ShapeError, 3: NumericalError, 4: DeviceError, 5:
 class RestartOptionsC(C.Structure):
     _fields_ = [("m_r", C.c_int64), ("tol", C.c_double), ("k_max", C.c_int64),
                 ("budget_total_m", C.c_int64), ("divergence_factor", C.c_double),
-                ("dense_f", C.c_int32), ("quad_nodes", C.c_int32)]
+                ("dense_f", C.c_int32), ("quad_nodes", C.c_int32), ("diagnostics", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class CycleRecordC(C.Structure):
@@ -468,12 +469,13 @@ class RestartOptions:
     divergence_factor: float = 1e6
     dense_f: str = "auto"  # auto | full | quadrature
     quad_nodes: int = 0
+    diagnostics: bool = False  # per-cycle kappa_W / leftmost Ritz (restart.cpp:101,103)
 
     def to_c(self) -> RestartOptionsC:
         mode = {"auto": DENSE_AUTO, "full": DENSE_FULL, "quadrature": DENSE_QUADRATURE}[self.dense_f]
         return RestartOptionsC(int(self.m_r), float(self.tol), int(self.k_max),
                                int(self.budget_total_m), float(self.divergence_factor), mode,
-                               int(self.quad_nodes))
+                               int(self.quad_nodes), int(bool(self.diagnostics)), 0)
 
 
 @dataclass

@@ -366,7 +366,7 @@ int rkmf_context_destroy(rkmf_context* ctx) {
   for (DevBuf* b : {&ctx->z, &ctx->pacc, &ctx->sacc, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
                     &ctx->ws, &ctx->u, &ctx->g, &ctx->fhat, &ctx->ref, &ctx->partial,
                     &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch, &ctx->gram,
-                    &ctx->cl})
+                    &ctx->cl, &ctx->diag})
     b->release();
   for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->kpool) cudaEventDestroy(e);
@@ -418,6 +418,8 @@ void rkmf_restart_options_default(rkmf_restart_options* o) {  // restart.hpp:20-
   o->divergence_factor = 1e6;
   o->dense_f = RKMF_DENSE_AUTO;
   o->quad_nodes = 0;
+  o->diagnostics = 0;
+  o->reserved = 0;
 }
 
 int rkmf_matrix_create_host(rkmf_context* ctx, int64_t n_rows, int64_t n_cols,
@@ -856,6 +858,17 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       }
       if (classical) run_steps_classical(ctx, A, bb, tol_break, true, cl);
       else run_steps(ctx, A, S, bb, tol_break, true);
+      // diagnostics: Gram of W_m before final_update overwrites column 0
+      bool diag_ok = false;
+      double* Gd = nullptr;
+      if (opts.diagnostics) {
+        Gd = static_cast<double*>(ctx->diag.ensure(sizeof(double) * size_t(m_eff) * size_t(m_eff)));
+        diag_ok = launch_gram(n, int(m_eff), bb.ldw, bb.W, ctx->st_dev, Gd, st);
+        if (diag_ok) {
+          ctx->launches++;
+          comm_allreduce_sum(ctx, Gd, size_t(m_eff) * size_t(m_eff));
+        }
+      }
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e1), st));
       // ---- dense f ----
       if (dense == RKMF_DENSE_FULL) {
@@ -921,6 +934,17 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
                                                              : std::numeric_limits<double>::quiet_NaN();
       rec.kappa_W = std::numeric_limits<double>::quiet_NaN();
       rec.leftmost_ritz_re = std::numeric_limits<double>::quiet_NaN();
+      if (diag_ok) {  // approximants.cpp:29-47 on the mk kept columns
+        std::vector<double> Gh(size_t(m_eff) * size_t(m_eff)), Rh(size_t(bb.ldr) * size_t(m_eff));
+        RKMF_CUDA(cudaMemcpy(Gh.data(), Gd, sizeof(double) * Gh.size(), cudaMemcpyDeviceToHost));
+        RKMF_CUDA(cudaMemcpy(Rh.data(), bb.Rbar, sizeof(double) * Rh.size(),
+                             cudaMemcpyDeviceToHost));
+        std::vector<double> Gk(size_t(mk) * size_t(mk));
+        for (int64_t i = 0; i < mk; ++i)
+          for (int64_t j = 0; j < mk; ++j) Gk[size_t(i * mk + j)] = Gh[size_t(i * m_eff + j)];
+        rec.kappa_W = kappa_from_gram(Gk, int(mk));
+        rec.leftmost_ritz_re = leftmost_ritz(Rh, bb.ldr, int(mk));
+      }
       rec.alpha_dev = k == 1 ? 0.0 : std::fabs(h.alpha_k - 1.0);
       rec.start_norm = h.alpha_k;
       rec.subdiag = h.coupling;

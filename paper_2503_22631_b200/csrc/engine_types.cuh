@@ -68,7 +68,7 @@ struct rkmf_context {
   SolveState* st_dev = nullptr;
   SolveState* st_host = nullptr;  // pinned
   DevBuf z, pacc, sacc, W, U, Rbar, Racc, ws, u, g, fhat, ref, partial, qshift, qweight, qpi,
-      qemx, scratch, gram, cl;
+      qemx, scratch, gram, cl, diag;
   int64_t racc_ld = 0;
   std::vector<double> last_R;
   int64_t last_M = 0;

@@ -190,6 +190,12 @@ void launch_cl_decide(int k, int64_t ldr, int64_t n_global, double tol, double* 
 void launch_cl_scale(int64_t n, int k, int64_t ldw, double* W, const double* z,
                      const double* Rbar, int64_t ldr, const SolveState* st_dev, cudaStream_t st);
 
+// diag.cu: per-cycle kappa_W and leftmost Ritz value (opt-in)
+bool launch_gram(int64_t n, int m, int64_t ldw, const double* W, const SolveState* st_dev,
+                 double* G, cudaStream_t st);
+double kappa_from_gram(const std::vector<double>& G, int m);
+double leftmost_ritz(const std::vector<double>& Rbar, int64_t ldr, int m);
+
 // densef.cu
 void launch_raccum_append(double* R, int64_t ldr_acc, int64_t M, const double* Rbar,
                           int64_t ldr, SolveState* st_dev, cudaStream_t st);

@@ -365,3 +365,34 @@ def test_classical_breakdown_and_zero_start(rk, oracle, torch):
     assert np.linalg.norm(r.f_hat - ref) <= 1e-12 * np.linalg.norm(ref)
     with pytest.raises(rk.ParameterError, match="zero start vector"):
         rk.restarted_krylov(dA, np.zeros(n), f, rk.RestartOptions(m_r=5), None)
+
+
+# ---------------- per-cycle diagnostics (restart.cpp:101,103) ----------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,sketched", [("cfg2", 14, True), ("cfg4", 12, True),
+                                             ("cfg1", 40, False)])
+def test_cycle_diagnostics_match_numpy(rk, oracle, torch, name, N, sketched):
+    """kappa_W = cond_2(W_m) and the leftmost Ritz value of R_m for cycle 1,
+    against numpy's SVD / eig of the oracle's decomposition of the same start."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1) if sketched else None
+    OS = oracle.make_sketch(P.d, P.n, P.zeta, 1) if sketched else None
+    f = rk.FunctionSpec.exp_neg(P.t)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max, diagnostics=True)
+    r = rk.restarted_krylov(A, P.b, f, opts, S)
+    dec = oracle.arnoldi_decomp((P.row_ptr, P.col_idx, P.values), P.b, P.m, OS)
+    m = dec.m
+    sv = np.linalg.svd(dec.W[:, :m], compute_uv=False)
+    kappa = sv[0] / sv[-1]
+    ritz = np.linalg.eigvals(dec.Rbar[:m, :m])
+    h0 = r.history[0]
+    assert h0.kappa_W == pytest.approx(kappa, rel=1e-6)
+    assert h0.leftmost_ritz_re == pytest.approx(float(np.min(ritz.real)),
+                                                rel=1e-8, abs=1e-10 * np.abs(ritz).max())
+    for h in r.history:
+        assert np.isfinite(h.kappa_W) and h.kappa_W >= 1.0
+    # off by default
+    r2 = rk.restarted_krylov(A, P.b, f, rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=2), S)
+    assert np.isnan(r2.history[0].kappa_W)
