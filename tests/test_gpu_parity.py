@@ -186,8 +186,10 @@ def test_restart_device_resident_and_reference(rk, oracle, torch):
     ref = torch.tensor(rh.f_hat, device="cuda")
     rd = rk.restarted_krylov(A, bd, f, opts, S, reference=ref)
     assert rd.f_hat.is_cuda
-    assert rel(rd.f_hat, rh.f_hat) <= 1e-14
-    assert rd.history[-1].error_vs_reference <= 1e-14
+    # the per-block sketch partials meet in fp64 atomics (K2), so two solves
+    # agree to run-to-run rounding, not bit for bit
+    assert rel(rd.f_hat, rh.f_hat) <= 1e-12
+    assert rd.history[-1].error_vs_reference <= 1e-12
     assert rd.solve_ms > 0 and all(h.build_ms > 0 for h in rd.history)
 
 
