@@ -542,8 +542,15 @@ int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_globa
       const int64_t off_stride = tile_off_stride(d);
       RKMF_CUDA(cudaMalloc(&S->rows, sizeof(uint16_t) * size_t(std::max<int64_t>(n * zeta, 1))));
       RKMF_CUDA(cudaMalloc(&S->signs, size_t(std::max<int64_t>(n * zeta, 1))));
-      RKMF_CUDA(cudaMalloc(&S->tile_off, sizeof(uint16_t) * size_t(std::max<int64_t>(tiles * off_stride, 1))));
-      RKMF_CUDA(cudaMalloc(&S->tile_ent, size_t(std::max<int64_t>(tiles * kTileRows * zeta, 16))));
+      // one allocation for the tile layout (header | entries), so a single L2
+      // access-policy window can keep it resident across steps
+      const size_t ob = round_up(int64_t(sizeof(uint16_t)) * std::max<int64_t>(tiles * off_stride, 1), 256);
+      const size_t eb = size_t(std::max<int64_t>(tiles * kTileRows * zeta, 16)) + 16;
+      void* tl = nullptr;
+      RKMF_CUDA(cudaMalloc(&tl, ob + eb));
+      S->tile_off = static_cast<uint16_t*>(tl);
+      S->tile_ent = static_cast<uint8_t*>(tl) + ob;
+      S->layout_bytes = ob + eb;
       launch_sketch_generate(d, n, col_begin, zeta, seed, S->rows, S->signs, ctx->stream);
       launch_sketch_tiles(d, n, zeta, S->rows, S->signs, S->tile_off, S->tile_ent, ctx->stream);
       ctx->launches += 2;
@@ -552,7 +559,6 @@ int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_globa
       if (S->rows) cudaFree(S->rows);
       if (S->signs) cudaFree(S->signs);
       if (S->tile_off) cudaFree(S->tile_off);
-      if (S->tile_ent) cudaFree(S->tile_ent);
       delete S;
       throw;
     }
@@ -565,8 +571,7 @@ int rkmf_sketch_destroy(rkmf_sketch* S) {
   cudaSetDevice(S->device);
   cudaFree(S->rows);
   cudaFree(S->signs);
-  cudaFree(S->tile_off);
-  cudaFree(S->tile_ent);
+  cudaFree(S->tile_off);  // also holds tile_ent
   delete S;
   return RKMF_OK;
 }
@@ -634,6 +639,11 @@ int rkmf_spmv_sketch(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch*
   });
 }
 
+bool flush_l2_between() {  // RKMF_BENCH_FLUSH=1: kernel_bench flushes L2 between launches
+  const char* e = getenv("RKMF_BENCH_FLUSH");
+  return e && e[0] == '1';
+}
+
 int rkmf_kernel_bench(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S, int32_t mode,
                       const double* d_x, double* d_z, double* d_p, int32_t reps, double* avg_ms) {
   return guarded(ctx, [&] {
@@ -651,13 +661,31 @@ int rkmf_kernel_bench(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch
                          nullptr, 0, grid, ctx->stream);
     };
     launch();  // warm-up
-    RKMF_CUDA(cudaEventRecord(ctx->event(0), ctx->stream));
-    for (int i = 0; i < reps; ++i) launch();
-    RKMF_CUDA(cudaEventRecord(ctx->event(1), ctx->stream));
-    RKMF_CUDA(cudaEventSynchronize(ctx->event(1)));
-    float ms = 0.f;
-    RKMF_CUDA(cudaEventElapsedTime(&ms, ctx->event(0), ctx->event(1)));
-    *avg_ms = double(ms) / reps;
+    if (flush_l2_between()) {  // cold-L2 variant: a 256 MB write between timed launches
+      DevBuf junk;
+      junk.ensure(size_t(256) << 20);
+      double tot = 0.0;
+      for (int i = 0; i < reps; ++i) {
+        RKMF_CUDA(cudaMemsetAsync(junk.p, i & 0xff, size_t(256) << 20, ctx->stream));
+        RKMF_CUDA(cudaEventRecord(ctx->event(0), ctx->stream));
+        launch();
+        RKMF_CUDA(cudaEventRecord(ctx->event(1), ctx->stream));
+        RKMF_CUDA(cudaEventSynchronize(ctx->event(1)));
+        float ms = 0.f;
+        RKMF_CUDA(cudaEventElapsedTime(&ms, ctx->event(0), ctx->event(1)));
+        tot += ms;
+      }
+      junk.release();
+      *avg_ms = tot / reps;
+    } else {
+      RKMF_CUDA(cudaEventRecord(ctx->event(0), ctx->stream));
+      for (int i = 0; i < reps; ++i) launch();
+      RKMF_CUDA(cudaEventRecord(ctx->event(1), ctx->stream));
+      RKMF_CUDA(cudaEventSynchronize(ctx->event(1)));
+      float ms = 0.f;
+      RKMF_CUDA(cudaEventElapsedTime(&ms, ctx->event(0), ctx->event(1)));
+      *avg_ms = double(ms) / reps;
+    }
     ctx->launches += reps + 1;
   });
 }

@@ -148,8 +148,9 @@ struct rkmf_sketch {
   double scale = 1.0;
   uint16_t* rows = nullptr;
   int8_t* signs = nullptr;
-  uint16_t* tile_off = nullptr;
+  uint16_t* tile_off = nullptr;  // one allocation: header, then entries
   uint8_t* tile_ent = nullptr;
+  size_t layout_bytes = 0;
   SketchView view() const {
     SketchView v;
     v.d = d;
