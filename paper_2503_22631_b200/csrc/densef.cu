@@ -21,7 +21,9 @@
 // rule in u converges geometrically (poles at distance (pi-|arg z|)/2).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "rkmf_internal.cuh"
 
@@ -203,11 +205,173 @@ __global__ void quad_reduce_kernel(int nq, int mkmax, const double* __restrict__
   }
 }
 
+// ---- ExpNeg quadrature: complex nodes, one warp per node ----
+// Same block recursion as the InvSqrt kernel with complex shifts sigma_q:
+// (sigma I + H) x = e1 by complex Givens rotations; partial[q][j] =
+// Re(w_q pi_q x_j) (conjugate nodes folded into w_q by the host).
+struct cplx { double re, im; };
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  const double d = b.re * b.re + b.im * b.im;
+  return {(a.re * b.re + a.im * b.im) / d, (a.im * b.re - a.re * b.im) / d};
+}
+constexpr int kMaxMC = 64;
+__global__ void __launch_bounds__(32)
+    quad_expneg_kernel(const double* __restrict__ Rbar, int64_t ldr, int mkmax,
+                       const cplx* __restrict__ shift, const cplx* __restrict__ weight, cplx* pi,
+                       cplx* emx, int64_t cycle, const SolveState* st, double* partial,
+                       int mk_in, double coupling_in) {
+  // mk_in >= 0: replay of a past cycle (its block of R_accum, its coupling
+  // R_accum(M, M-1)); else the current cycle from the solve state
+  extern __shared__ cplx Mc[];  // mk x mk, column-major
+  __shared__ cplx rhs[kMaxMC];
+  const int q = blockIdx.x, lane = threadIdx.x;
+  const int mk = mk_in >= 0 ? mk_in : st->stopped;
+  const cplx sg = shift[q];
+  cplx piq = pi[q];
+  if (cycle > 1) {
+    const cplx c = {-(mk_in >= 0 ? coupling_in : st->coupling * st->alpha_k), 0.0};
+    piq = cmul(cmul(piq, c), emx[q]);
+  }
+  for (int64_t e = lane; e < int64_t(mk) * mk; e += 32) {
+    const int i = int(e % mk), j = int(e / mk);
+    Mc[e] = {Rbar[int64_t(j) * ldr + i] + (i == j ? sg.re : 0.0), i == j ? sg.im : 0.0};
+  }
+  for (int i = lane; i < mk; i += 32) rhs[i] = {i == 0 ? 1.0 : 0.0, 0.0};
+  __syncwarp();
+  for (int k = 0; k + 1 < mk; ++k) {  // zero (k+1, k): rows k, k+1 by a unitary rotation
+    const cplx a = Mc[int64_t(k) * mk + k], b = Mc[int64_t(k) * mk + k + 1];
+    const double r = sqrt(a.re * a.re + a.im * a.im + b.re * b.re + b.im * b.im);
+    const cplx c = r == 0.0 ? cplx{1.0, 0.0} : cplx{a.re / r, a.im / r};
+    const cplx s = r == 0.0 ? cplx{0.0, 0.0} : cplx{b.re / r, b.im / r};
+    const cplx cc = {c.re, -c.im}, sc = {s.re, -s.im};
+    for (int j = k + lane; j < mk; j += 32) {
+      const cplx x0 = Mc[int64_t(j) * mk + k], x1 = Mc[int64_t(j) * mk + k + 1];
+      const cplx y0 = cmul(cc, x0), y1 = cmul(sc, x1);
+      const cplx z0 = cmul(s, x0), z1 = cmul(c, x1);
+      Mc[int64_t(j) * mk + k] = {y0.re + y1.re, y0.im + y1.im};
+      Mc[int64_t(j) * mk + k + 1] = {z1.re - z0.re, z1.im - z0.im};
+    }
+    if (lane == 0) {
+      const cplx r0 = rhs[k], r1 = rhs[k + 1];
+      const cplx y0 = cmul(cc, r0), y1 = cmul(sc, r1), z0 = cmul(s, r0), z1 = cmul(c, r1);
+      rhs[k] = {y0.re + y1.re, y0.im + y1.im};
+      rhs[k + 1] = {z1.re - z0.re, z1.im - z0.im};
+    }
+    __syncwarp();
+  }
+  for (int i = mk - 1; i >= 0; --i) {  // back substitution
+    const cplx xi = cdiv(rhs[i], Mc[int64_t(i) * mk + i]);
+    __syncwarp();
+    for (int r = lane; r < i; r += 32) {
+      const cplx t = cmul(Mc[int64_t(i) * mk + r], xi);
+      rhs[r] = {rhs[r].re - t.re, rhs[r].im - t.im};
+    }
+    if (lane == 0) rhs[i] = xi;
+    __syncwarp();
+  }
+  const cplx wq = cmul(weight[q], piq);
+  if (partial)
+    for (int j = lane; j < mkmax; j += 32)
+      partial[int64_t(q) * mkmax + j] = j < mk ? cmul(wq, rhs[j]).re : 0.0;
+  if (lane == 0) {
+    pi[q] = piq;
+    emx[q] = rhs[mk - 1];
+  }
+}
+
 int grid_for(int64_t work) {
   return int(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 16)));
 }
 
 }  // namespace
+
+// Contour for exp(-t z) over the t-scaled spectrum (z = t lambda): the parabola
+// zeta(u) = x0 + p u^2 + i q u, u in R, opening to the right where e^{-zeta}
+// decays. Its vertex sits D = 4 left of the leftmost Ritz value of cycle 1
+// (|e^{-zeta}| stays within e^4 of the solution's scale; anchoring further left
+// costs digits: e^{lmin - x0} of cancellation). q encloses every Ritz value
+// with Re < lmin + 40 (beyond that e^{-z} is below 1e-17 of the leading term)
+// with a 2x imaginary margin; the trapezoid step h = 0.15 D / q keeps the poles
+// ~D/q from the real u axis (discretisation error ~ e^{-2 pi D/(q h)}); the sum
+// is truncated where Re zeta = lmin + 45. Against scipy's expm on BASELINE
+// R_accum: 1e-15..1e-13 whenever the later cycles' Ritz values stay inside;
+// the engine checks every cycle (ExpContour::inside) and otherwise redesigns
+// from all Ritz values seen and replays the node states.
+ExpContour design_exp_contour(const std::vector<double>& wr, const std::vector<double>& wi) {
+  ExpContour c;
+  c.lmin = *std::min_element(wr.begin(), wr.end());
+  const double D = 4.0;
+  c.x0 = c.lmin - D;
+  c.p = 1.0;
+  c.q = 10.0;
+  for (size_t i = 0; i < wr.size(); ++i)
+    if (wr[i] < c.lmin + 40.0)
+      c.q = std::max(c.q, (2.0 * std::fabs(wi[i]) + 2.0) / std::sqrt(std::max(wr[i] - c.x0, 1e-3)));
+  c.h = 0.15 * D / c.q;
+  c.K = int(std::ceil(std::sqrt((c.lmin + 45.0 - c.x0) / c.p) / c.h));
+  return c;
+}
+
+// a later Ritz value is safe if it lies at most D/4 left of the design's
+// leftmost (its poles stay >= ~3D/(4q) from the real u axis) and inside the
+// parabola with a 1.5x imaginary margin; otherwise the engine redesigns
+bool ExpContour::inside(double re, double im) const {
+  if (re >= lmin + 40.0) return true;  // negligible weight
+  if (re < x0 + 3.0) return false;
+  return std::fabs(im) <= q * std::sqrt((re - x0) / p) / 1.5;
+}
+
+void exp_contour_nodes(const ExpContour& c, double t, std::vector<double>& shift,
+                       std::vector<double>& weight) {
+  // exp(-tR) e1 = sum_k w_k (zeta_k I - tR)^{-1} e1, w_k = -e^{-zeta} zeta' h / (2 pi i)
+  // (clockwise parabola), (zeta I - tR)^{-1} = -(1/t) (sigma I + R)^{-1}, sigma = -zeta/t;
+  // nodes u = k h, k = 0..K, the k > 0 ones standing for their conjugate pairs (x2, Re)
+  const int n = c.K + 1;
+  shift.assign(size_t(2 * n), 0.0);
+  weight.assign(size_t(2 * n), 0.0);
+  for (int k = 0; k < n; ++k) {
+    const double u = k * c.h;
+    const double zr = c.x0 + c.p * u * u, zi = c.q * u;
+    const double dzr = 2.0 * c.p * u, dzi = c.q;
+    // e^{-zeta} zeta'
+    const double ea = std::exp(-zr);
+    const double er = ea * std::cos(-zi), ei = ea * std::sin(-zi);
+    const double pr = er * dzr - ei * dzi, pim = er * dzi + ei * dzr;
+    // w = -(pr + i pim) h / (2 pi i) = -(h / 2pi) (pim - i pr)
+    const double f = -c.h / (2.0 * M_PI);
+    double wr = f * pim, wim = -f * pr;
+    // times -(1/t), and 2 for the conjugate pair
+    const double g = -(k == 0 ? 1.0 : 2.0) / t;
+    wr *= g;
+    wim *= g;
+    shift[size_t(2 * k)] = -zr / t;
+    shift[size_t(2 * k + 1)] = -zi / t;
+    weight[size_t(2 * k)] = wr;
+    weight[size_t(2 * k + 1)] = wim;
+  }
+}
+
+void launch_quad_expneg_cycle(const double* Rbar, int64_t ldr, int mkmax, int64_t cycle,
+                              QuadState* q, double* g, const SolveState* st_dev,
+                              double* partial, cudaStream_t st, int mk_replay,
+                              double coupling_replay) {
+  if (mkmax > kMaxMC) param_error("quadrature: m_r > 64 is not supported for exp_neg");
+  const size_t smem = 16 * size_t(mkmax) * size_t(mkmax);
+  if (smem > 48 * 1024)
+    RKMF_CUDA(cudaFuncSetAttribute(quad_expneg_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const bool replay = mk_replay >= 0;
+  quad_expneg_kernel<<<q->nq, 32, smem, st>>>(
+      Rbar, ldr, mkmax, reinterpret_cast<const cplx*>(q->shift),
+      reinterpret_cast<const cplx*>(q->weight), reinterpret_cast<cplx*>(q->pi),
+      reinterpret_cast<cplx*>(q->emx), cycle, st_dev, replay ? nullptr : partial, mk_replay,
+      coupling_replay);
+  if (!replay) quad_reduce_kernel<<<1, 128, 0, st>>>(q->nq, mkmax, partial, g, st_dev);
+  RKMF_CUDA(cudaGetLastError());
+}
 
 void launch_raccum_append(double* R, int64_t ld, int64_t M, const double* Rbar, int64_t ldr,
                           SolveState* st_dev, cudaStream_t st) {

@@ -290,14 +290,20 @@ double kappa_from_gram(const std::vector<double>& G, int m) {
   return std::sqrt(lmax / lmin);
 }
 
-// leftmost Ritz real part of R_m (Rbar column-major with leading dim ldr)
-double leftmost_ritz(const std::vector<double>& Rbar, int64_t ldr, int m) {
+// all Ritz values of R_m (Rbar column-major with leading dim ldr)
+void ritz_values(const std::vector<double>& Rbar, int64_t ldr, int m, std::vector<double>& wr,
+                 std::vector<double>& wi) {
   std::vector<double> h(size_t(m) * size_t(m), 0.0);
   for (int j = 0; j < m; ++j)
     for (int i = 0; i <= std::min(j + 1, m - 1); ++i)
       h[size_t(i) * m + j] = Rbar[size_t(j) * size_t(ldr) + size_t(i)];
-  std::vector<double> wr, wi;
   hessenberg_eigenvalues(h, m, wr, wi);
+}
+
+// leftmost Ritz real part of R_m
+double leftmost_ritz(const std::vector<double>& Rbar, int64_t ldr, int m) {
+  std::vector<double> wr, wi;
+  ritz_values(Rbar, ldr, m, wr, wi);
   return *std::min_element(wr.begin(), wr.end());
 }
 

@@ -759,8 +759,6 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     if (dense == RKMF_DENSE_AUTO) dense = fn_kind == RKMF_FN_EXP_NEG ? RKMF_DENSE_FULL : RKMF_DENSE_QUADRATURE;
     if (dense == RKMF_DENSE_FULL && fn_kind != RKMF_FN_EXP_NEG)
       param_error("rkmf_b200: FULL dense f is implemented for exp_neg only");
-    if (dense == RKMF_DENSE_QUADRATURE && fn_kind != RKMF_FN_INV_SQRT)
-      param_error("rkmf_b200: quadrature restart is implemented for inv_sqrt only");
     const int64_t n = A->view.n_rows;  // local rows when partitioned
     const int64_t m_eff = std::min(opts.m_r, A->n_rows_global());  // restart.cpp:38
     check_builder_args(A, S, m_eff);
@@ -831,7 +829,7 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     };
     QuadState q{};
     double* partial = nullptr;
-    if (dense == RKMF_DENSE_QUADRATURE) {
+    if (dense == RKMF_DENSE_QUADRATURE && fn_kind == RKMF_FN_INV_SQRT) {
       q.nq = opts.quad_nodes > 0 ? opts.quad_nodes : 512;
       q.shift = static_cast<double*>(ctx->qshift.ensure(sizeof(double) * size_t(q.nq)));
       q.weight = static_cast<double*>(ctx->qweight.ensure(sizeof(double) * size_t(q.nq)));
@@ -855,6 +853,10 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     }
 
     const double tol_break = 1e-14 * A->norm1;  // basis.cpp:118
+    ExpContour contour;
+    bool exp_fallback = false;
+    std::vector<double> ritz_re, ritz_im;  // t-scaled Ritz values of all cycles so far
+    std::vector<int64_t> cyc_M, cyc_mk;     // R_accum block offset and size per cycle
     int64_t M = 0;
     double first_update = -1.0;
     long long matvecs = 0, dot_n = 0, dot_d = 0, updates = 0, peak = 0;
@@ -899,14 +901,11 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       }
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e1), st));
       // ---- dense f ----
-      if (dense == RKMF_DENSE_FULL) {
+      // FULL exp(-t R_accum) e1 from the appended R_accum (restart.cpp:61-78)
+      auto full_expneg = [&] {
         const int64_t N = M + m_eff;
-        ensure_racc(N);
-        ctx->timed(3, [&] {
-          launch_raccum_append(Racc, ldR, M, bb.Rbar, bb.ldr, ctx->st_dev, st);
-          launch_dense_norm1(Racc, ldR, N, &ctx->st_dev->rnorm1, st);
-        });
-        ctx->launches += 2;
+        ctx->timed(3, [&] { launch_dense_norm1(Racc, ldR, N, &ctx->st_dev->rnorm1, st); });
+        ctx->launches++;
         ctx->sync_state();
         const double xn = std::fabs(fn_t) * ctx->st_host->rnorm1;
         int s = 0;
@@ -918,18 +917,79 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
           dense_expneg_e1(Racc, ldR, N, fn_t, s, ws, u, st, &nl);
           launch_make_g(u, M, int(m_eff), g, ctx->st_dev, st);
         });
-        ctx->launches += nl + 2;
-      } else {
+        ctx->launches += nl + 1;
+      };
+      if (M + m_eff <= Ncap) {  // R_accum (FULL, the exp fallback, rkmf_last_r_accum)
+        ensure_racc(M + m_eff);
+        ctx->timed(3, [&] { launch_raccum_append(Racc, ldR, M, bb.Rbar, bb.ldr, ctx->st_dev, st); });
+        ctx->launches++;
+      }
+      if (dense == RKMF_DENSE_FULL || exp_fallback) {
+        full_expneg();
+      } else if (fn_kind == RKMF_FN_INV_SQRT) {
         ctx->timed(3, [&] {
-          if (M + m_eff <= Ncap) {  // keep R_accum for rkmf_last_r_accum
-            ensure_racc(M + m_eff);
-            launch_raccum_append(Racc, ldR, M, bb.Rbar, bb.ldr, ctx->st_dev, st);
-            ctx->launches++;
-          }
           launch_quad_invsqrt_cycle(bb.Rbar, bb.ldr, int(m_eff), k, &q, g, ctx->st_dev, partial,
                                     st);
         });
         ctx->launches += 2;
+      } else {
+        // ExpNeg restart quadrature. The contour is designed from the Ritz
+        // values seen so far; when a cycle's Ritz values leave it, it is
+        // redesigned from all of them and the node states are rebuilt by
+        // replaying the earlier cycles' blocks of R_accum (kept on device),
+        // O(cycles N_q m^2) once. Only contours that would need > 4096 nodes
+        // send the solve to FULL.
+        ctx->sync_state();
+        const int mk = ctx->st_host->stopped;
+        std::vector<double> Rh(size_t(bb.ldr) * size_t(m_eff)), wr, wi;
+        RKMF_CUDA(cudaMemcpy(Rh.data(), bb.Rbar, sizeof(double) * Rh.size(), cudaMemcpyDeviceToHost));
+        ritz_values(Rh, bb.ldr, mk, wr, wi);
+        bool redesign = k == 1;
+        for (size_t i = 0; i < wr.size(); ++i) {
+          wr[i] *= fn_t;
+          wi[i] *= fn_t;
+          if (k > 1 && !contour.inside(wr[i], wi[i])) redesign = true;
+          ritz_re.push_back(wr[i]);
+          ritz_im.push_back(wi[i]);
+        }
+        if (redesign) {
+          contour = design_exp_contour(ritz_re, ritz_im);
+          if (contour.K > 4096) exp_fallback = true;
+        }
+        if (redesign && !exp_fallback) {
+          std::vector<double> hs, hw;
+          exp_contour_nodes(contour, fn_t, hs, hw);
+          q.nq = contour.K + 1;
+          q.shift = static_cast<double*>(ctx->qshift.ensure(sizeof(double) * hs.size()));
+          q.weight = static_cast<double*>(ctx->qweight.ensure(sizeof(double) * hw.size()));
+          q.pi = static_cast<double*>(ctx->qpi.ensure(sizeof(double) * hs.size()));
+          q.emx = static_cast<double*>(ctx->qemx.ensure(sizeof(double) * hs.size()));
+          partial = static_cast<double*>(ctx->partial.ensure(sizeof(double) * size_t(q.nq) * size_t(m_eff)));
+          std::vector<double> ones(hs.size(), 0.0);
+          for (size_t i = 0; i < ones.size(); i += 2) ones[i] = 1.0;
+          RKMF_CUDA(cudaMemcpyAsync(q.shift, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice, st));
+          RKMF_CUDA(cudaMemcpyAsync(q.weight, hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice, st));
+          RKMF_CUDA(cudaMemcpyAsync(q.pi, ones.data(), sizeof(double) * ones.size(), cudaMemcpyHostToDevice, st));
+          for (size_t j = 0; j < cyc_M.size(); ++j) {  // replay cycles 1..k-1
+            double coup = 0.0;
+            if (j > 0)  // R_accum(M_j, M_j - 1) = coupling * alpha (restart.cpp:67)
+              RKMF_CUDA(cudaMemcpy(&coup, Racc + (cyc_M[j] - 1) * ldR + cyc_M[j], sizeof(double),
+                                   cudaMemcpyDeviceToHost));
+            launch_quad_expneg_cycle(Racc + cyc_M[j] * ldR + cyc_M[j], ldR, int(m_eff),
+                                     int64_t(j) + 1, &q, g, ctx->st_dev, partial, st,
+                                     int(cyc_mk[j]), coup);
+            ctx->launches++;
+          }
+        }
+        if (exp_fallback) {
+          full_expneg();
+        } else {
+          ctx->timed(3, [&] {
+            launch_quad_expneg_cycle(bb.Rbar, bb.ldr, int(m_eff), k, &q, g, ctx->st_dev, partial,
+                                     st);
+          });
+          ctx->launches += 2;
+        }
       }
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e2), st));
       ctx->timed(4, [&] {
@@ -982,6 +1042,8 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       if (first_update < 0.0) first_update = yn;
       else if (yn > opts.divergence_factor * first_update)
         numerical_error("restart divergence (cycle " + std::to_string(k) + ")");
+      cyc_M.push_back(M);
+      cyc_mk.push_back(mk);
       M += mk;
       res->cycles = k;
       res->total_m = M;

@@ -195,6 +195,8 @@ bool launch_gram(int64_t n, int m, int64_t ldw, const double* W, const SolveStat
                  double* G, cudaStream_t st);
 double kappa_from_gram(const std::vector<double>& G, int m);
 double leftmost_ritz(const std::vector<double>& Rbar, int64_t ldr, int m);
+void ritz_values(const std::vector<double>& Rbar, int64_t ldr, int m, std::vector<double>& wr,
+                 std::vector<double>& wi);
 
 // densef.cu
 void launch_raccum_append(double* R, int64_t ldr_acc, int64_t M, const double* Rbar,
@@ -219,5 +221,23 @@ struct QuadState {
 void launch_quad_invsqrt_cycle(const double* Rbar, int64_t ldr, int mk, int64_t cycle,
                                QuadState* q, double* g, const SolveState* st_dev,
                                double* partial, cudaStream_t st);
+// ExpNeg quadrature (complex nodes, see densef.cu): shift/weight/pi/emx hold
+// nq complex values (interleaved re, im)
+// mk_replay >= 0: replay a past cycle (its R_accum block, its coupling) to
+// rebuild the node states after a contour change; no output
+void launch_quad_expneg_cycle(const double* Rbar, int64_t ldr, int mk, int64_t cycle,
+                              QuadState* q, double* g, const SolveState* st_dev,
+                              double* partial, cudaStream_t st, int mk_replay = -1,
+                              double coupling_replay = 0.0);
+// the contour for exp(-t z) from the t-scaled Ritz values of the first cycle
+struct ExpContour {
+  double x0 = 0, p = 1, q = 10, h = 0.05, lmin = 0;
+  int K = 0;
+  bool inside(double re, double im) const;  // with the design margins
+};
+ExpContour design_exp_contour(const std::vector<double>& wr, const std::vector<double>& wi);
+// host node arrays: shift (sigma = -zeta / t) and weight, complex interleaved
+void exp_contour_nodes(const ExpContour& c, double t, std::vector<double>& shift,
+                       std::vector<double>& weight);
 
 }  // namespace rkmf_b200

@@ -398,3 +398,29 @@ def test_cycle_diagnostics_match_numpy(rk, oracle, torch, name, N, sketched):
     # off by default
     r2 = rk.restarted_krylov(A, P.b, f, rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=2), S)
     assert np.isnan(r2.history[0].kappa_W)
+
+
+# ---------------- ExpNeg restart quadrature ----------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,N,m", [("cfg2", 16, None), ("cfg4", 14, None), ("cfg1", 48, None),
+                                      ("cfg1", 64, 10), ("cfg2", 24, 20)])
+def test_expneg_quadrature_matches_full_and_oracle(rk, oracle, torch, name, N, m):
+    """dense_f = quadrature for exp(-tA): O(N_q m^2) per cycle instead of
+    f(R_accum) in full; same f_hat as FULL and the oracle (1e-9), same cycles."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    mr = m or P.m
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    f = rk.FunctionSpec.exp_neg(P.t)
+    b = torch.tensor(P.b, device="cuda")
+    rq = rk.restarted_krylov(A, b, f, rk.RestartOptions(m_r=mr, tol=P.tol, k_max=P.k_max,
+                                                        dense_f="quadrature"), S)
+    rf = rk.restarted_krylov(A, b, f, rk.RestartOptions(m_r=mr, tol=P.tol, k_max=P.k_max), S)
+    OS = oracle.make_sketch(P.d, P.n, P.zeta, 1)
+    o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, oracle.KIND_EXP_NEG, P.t,
+                                m_r=mr, tol=P.tol, k_max=P.k_max, S=OS)
+    fq, ff = rq.f_hat.cpu().numpy(), rf.f_hat.cpu().numpy()
+    assert rq.converged and abs(rq.cycles - o.cycles) <= 1 and rq.cycles == rf.cycles
+    assert np.linalg.norm(fq - ff) <= 1e-10 * np.linalg.norm(ff)
+    assert np.linalg.norm(fq - o.f_hat) <= 1e-9 * np.linalg.norm(o.f_hat)
