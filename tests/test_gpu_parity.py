@@ -424,3 +424,60 @@ def test_expneg_quadrature_matches_full_and_oracle(rk, oracle, torch, name, N, m
     assert rq.converged and abs(rq.cycles - o.cycles) <= 1 and rq.cycles == rf.cycles
     assert np.linalg.norm(fq - ff) <= 1e-10 * np.linalg.norm(ff)
     assert np.linalg.norm(fq - o.f_hat) <= 1e-9 * np.linalg.norm(o.f_hat)
+
+
+# ---------------- acceptance c8/c9 and the R_accum pattern on device ----------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("eps,vx,vy", [(0.1, 1.0, 0.01), (0.01, 1.0, 0.01), (0.01, 1.0, 1.0)])
+def test_restarted_convergence_conv_diff_grids(rk, torch, eps, vx, vy):
+    """acceptance.cpp:346-425 (c8/c9) on 60x60 convection-diffusion grids: m_r = 20,
+    d = 320, zeta in {1, 4}, tol = 1e-13 ||b||, k_max = 50. Both builders reach
+    the exact exp(-tA)b (scipy expm_multiply): classical <= 1e-8, randomized
+    <= 1e-9; at the last common cycle randomized error <= 10x classical."""
+    from scipy.sparse.linalg import expm_multiply
+    A = H.conv_diff_2d(60, 60, eps, vx, vy)
+    n = A.shape[0]
+    b = H.random_vector(n, 11)
+    t = 2.0 / abs(A).sum(axis=0).max()
+    ref = expm_multiply(-t * A, b)
+    dA = rk.SparseMatrix.from_scipy(A)
+    f = rk.FunctionSpec.exp_neg(t)
+    opts = rk.RestartOptions(m_r=20, k_max=50, tol=1e-13 * np.linalg.norm(b))
+    rc = rk.restarted_krylov(dA, b, f, opts, None, reference=ref)
+    ec = [h.error_vs_reference for h in rc.history]
+    assert min(ec) <= 1e-8
+    for zeta in (1, 4):
+        S = rk.make_sketch(320, n, zeta, 1)
+        rr = rk.restarted_krylov(dA, b, f, opts, S, reference=ref)
+        er = [h.error_vs_reference for h in rr.history]
+        assert min(er) <= 1e-9, (zeta, min(er))
+        common = min(len(ec), len(er))
+        assert er[common - 1] <= 10.0 * max(ec[common - 1], 1e-15)
+
+
+@pytest.mark.gpu
+def test_r_accum_block_pattern(rk, torch):
+    """test_restart.cpp:131-164: the accumulated compression keeps the block
+    lower-bidiagonal pattern exactly (zeros are exact), couplings nonzero."""
+    A = H.conv_diff_2d(12, 12, 0.1, 0.01, 1.0)
+    b = H.random_vector(A.shape[0], 3)
+    m_r = 8
+    S = rk.make_sketch(64, A.shape[0], 4, 12)
+    r = rk.restarted_krylov(rk.SparseMatrix.from_scipy(A), b,
+                            rk.FunctionSpec.exp_neg(1.0 / abs(A).sum(axis=0).max()),
+                            rk.RestartOptions(m_r=m_r, tol=1e-30, k_max=4), S)
+    assert r.cycles == 4
+    R = r.R_accum
+    assert R.shape == (4 * m_r, 4 * m_r)
+    checked = 0
+    for i in range(R.shape[0]):
+        for j in range(R.shape[1]):
+            bi, bj = i // m_r, j // m_r
+            in_diag = bi == bj and (i % m_r) <= (j % m_r) + 1
+            coupling = bi == bj + 1 and i % m_r == 0 and j % m_r == m_r - 1
+            if not in_diag and not coupling:
+                checked += 1
+                assert R[i, j] == 0.0, (i, j)
+    assert checked > 0
+    for k in range(1, 4):
+        assert R[k * m_r, k * m_r - 1] != 0.0
