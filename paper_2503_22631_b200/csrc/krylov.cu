@@ -294,6 +294,7 @@ constexpr int kMaxCoef = 1024;
 
 // W[:,k+1] = (z - W[:,0..k] r) / r_kk   (basis.cpp:135). Two rows per thread
 // with 16-byte loads; the k+1 column streams are issued 4 at a time.
+template <int UNR>
 __global__ void __launch_bounds__(kUpdThreads)
     basis_update_kernel(int64_t n, int k, int64_t ldw, double* W, const double* __restrict__ z,
                         const double* __restrict__ Rbar, int64_t ldr, const SolveState* st) {
@@ -310,12 +311,12 @@ __global__ void __launch_bounds__(kUpdThreads)
        i2 += int64_t(gridDim.x) * kUpdThreads) {
     double a0 = 0.0, a1 = 0.0;
     int c = 0;
-    for (; c + 3 <= k; c += 4) {
-      double2 v[4];
+    for (; c + UNR - 1 <= k; c += UNR) {
+      double2 v[UNR];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const double2*>(W + int64_t(c + q) * ldw) + i2);
+      for (int q = 0; q < UNR; ++q) v[q] = __ldcs(reinterpret_cast<const double2*>(W + int64_t(c + q) * ldw) + i2);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < UNR; ++q) {
         a0 += v[q].x * coef[c + q];
         a1 += v[q].y * coef[c + q];
       }
@@ -492,15 +493,32 @@ void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, doubl
 void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double* z,
                          const double* Rbar, int64_t ldr, const SolveState* st_dev,
                          cudaStream_t st) {
-  launch_maybe_pdl(basis_update_kernel, dim3(stream_grid(std::max<int64_t>(n / 2, 1), kUpdThreads)),
-                   dim3(kUpdThreads), 0, st, n, k, ldw, W, z, Rbar, ldr, st_dev);
+  // Blocks per SM: 24 (three waves of 8 resident) beats one resident wave by
+  // 4% on the whole cfg2 solve: the (k+1)-column read streams keep more DRAM
+  // pages open with the extra in-flight blocks (read-only microbenchmark of 26
+  // streams: 6.49 -> 6.86 TB/s). RKMF_K4_GRIDX / RKMF_K4_UNROLL override.
+  static const int unr = [] { const char* e = getenv("RKMF_K4_UNROLL"); return e ? atoi(e) : 4; }();
+  static const int gx = [] { const char* e = getenv("RKMF_K4_GRIDX"); return e ? atoi(e) : 24; }();
+  const int64_t need = (std::max<int64_t>(n / 2, 1) + kUpdThreads - 1) / kUpdThreads;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sm_count()) * gx)));
+  if (unr == 8)
+    launch_maybe_pdl(basis_update_kernel<8>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, W, z,
+                     Rbar, ldr, st_dev);
+  else if (unr == 2)
+    launch_maybe_pdl(basis_update_kernel<2>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, W, z,
+                     Rbar, ldr, st_dev);
+  else
+    launch_maybe_pdl(basis_update_kernel<4>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, W, z,
+                     Rbar, ldr, st_dev);
 }
 
 void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const double* z,
                          const double* Rbar, int64_t ldr, const double* g, double* f_hat,
                          const double* ref, SolveState* st_dev, cudaStream_t st) {
   if (m_eff > kMaxCoef) param_error("restart: m_r > 1024 is not supported on device");
-  final_update_kernel<<<stream_grid(n, kUpdThreads), kUpdThreads, 0, st>>>(
+  const int64_t fneed = (std::max<int64_t>(n, 1) + kUpdThreads - 1) / kUpdThreads;
+  final_update_kernel<<<int(std::max<int64_t>(1, std::min<int64_t>(fneed, int64_t(sm_count()) * 24))),
+                        kUpdThreads, 0, st>>>(
       n, m_eff, ldw, W, z, Rbar, ldr, g, f_hat, ref, st_dev);
   RKMF_CUDA(cudaGetLastError());
 }
