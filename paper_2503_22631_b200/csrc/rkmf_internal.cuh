@@ -153,6 +153,9 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
                         const double* xscale_dev, double* z, double* pacc,
                         const int32_t* stop_flag, int step, int grid, cudaStream_t st);
 int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode);
+// the same pipeline for the sketch of x alone (mode 2)
+bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double* xscale_dev,
+                             double* pacc, cudaStream_t st);
 // TMA-pipelined mode-1 kernel (spmv_pipe.cu); returns false when not applicable.
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z, double* pacc,

@@ -180,6 +180,9 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
   if (mode == 1 && A && S && use_pipe() &&
       launch_spmv_sketch_pipe(A, S, x, xscale_dev, z, pacc, stop_flag, step, st))
     return;
+  if (mode == 2 && S && !stop_flag && use_pipe() &&
+      launch_sketch_only_pipe(S, x, xscale_dev, pacc, st))
+    return;
   if (grid <= 0) grid = spmv_sketch_grid(A, S, mode);
   const uint16_t* toff = S ? S->tile_off : nullptr;
   const uint8_t* tent = S ? S->tile_ent : nullptr;

@@ -117,8 +117,9 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     const uint64_t mpol = l2_policy(l2_hints);
     // row-pointer pair of the next tile, prefetched one iteration ahead so the
     // bulk copies of a tile are issued without a dependent global round trip
+    // rp == nullptr: sketch of x only (the start vector), no matrix stream
     long long nrs = 0, nre = 0;
-    if (blockIdx.x < num_tiles) {
+    if (rp && blockIdx.x < num_tiles) {
       const int64_t r0 = int64_t(blockIdx.x) * kTileRows;
       nrs = (long long)rp[r0];
       nre = (long long)rp[min(n, r0 + kTileRows)];
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const long long rs = nrs, re = nre;
       const int64_t nt = tile + gridDim.x;
-      if (nt < num_tiles) {
+      if (rp && nt < num_tiles) {
         nrs = (long long)rp[nt * kTileRows];
         nre = (long long)rp[min(n, nt * kTileRows + kTileRows)];
       }
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       const long long vs0 = rs & ~1LL, cs0 = rs & ~3LL;
       const uint32_t vbytes = uint32_t(((re - vs0) * 8 + 15) & ~15LL);
       const uint32_t cbytes = uint32_t(((re - cs0) * 4 + 15) & ~15LL);
-      const uint32_t rbytes = sizeof(RP) == 4 ? 528u : 1040u;
+      const uint32_t rbytes = !rp ? 0u : (sizeof(RP) == 4 ? 528u : 1040u);
       const uint32_t obytes = uint32_t(off_stride) * 2u;
       const uint32_t ebytes = uint32_t(kTileRows * zeta);
       TileMeta* meta = reinterpret_cast<TileMeta*>(st + L.meta);
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       meta->cshift = int(rs - cs0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&full[s], rbytes + (re > rs ? vbytes + cbytes : 0u) + obytes + ebytes);
-      bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s], pol);
+      if (rp) bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s], pol);
       if (re > rs) {
         bulk_g2s(st + L.val, val + vs0, vbytes, &full[s], pol);
         bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s], pol);
@@ -211,11 +212,11 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       const int64_t row = tile * kTileRows + rl;
       const bool live = row < n;
       int lo = 0, hi = 0;
-      if (live) {
+      if (live && rp) {
         lo = int((long long)rps[rl] - meta.rs);
         hi = int((long long)rps[rl + 1] - meta.rs);
       }
-      double sum = 0.0;
+      double sum = (!rp && live && part == 0) ? x[row] : 0.0;  // sketch-only: z = x
       for (int e = lo + part; e < hi; e += 8 * TPR) {
         double v[8], xv[8];
 #pragma unroll
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       for (int o = 1; o < TPR; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       sum *= xs;
       if (part == 0) {
-        if (live) z[row] = sum;
+        if (live && z) z[row] = sum;
         const double zt = live ? sum * sscale : 0.0;
         zs[rl] = zt;
         zs[kTileRows + rl] = -zt;
@@ -304,10 +305,16 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   // of them: take the configuration that keeps >= 64 KB per SM ahead (HBM
   // latency x per-SM bandwidth), then the one with more resident blocks, then
   // more stages. Cached per shape.
-  static thread_local int64_t key_c = -1;
-  static thread_local int best_s = 0, best_per = 0;
+  // (a few shapes per thread: the step SpMV and the start sketch alternate)
+  static thread_local int64_t keys[4] = {-1, -1, -1, -1};
+  static thread_local int bests[4][2];
+  static thread_local int next_slot = 0;
   const int64_t key = (int64_t(A->cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP);
-  if (key != key_c) {
+  int slot = -1;
+  for (int i = 0; i < 4; ++i)
+    if (keys[i] == key) slot = i;
+  int best_s = slot >= 0 ? bests[slot][0] : 0, best_per = slot >= 0 ? bests[slot][1] : 0;
+  if (slot < 0) {
     best_s = 0;
     best_per = 0;
     int64_t best_ahead = -1;
@@ -329,7 +336,11 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
         best_s = s;
       }
     }
-    key_c = key;
+    slot = next_slot;
+    next_slot = (next_slot + 1) & 3;
+    keys[slot] = key;
+    bests[slot][0] = best_s;
+    bests[slot][1] = best_per;
   }
   if (best_s == 0) return false;
   const int stages = best_s, per_sm = best_per;
@@ -397,6 +408,24 @@ bool launch_pipe_rp(const CsrView* A, const SketchView* S, const double* x,
 }
 
 }  // namespace
+
+// sketch of x alone through the same pipeline (no matrix stream): the start
+// vector's S*start (basis.cpp:103-104), mode 2 of launch_spmv_sketch
+bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double* xscale_dev,
+                             double* pacc, cudaStream_t st) {
+  CsrView v{};
+  v.n_rows = S->n;
+  v.n_cols = S->n;
+  v.nnz = 0;
+  v.row_ptr = nullptr;
+  v.rp64 = false;
+  v.col = nullptr;
+  v.val = nullptr;
+  v.cap = 8;
+  v.max_tile_nnz = 0;
+  v.padded = true;
+  return launch_pipe_t<int32_t, 1, 1>(&v, S, x, xscale_dev, nullptr, pacc, nullptr, 0, st);
+}
 
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z, double* pacc,
