@@ -294,10 +294,25 @@ constexpr int kMaxCoef = 1024;
 
 // W[:,k+1] = (z - W[:,0..k] r) / r_kk   (basis.cpp:135). Two rows per thread
 // with 16-byte loads; the k+1 column streams are issued 4 at a time.
-template <int UNR>
+// W and z are read with ld.global.lu (last use): 2.4% faster on the cfg2 solve
+// than evict-first streaming loads, 6% faster than default loads. rev walks
+// the rows from the end (RKMF_K4_ORDER=1 alternates per step, 2 always): the
+// next step would then start on the rows still in L2, but it measured no
+// faster, nor did pinning the last-read rows with evict_last. The whole-solve
+// time is sensitive to this kernel's code generation (the same loads without
+// the runtime rev select measured 4% slower), so rev stays.
+template <int LD>
+__device__ __forceinline__ double2 ld_w(const double2* p) {
+  if (LD == 0) return __ldcs(p);
+  if (LD == 1) return __ldg(p);
+  return __ldlu(p);
+}
+
+template <int UNR, int LD>
 __global__ void __launch_bounds__(kUpdThreads)
     basis_update_kernel(int64_t n, int k, int64_t ldw, double* W, const double* __restrict__ z,
-                        const double* __restrict__ Rbar, int64_t ldr, const SolveState* st) {
+                        const double* __restrict__ Rbar, int64_t ldr, const SolveState* st,
+                        int rev) {
   pdl_wait_then_trigger();
   if (st->stopped <= k) return;  // no update at (or after) a breakdown step
   __shared__ double coef[kMaxCoef];
@@ -307,14 +322,17 @@ __global__ void __launch_bounds__(kUpdThreads)
   const double rkk = Rbar[int64_t(k) * ldr + k + 1];
   double* out = W + int64_t(k + 1) * ldw;
   const int64_t n2 = n / 2;
-  for (int64_t i2 = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x; i2 < n2;
-       i2 += int64_t(gridDim.x) * kUpdThreads) {
+  for (int64_t j2 = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x; j2 < n2;
+       j2 += int64_t(gridDim.x) * kUpdThreads) {
+    const int64_t i2 = rev ? n2 - 1 - j2 : j2;
     double a0 = 0.0, a1 = 0.0;
     int c = 0;
     for (; c + UNR - 1 <= k; c += UNR) {
       double2 v[UNR];
 #pragma unroll
-      for (int q = 0; q < UNR; ++q) v[q] = __ldcs(reinterpret_cast<const double2*>(W + int64_t(c + q) * ldw) + i2);
+      for (int q = 0; q < UNR; ++q) {
+        v[q] = ld_w<LD>(reinterpret_cast<const double2*>(W + int64_t(c + q) * ldw) + i2);
+      }
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
         a0 += v[q].x * coef[c + q];
@@ -322,11 +340,11 @@ __global__ void __launch_bounds__(kUpdThreads)
       }
     }
     for (; c <= k; ++c) {
-      const double2 v = __ldcs(reinterpret_cast<const double2*>(W + int64_t(c) * ldw) + i2);
+      const double2 v = ld_w<LD>(reinterpret_cast<const double2*>(W + int64_t(c) * ldw) + i2);
       a0 += v.x * coef[c];
       a1 += v.y * coef[c];
     }
-    const double2 zz = __ldcs(reinterpret_cast<const double2*>(z) + i2);
+    const double2 zz = ld_w<LD>(reinterpret_cast<const double2*>(z) + i2);
     double2 o;
     o.x = (zz.x - a0) / rkk;
     o.y = (zz.y - a1) / rkk;
@@ -501,15 +519,25 @@ void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double*
   static const int gx = [] { const char* e = getenv("RKMF_K4_GRIDX"); return e ? atoi(e) : 24; }();
   const int64_t need = (std::max<int64_t>(n / 2, 1) + kUpdThreads - 1) / kUpdThreads;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sm_count()) * gx)));
-  if (unr == 8)
-    launch_maybe_pdl(basis_update_kernel<8>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, W, z,
-                     Rbar, ldr, st_dev);
-  else if (unr == 2)
-    launch_maybe_pdl(basis_update_kernel<2>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, W, z,
-                     Rbar, ldr, st_dev);
-  else
-    launch_maybe_pdl(basis_update_kernel<4>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, W, z,
-                     Rbar, ldr, st_dev);
+  // RKMF_K4_LOAD: 0 streaming (evict-first), 1 default, 2 last-use (default)
+  static const int ldm = [] { const char* e = getenv("RKMF_K4_LOAD"); return e ? atoi(e) : 2; }();
+  static const int order = [] { const char* e = getenv("RKMF_K4_ORDER"); return e ? atoi(e) : 0; }();
+  const int rev = order == 1 ? (k & 1) : (order == 2 ? 1 : 0);
+#define RKMF_K4(U, L)                                                                       \
+  launch_maybe_pdl(basis_update_kernel<U, L>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, \
+                   W, z, Rbar, ldr, st_dev, rev)
+  if (unr == 8) {
+    RKMF_K4(8, 2);
+  } else if (unr == 2) {
+    RKMF_K4(2, 2);
+  } else if (ldm == 1) {
+    RKMF_K4(4, 1);
+  } else if (ldm == 0) {
+    RKMF_K4(4, 0);
+  } else {
+    RKMF_K4(4, 2);
+  }
+#undef RKMF_K4
 }
 
 void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const double* z,
@@ -517,9 +545,9 @@ void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const dou
                          const double* ref, SolveState* st_dev, cudaStream_t st) {
   if (m_eff > kMaxCoef) param_error("restart: m_r > 1024 is not supported on device");
   const int64_t fneed = (std::max<int64_t>(n, 1) + kUpdThreads - 1) / kUpdThreads;
-  final_update_kernel<<<int(std::max<int64_t>(1, std::min<int64_t>(fneed, int64_t(sm_count()) * 24))),
-                        kUpdThreads, 0, st>>>(
-      n, m_eff, ldw, W, z, Rbar, ldr, g, f_hat, ref, st_dev);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(fneed, int64_t(sm_count()) * 24)));
+  final_update_kernel<<<grid, kUpdThreads, 0, st>>>(n, m_eff, ldw, W, z, Rbar, ldr, g, f_hat, ref,
+                                                    st_dev);
   RKMF_CUDA(cudaGetLastError());
 }
 
