@@ -31,7 +31,8 @@ from typing import List, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librkmf_b200.so")
+# RKMF_LIB_PATH selects an alternative build (A/B experiments with build flags)
+LIB_PATH = os.environ.get("RKMF_LIB_PATH") or os.path.join(_HERE, "_lib", "librkmf_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 RKMF_OK = 0
@@ -107,6 +108,7 @@ SYMBOLS = [
     ("rkmf_matrix_create_device", C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _PP]),
     ("rkmf_matrix_destroy", C.c_int, [_P]),
     ("rkmf_matrix_info", C.c_int, [_P, _P, _P, _P, _P]),
+    ("rkmf_matrix_dia", C.c_int, [_P, C.c_int, _P]),
     ("rkmf_sketch_create", C.c_int, [_P, _I64, _I64, _I64, _U64, _PP]),
     ("rkmf_sketch_destroy", C.c_int, [_P]),
     ("rkmf_sketch_set_scale", C.c_int, [_P, _D]),
@@ -245,6 +247,21 @@ class SparseMatrix:
     @property
     def shape(self):
         return (self.n_rows, self.n_cols)
+
+    def set_diagonal_copy(self, enable: bool) -> int:
+        """Drop (False) or build (True, if the matrix qualifies) the diagonal
+        copy the fused SpMV + sketch streams instead of the CSR arrays;
+        returns the diagonal count (0 = CSR only). Results are identical."""
+        nd = C.c_int()
+        self.ctx.check(lib().rkmf_matrix_dia(self.h, int(bool(enable)), C.byref(nd)))
+        return nd.value
+
+    @property
+    def ndiag(self) -> int:
+        """Diagonals of the stored diagonal copy (0 = CSR only)."""
+        nd = C.c_int()
+        self.ctx.check(lib().rkmf_matrix_dia(self.h, 2, C.byref(nd)))
+        return nd.value
 
     @classmethod
     def from_csr(cls, row_ptr, col_idx, values, n_cols: Optional[int] = None,

@@ -90,6 +90,7 @@ void finish_matrix(rkmf_matrix* M, int64_t max_tile_nnz, bool require_sorted) {
   colsum.release();
   if (hf[0]) shape_error("invalid CSR structure (sparse.cpp:61-81 invariants)");
   if (hf[1]) numerical_error("non-finite matrix entry");
+  if (dia_enabled_by_env()) build_dia(M);
 }
 
 __global__ void rp_narrow_kernel(int64_t n, const int64_t* __restrict__ src, int32_t* dst) {
@@ -495,11 +496,22 @@ int rkmf_matrix_destroy(rkmf_matrix* M) {
   cudaSetDevice(M->device);
   if (M->halo.send_idx) cudaFree(M->halo.send_idx);
   if (M->halo.sendbuf) cudaFree(M->halo.sendbuf);
+  drop_dia(M);
   if (M->rp) cudaFree(M->rp);
   if (M->col) cudaFree(M->col);
   if (M->val) cudaFree(M->val);
   delete M;
   return RKMF_OK;
+}
+
+int rkmf_matrix_dia(rkmf_matrix* M, int enable, int* ndiag) {
+  if (!M) return RKMF_PARAMETER_ERROR;
+  return guarded(M->ctx, [&] {
+    set_device(M->ctx);
+    if (enable == 1) build_dia(M);
+    else if (enable == 0) drop_dia(M);  // other values: query only
+    if (ndiag) *ndiag = M->view.ndiag;
+  });
 }
 
 int rkmf_matrix_info(const rkmf_matrix* M, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,

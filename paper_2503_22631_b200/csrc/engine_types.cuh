@@ -134,6 +134,8 @@ struct rkmf_matrix {
   int32_t* col = nullptr;
   double* val = nullptr;
   double norm1 = 0.0;
+  double* dia_val = nullptr;  // optional diagonal copy (dia.cu)
+  int32_t* dia_off = nullptr;  // its sorted diagonal offsets
   bool partitioned = false;
   HaloPlan halo;
   int64_t n_rows_global() const { return partitioned ? halo.n_global : view.n_rows; }
@@ -165,6 +167,10 @@ struct rkmf_sketch {
 
 
 namespace rkmf_b200 {
+// dia.cu
+void build_dia(rkmf_matrix* M);
+void drop_dia(rkmf_matrix* M);
+bool dia_enabled_by_env();
 // comm.cu
 void comm_allreduce_sum(rkmf_context* ctx, double* buf, size_t count);
 void comm_halo_exchange(rkmf_context* ctx, const rkmf_matrix* A, double* x);

@@ -104,7 +104,13 @@ struct CsrView {
   int cap;  // products staged per chunk (shared memory)
   int64_t max_tile_nnz;  // largest nonzero count of a 128-row tile
   bool padded;           // arrays carry the tail padding the TMA path needs
+  // optional diagonal copy (dia.cu): [tile][diag][128] values at the sorted
+  // column offsets doff; ndiag == 0 when the matrix has none
+  const double* dval;
+  const int32_t* doff;
+  int ndiag;
 };
+constexpr int kMaxDiag = 32;
 // Row-pointer tail padding (entries) and value/column padding (elements)
 // allocated by the engine so 16-byte-rounded bulk copies stay in bounds.
 constexpr int64_t kRpPad = 136;
@@ -125,9 +131,7 @@ __host__ __device__ inline int64_t tile_off_stride(int64_t d) { return (2 * d + 
 // 2NT-1-t, 2NT+t, 4NT-1-t, ... (snake), so each warp walks 32 slots of
 // near-equal length and every thread gets about the same number of entries. zs2 holds the scaled
 // z of the tile's rows twice, zs2[r] = +z_r and zs2[128 + r] = -z_r, so an
-// entry byte (local row | sign << 7) indexes its signed value directly. Reading
-// one entry past a slot's end stays inside shared memory (the stage layouts
-// place zs2 after the entries) and is masked.
+// entry byte (local row | sign << 7) indexes its signed value directly.
 template <int NT = 128>
 __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t* off,
                                                    const uint8_t* ent, const double* zs2,
@@ -138,13 +142,15 @@ __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t*
     if (s >= d) continue;
     const int e0 = off[s], e1 = off[s + 1];
     double a0 = 0.0, a1 = 0.0;
+    int e = e0;
 #pragma unroll 1
-    for (int e = e0; e < e1; e += 2) {
+    for (; e + 1 < e1; e += 2) {
       const double v0 = zs2[ent[e]];
       const double v1 = zs2[ent[e + 1]];
       a0 += v0;
-      a1 += e + 1 < e1 ? v1 : 0.0;
+      a1 += v1;
     }
+    if (e < e1) a0 += zs2[ent[e]];  // odd length: no masked over-read (bank conflicts)
     acc[bins[s]] += a0 + a1;
   }
 }

@@ -36,17 +36,19 @@ struct StageLayout {
   uint32_t rp, val, col, off, ent, zs, meta, stride;
 };
 
+// FMT 0 (CSR): row pointers, up to cap values and columns (+ alignment slack);
+// FMT 1 (DIA): cap = ndiag * 128 values, no row pointers or columns.
 __host__ __device__ inline StageLayout stage_layout(int rp_bytes, int cap, int off_stride,
-                                                    int zeta) {
+                                                    int zeta, int fmt) {
   auto r16 = [](uint32_t x) { return (x + 15u) & ~15u; };
   StageLayout L;
   uint32_t o = 0;
   L.rp = o;
-  o += r16(uint32_t(rp_bytes) * 136u);
+  o += fmt ? 0u : r16(uint32_t(rp_bytes) * 136u);
   L.val = o;
-  o += r16(uint32_t(cap + 2) * 8u);
+  o += fmt ? uint32_t(cap) * 8u : r16(uint32_t(cap + 2) * 8u);
   L.col = o;
-  o += r16(uint32_t(cap + 4) * 4u);
+  o += fmt ? 0u : r16(uint32_t(cap + 4) * 4u);
   L.off = o;
   o += r16(uint32_t(off_stride) * 2u);
   L.ent = o;
@@ -81,7 +83,11 @@ constexpr int spmv_threads() { return G * kTileRows * TPR; }
 template <int TPR, int G>
 constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads + 32; }
 
-template <typename RP, int TPR, int G>
+// FMT 1 streams a diagonal (DIA) copy of the matrix instead of the CSR arrays
+// (build_dia, dia.cu): val = [tile][diag][128] values, doff = the ndiag sorted
+// column offsets; x is read at row + doff[q] (coalesced across a warp).
+// (a 4-blocks-per-SM register cap, 56 registers with spills, measured slower)
+template <typename RP, int TPR, int G, int FMT>
 __global__ void __launch_bounds__(block_threads<TPR, G>())
     spmv_sketch_pipe_kernel(int64_t n, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ val, const double* __restrict__ x,
@@ -89,12 +95,16 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
                             int cap, int d, int zeta, int off_stride,
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
                             double sscale, double* pacc, const int32_t* stop, int step,
-                            int nstages, int l2_hints, int debug) {
+                            int nstages, int l2_hints, int debug, const int32_t* __restrict__ doff,
+                            int ndiag, int64_t ncols) {
   constexpr int kSpmv = spmv_threads<TPR, G>();
   constexpr int kGroup = kTileRows * TPR;
   extern __shared__ __align__(128) unsigned char smem[];
-  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
+  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, FMT);
   __shared__ __align__(8) uint64_t full[kStages], zsr[kStages], empty[kStages];
+  __shared__ int32_t doff_s[FMT ? kMaxDiag : 1];
+  if (FMT)
+    for (int q = threadIdx.x; q < ndiag; q += blockDim.x) doff_s[q] = doff[q];
   double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d], sketch threads
   const int t = threadIdx.x;
   if (t == 0) {
@@ -119,7 +129,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     // bulk copies of a tile are issued without a dependent global round trip
     // rp == nullptr: sketch of x only (the start vector), no matrix stream
     long long nrs = 0, nre = 0;
-    if (rp && blockIdx.x < num_tiles) {
+    if (!FMT && rp && blockIdx.x < num_tiles) {
       const int64_t r0 = int64_t(blockIdx.x) * kTileRows;
       nrs = (long long)rp[r0];
       nre = (long long)rp[min(n, r0 + kTileRows)];
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const long long rs = nrs, re = nre;
       const int64_t nt = tile + gridDim.x;
-      if (rp && nt < num_tiles) {
+      if (!FMT && rp && nt < num_tiles) {
         nrs = (long long)rp[nt * kTileRows];
         nre = (long long)rp[min(n, nt * kTileRows + kTileRows)];
       }
@@ -142,6 +152,18 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       const uint32_t rbytes = !rp ? 0u : (sizeof(RP) == 4 ? 528u : 1040u);
       const uint32_t obytes = uint32_t(off_stride) * 2u;
       const uint32_t ebytes = uint32_t(kTileRows * zeta);
+      if (FMT) {  // one contiguous block of ndiag x 128 values
+        const uint32_t dbytes = uint32_t(cap) * 8u;
+        mbar_expect_tx(&full[s], dbytes + obytes + ebytes);
+        bulk_g2s(st + L.val, val + tile * int64_t(cap), dbytes, &full[s], pol);
+        bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], mpol);
+        bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], mpol);
+        if (++s == nstages) {
+          s = 0;
+          if (it >= nstages) eph ^= 1u;
+        }
+        continue;
+      }
       TileMeta* meta = reinterpret_cast<TileMeta*>(st + L.meta);
       meta->rs = rs;
       meta->vshift = int(rs - vs0);
@@ -199,8 +221,28 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
   const int rl = gt / TPR, part = gt % TPR;
   int it = g;
   int s = g % nstages;
+  // FMT 2 (at most 8 diagonals): the x reads of a tile do not depend on the
+  // staged data, so each thread loads the next tile's x while this tile's
+  // stage is still landing (one tile of x latency hidden per group)
+  double xnext[FMT == 2 ? 8 : 1];
+  auto load_x = [&](int64_t tl, double* dst) {
+    const int64_t row = tl * kTileRows + rl;
+#pragma unroll
+    for (int q = 0; q < (FMT == 2 ? 8 : 1); ++q) {
+      const int64_t c = row + doff_s[min(q, ndiag - 1)];
+      dst[q] = (row < n && q < ndiag && c >= 0 && c < ncols) ? __ldg(x + c) : 0.0;
+    }
+  };
+  if (FMT == 2 && blockIdx.x + int64_t(g) * gridDim.x < num_tiles)
+    load_x(blockIdx.x + int64_t(g) * gridDim.x, xnext);
   for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
        tile += int64_t(G) * gridDim.x, it += G) {
+    double xcur[FMT == 2 ? 8 : 1];
+    if (FMT == 2) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xcur[q] = xnext[q];
+      if (tile + int64_t(G) * gridDim.x < num_tiles) load_x(tile + int64_t(G) * gridDim.x, xnext);
+    }
     mbar_wait(&full[s], uint32_t(it / nstages) & 1u);
     unsigned char* st = smem + s * L.stride;
     if (!(debug & 4)) {
@@ -212,11 +254,35 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       const int64_t row = tile * kTileRows + rl;
       const bool live = row < n;
       int lo = 0, hi = 0;
-      if (live && rp) {
+      if (!FMT && live && rp) {
         lo = int((long long)rps[rl] - meta.rs);
         hi = int((long long)rps[rl + 1] - meta.rs);
       }
-      double sum = (!rp && live && part == 0) ? x[row] : 0.0;  // sketch-only: z = x
+      double sum = (!FMT && !rp && live && part == 0) ? x[row] : 0.0;  // sketch-only: z = x
+      if (FMT == 2 && live) {
+        const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < ndiag) sum += vt[q * kTileRows] * xcur[q];
+      }
+      if (FMT == 1 && live) {
+        // the CSR row's entries in column order (a sequential sum like the
+        // reference's); padding slots hold 0.0, an exact no-op term
+        const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
+        for (int q0 = 0; q0 < ndiag; q0 += 8) {
+          double v[8], xv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int qq = min(q0 + q, ndiag - 1);
+            const int64_t c = row + doff_s[qq];
+            v[q] = vt[qq * kTileRows];
+            xv[q] = (c >= 0 && c < ncols) ? __ldg(x + c) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q0 + q < ndiag) sum += v[q] * xv[q];
+        }
+      }
       for (int e = lo + part; e < hi; e += 8 * TPR) {
         double v[8], xv[8];
 #pragma unroll
@@ -245,8 +311,8 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
 }
 
 template <typename RP>
-size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages) {
-  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta);
+size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages, int fmt) {
+  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, fmt);
   return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
 }
 
@@ -293,13 +359,14 @@ int sms() {
   return v;
 }
 
-template <typename RP, int TPR, int G>
+template <typename RP, int TPR, int G, int FMT = 0>
 bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
                    int step, cudaStream_t st) {
   constexpr int kThreads = block_threads<TPR, G>();
   const int off_stride = int(tile_off_stride(S->d));
-  auto fn = spmv_sketch_pipe_kernel<RP, TPR, G>;
+  auto fn = spmv_sketch_pipe_kernel<RP, TPR, G, FMT>;
+  const int cap = FMT ? A->ndiag * kTileRows : A->cap;
   // Pick the stage count. G stages feed the SpMV groups and one the sketch,
   // so (stages - G - 1) x resident blocks x stage bytes are in flight ahead
   // of them: take the configuration that keeps >= 64 KB per SM ahead (HBM
@@ -309,7 +376,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   static thread_local int64_t keys[4] = {-1, -1, -1, -1};
   static thread_local int bests[4][2];
   static thread_local int next_slot = 0;
-  const int64_t key = (int64_t(A->cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP);
+  const int64_t key = (int64_t(cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP) ^ (FMT << 4);
   int slot = -1;
   for (int i = 0; i < 4; ++i)
     if (keys[i] == key) slot = i;
@@ -318,11 +385,11 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
     best_s = 0;
     best_per = 0;
     int64_t best_ahead = -1;
-    const int64_t stride = int64_t(stage_layout(int(sizeof(RP)), A->cap, off_stride,
-                                                int(S->zeta)).stride);
+    const int64_t stride = int64_t(stage_layout(int(sizeof(RP)), cap, off_stride,
+                                                int(S->zeta), FMT).stride);
     for (int s = G + 2; s <= kStages; ++s) {
       if (env_stages() && s != env_stages()) continue;
-      const size_t sm = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta), s);
+      const size_t sm = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), s, FMT);
       if (sm > 220 * 1024) continue;
       RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
       int per = 0;
@@ -344,14 +411,15 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   }
   if (best_s == 0) return false;
   const int stages = best_s, per_sm = best_per;
-  const size_t smem = pipe_smem<RP>(A->cap, int(S->d), off_stride, int(S->zeta), stages);
+  const size_t smem = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), stages, FMT);
   RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
   launch_maybe_pdl(fn, dim3(grid), dim3(kThreads), smem, st, A->n_rows,
-                   static_cast<const RP*>(A->row_ptr), A->col, A->val, x, xscale_dev, z, tiles,
-                   A->cap, int(S->d), int(S->zeta), off_stride, S->tile_off, S->tile_ent,
-                   S->scale, pacc, stop, step, stages, env_l2_hints(), env_debug());
+                   static_cast<const RP*>(A->row_ptr), A->col, FMT ? A->dval : A->val, x,
+                   xscale_dev, z, tiles, cap, int(S->d), int(S->zeta), off_stride, S->tile_off,
+                   S->tile_ent, S->scale, pacc, stop, step, stages, env_l2_hints(), env_debug(),
+                   A->doff, A->ndiag, A->n_cols);
   return true;
 }
 
@@ -430,6 +498,17 @@ bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double*
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z, double* pacc,
                              const int32_t* stop_flag, int step, cudaStream_t st) {
+  if (A->ndiag > 0 && A->dval) {
+    // diagonal copy: one SpMV thread per row; two groups once rows are long
+    // (RKMF_DIA_G=1|2 overrides)
+    static const int gdia = [] { const char* e = getenv("RKMF_DIA_G"); return e ? atoi(e) : 0; }();
+    static const int pf = [] { const char* e = getenv("RKMF_DIA_PREFETCH"); return e ? atoi(e) : 1; }();
+    if (pf && A->ndiag <= 8)
+      return launch_pipe_t<int32_t, 1, 1, 2>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
+    if (gdia == 1 || (gdia != 2 && A->ndiag <= 10))
+      return launch_pipe_t<int32_t, 1, 1, 1>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
+    return launch_pipe_t<int32_t, 1, 2, 1>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
+  }
   if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
   return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
                  : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);

@@ -66,6 +66,73 @@ def test_spmv_and_sketch(rk, oracle, torch, name, N):
     assert A.norm1 == pytest.approx(oracle.norm1((P.row_ptr, P.col_idx, P.values)), rel=1e-13)
 
 
+# diagonal copy (dia.cu): the fused kernel streaming [tile][diag][128] values
+# must give exactly the CSR kernel's z and sketch, ragged tails included
+@pytest.mark.parametrize("name,N,nd", [("cfg1", 256, 5), ("cfg2", 41, 7), ("cfg4", 23, 7),
+                                       ("cfg3", 13, 27)])
+def test_dia_bitexact_vs_csr(rk, oracle, torch, name, N, nd):
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    assert A.ndiag == nd
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    x = P.b
+    z1, p1 = rk.spmv_sketch(A, S, x)
+    assert A.set_diagonal_copy(False) == 0
+    z0, p0 = rk.spmv_sketch(A, S, x)
+    # z bit-identical where the CSR kernel also sums each row sequentially
+    # (one thread per row, rows <= 10 long); the 27-point CSR kernel splits
+    # rows over 2 threads. The sketch's cross-block sums follow the grid,
+    # which differs between the two streams (rounding only).
+    if nd <= 10:
+        assert torch.equal(z1, z0)
+    assert rel(z1, z0) <= 1e-15 and rel(p1, p0) <= 1e-14
+    zo = oracle.spmv((P.row_ptr, P.col_idx, P.values), x)
+    assert rel(z1, zo) <= 1e-14
+    assert A.set_diagonal_copy(True) == nd
+
+
+def test_dia_eligibility(rk, torch):
+    rng = np.random.default_rng(5)
+    # scattered nonzeros: CSR only
+    assert rk.SparseMatrix.from_scipy(H.random_sparse(2000, 0.01, 3)).ndiag == 0
+    # 33 diagonals: more than the kernel's 32
+    offs = list(range(-16, 17))
+    A = sp.diags([rng.standard_normal(3000 - abs(o)) for o in offs], offs, format="csr")
+    assert rk.SparseMatrix.from_scipy(A).ndiag == 0
+    # tridiagonal with a ragged last tile and one explicit zero kept
+    n = 1000
+    T = sp.diags([rng.standard_normal(n - 1), 2 + rng.random(n), rng.standard_normal(n - 1)],
+                 [-1, 0, 1], format="csr")
+    T.data[5] = 0.0
+    M = rk.SparseMatrix.from_scipy(T)
+    assert M.ndiag == 3
+    x = rng.standard_normal(n)
+    S = rk.make_sketch(16, n, 4, 2)
+    z1, p1 = rk.spmv_sketch(M, S, x)
+    M.set_diagonal_copy(False)
+    z0, p0 = rk.spmv_sketch(M, S, x)
+    assert torch.equal(z1, z0) and rel(p1, p0) <= 1e-14
+    assert rel(z1, T @ x) <= 1e-14
+
+
+def test_dia_solve_identical(rk, torch):
+    """A whole restarted solve agrees to rounding with and without the copy."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build("cfg2", 30)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    assert A.ndiag == 7
+    S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED)
+    f = rk.FunctionSpec.exp_neg(P.t)
+    opts = rk.RestartOptions(m_r=20, tol=P.tol, k_max=P.k_max)
+    b = torch.tensor(P.b, device="cuda")
+    r1 = rk.restarted_krylov(A, b, f, opts, S)
+    A.set_diagonal_copy(False)
+    r0 = rk.restarted_krylov(A, b, f, opts, S)
+    assert r1.cycles == r0.cycles and r1.cycles >= 2
+    assert rel(r1.f_hat, r0.f_hat) <= 1e-12
+
+
 def test_spmv_irregular_rows(rk, oracle, torch):
     # long rows exercise the chunked CSR-stream path; empty rows too
     rng = np.random.default_rng(3)
