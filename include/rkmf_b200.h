@@ -136,7 +136,7 @@ int rkmf_matrix_destroy(rkmf_matrix* A);
 int rkmf_matrix_info(const rkmf_matrix* A, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
                      double* norm1);
 /* Storage format of the SpMV stream (B200-specific, no reference counterpart).
- * A matrix whose nonzeros lie on at most 32 diagonals (stencils) also gets a
+ * A matrix whose nonzeros lie on at most 8 diagonals (stencils) also gets a
  * diagonal copy on creation, streamed by the fused SpMV + sketch instead of the
  * CSR arrays (8 bytes per slot, no indices; results bit-identical). enable = 0
  * drops the copy (CSR path only), 1 builds it if the matrix qualifies, 2

@@ -6,13 +6,15 @@
 // the BASELINE configs: 5/7/27-point Laplacians, Q1, convection-diffusion),
 // the same matrix is stored here as [tile][diag][128 rows] fp64 values with
 // the sorted offsets on the side: 8 bytes per stored slot and no indices, and
-// the x reads at row + offset are coalesced across a warp instead of gathers.
+// the x reads at row + offset are coalesced across a warp instead of gathers
+// (and issued a tile ahead: they do not depend on the streamed values).
 // Slots where the CSR row has no entry hold 0.0, and each row's entries keep
 // the CSR's column order, so z = A x is bit-identical to the CSR kernel (a
 // padding term adds exactly 0.0).
 //
 // Eligibility (checked on device, one pass over the nonzeros): at most
-// kMaxDiag distinct offsets, columns strictly increasing within each row, and
+// kMaxDiag = 8 distinct offsets (27-point stencils stay on the CSR kernel,
+// which splits their rows over two threads and measured faster), columns strictly increasing within each row, and
 // the padded DIA stream smaller than 0.85x the CSR stream. Otherwise the matrix
 // keeps the CSR path only. RKMF_DIA=0 disables the copy at creation;
 // rkmf_matrix_dia() drops or (re)builds it.
@@ -30,7 +32,7 @@ namespace rkmf_b200 {
 
 namespace {
 
-constexpr int kSetSlots = 64;      // per-block offset set (shared memory)
+constexpr int kSetSlots = 32;      // per-block offset set (shared memory)
 constexpr int kGlobalSlots = 256;  // merged set (global memory)
 constexpr int32_t kEmpty = INT_MIN;
 

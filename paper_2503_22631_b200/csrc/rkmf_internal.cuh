@@ -110,7 +110,7 @@ struct CsrView {
   const int32_t* doff;
   int ndiag;
 };
-constexpr int kMaxDiag = 32;
+constexpr int kMaxDiag = 8;
 // Row-pointer tail padding (entries) and value/column padding (elements)
 // allocated by the engine so 16-byte-rounded bulk copies stay in bounds.
 constexpr int64_t kRpPad = 136;

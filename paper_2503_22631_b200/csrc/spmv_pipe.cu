@@ -37,7 +37,7 @@ struct StageLayout {
 };
 
 // FMT 0 (CSR): row pointers, up to cap values and columns (+ alignment slack);
-// FMT 1 (DIA): cap = ndiag * 128 values, no row pointers or columns.
+// FMT 2 (DIA): cap = ndiag * 128 values, no row pointers or columns.
 __host__ __device__ inline StageLayout stage_layout(int rp_bytes, int cap, int off_stride,
                                                     int zeta, int fmt) {
   auto r16 = [](uint32_t x) { return (x + 15u) & ~15u; };
@@ -83,9 +83,12 @@ constexpr int spmv_threads() { return G * kTileRows * TPR; }
 template <int TPR, int G>
 constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads + 32; }
 
-// FMT 1 streams a diagonal (DIA) copy of the matrix instead of the CSR arrays
-// (build_dia, dia.cu): val = [tile][diag][128] values, doff = the ndiag sorted
-// column offsets; x is read at row + doff[q] (coalesced across a warp).
+// FMT 2 streams a diagonal (DIA) copy of the matrix instead of the CSR arrays
+// (build_dia, dia.cu): val = [tile][diag][128] values, doff = the ndiag <= 8
+// sorted column offsets; x is read at row + doff[q] (coalesced across a warp)
+// one tile ahead of the stage it multiplies. (FMT 1 was the same without the
+// x prefetch; at 27 diagonals either DIA variant loses to the CSR kernel with
+// two threads per row, 875 vs 465 us on cfg3, so the copy is limited to 8.)
 // (a 4-blocks-per-SM register cap, 56 registers with spills, measured slower)
 template <typename RP, int TPR, int G, int FMT>
 __global__ void __launch_bounds__(block_threads<TPR, G>())
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
   const int rl = gt / TPR, part = gt % TPR;
   int it = g;
   int s = g % nstages;
-  // FMT 2 (at most 8 diagonals): the x reads of a tile do not depend on the
+  // FMT 2: the x reads of a tile do not depend on the
   // staged data, so each thread loads the next tile's x while this tile's
   // stage is still landing (one tile of x latency hidden per group)
   double xnext[FMT == 2 ? 8 : 1];
@@ -264,24 +267,6 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (q < ndiag) sum += vt[q * kTileRows] * xcur[q];
-      }
-      if (FMT == 1 && live) {
-        // the CSR row's entries in column order (a sequential sum like the
-        // reference's); padding slots hold 0.0, an exact no-op term
-        const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
-        for (int q0 = 0; q0 < ndiag; q0 += 8) {
-          double v[8], xv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int qq = min(q0 + q, ndiag - 1);
-            const int64_t c = row + doff_s[qq];
-            v[q] = vt[qq * kTileRows];
-            xv[q] = (c >= 0 && c < ncols) ? __ldg(x + c) : 0.0;
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (q0 + q < ndiag) sum += v[q] * xv[q];
-        }
       }
       for (int e = lo + part; e < hi; e += 8 * TPR) {
         double v[8], xv[8];
@@ -498,17 +483,8 @@ bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double*
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z, double* pacc,
                              const int32_t* stop_flag, int step, cudaStream_t st) {
-  if (A->ndiag > 0 && A->dval) {
-    // diagonal copy: one SpMV thread per row; two groups once rows are long
-    // (RKMF_DIA_G=1|2 overrides)
-    static const int gdia = [] { const char* e = getenv("RKMF_DIA_G"); return e ? atoi(e) : 0; }();
-    static const int pf = [] { const char* e = getenv("RKMF_DIA_PREFETCH"); return e ? atoi(e) : 1; }();
-    if (pf && A->ndiag <= 8)
-      return launch_pipe_t<int32_t, 1, 1, 2>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
-    if (gdia == 1 || (gdia != 2 && A->ndiag <= 10))
-      return launch_pipe_t<int32_t, 1, 1, 1>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
-    return launch_pipe_t<int32_t, 1, 2, 1>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
-  }
+  if (A->ndiag > 0 && A->dval)  // diagonal copy (at most 8 diagonals), x prefetched
+    return launch_pipe_t<int32_t, 1, 1, 2>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
   if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
   return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
                  : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
