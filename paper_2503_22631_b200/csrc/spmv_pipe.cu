@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
         ph ^= 1u;
       }
     }
-    for (int b = u; b < d; b += kSketchThreads) atomicAdd(pacc + b, acc[b]);
+    if (!(debug & 8))
+      for (int b = u; b < d; b += kSketchThreads) atomicAdd(pacc + b, acc[b]);
     return;
   }
 
@@ -314,7 +315,7 @@ int env_l2_hints() {
   return v;
 }
 
-int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather, 4 stream only)
+int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather, 4 no SpMV, 8 no pacc flush)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("RKMF_PIPE_DEBUG");
