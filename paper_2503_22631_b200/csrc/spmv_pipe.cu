@@ -90,7 +90,7 @@ constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads +
 // x prefetch; at 27 diagonals either DIA variant loses to the CSR kernel with
 // two threads per row, 875 vs 465 us on cfg3, so the copy is limited to 8.)
 // (a 4-blocks-per-SM register cap, 56 registers with spills, measured slower)
-template <typename RP, int TPR, int G, int FMT>
+template <typename RP, int TPR, int G, int FMT, int ND = 1>
 __global__ void __launch_bounds__(block_threads<TPR, G>())
     spmv_sketch_pipe_kernel(int64_t n, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ val, const double* __restrict__ x,
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
                             double sscale, double* pacc, const int32_t* stop, int step,
                             int nstages, int l2_hints, int debug, const int32_t* __restrict__ doff,
-                            int ndiag, int64_t ncols) {
+                            int ndiag, int64_t ncols, int sync_mode) {
   constexpr int kSpmv = spmv_threads<TPR, G>();
   constexpr int kGroup = kTileRows * TPR;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&zsr[s], kGroup);
-      mbar_init(&empty[s], kSketchThreads);
+      mbar_init(&empty[s], (sync_mode & 1) ? 1 : kSketchThreads);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -193,8 +193,14 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     int s = 0;
     uint32_t ph = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      mbar_wait(&zsr[s], ph);
-      mbar_wait(&full[s], ph);  // completed already (the SpMV group waited on it)
+      if (sync_mode & 1) {
+        // named barrier 8 + s (the SpMV group bar.arrives on it): a hardware
+        // barrier, so the waiting sketch warps take no issue slots
+        asm volatile("bar.sync %0, %1;" ::"r"(8 + s), "n"(kGroup + kSketchThreads) : "memory");
+      } else {
+        mbar_wait(&zsr[s], ph);
+        mbar_wait(&full[s], ph);  // completed already (the SpMV group waited on it)
+      }
       unsigned char* st = smem + s * L.stride;
       if (!(debug & 1))
         sketch_tile_gather<kSketchThreads>(u, d, reinterpret_cast<const uint16_t*>(st + L.off),
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       // orders this tile's acc updates before the next tile's (slot -> bin
       // ownership changes per tile)
       asm volatile("bar.sync 2, %0;" ::"n"(kSketchThreads) : "memory");
-      mbar_arrive(&empty[s]);
+      if (!(sync_mode & 1) || u == 0) mbar_arrive(&empty[s]);
       if (++s == nstages) {
         s = 0;
         ph ^= 1u;
@@ -223,31 +229,84 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
   const double xs = xscale ? *xscale : 1.0;
   const int g = t / kGroup, gt = t % kGroup;
   const int rl = gt / TPR, part = gt % TPR;
-  int it = g;
-  int s = g % nstages;
-  // FMT 2: the x reads of a tile do not depend on the
-  // staged data, so each thread loads the next tile's x while this tile's
-  // stage is still landing (one tile of x latency hidden per group)
-  double xnext[FMT == 2 ? 8 : 1];
-  auto load_x = [&](int64_t tl, double* dst) {
-    const int64_t row = tl * kTileRows + rl;
-#pragma unroll
-    for (int q = 0; q < (FMT == 2 ? 8 : 1); ++q) {
-      const int64_t c = row + doff_s[min(q, ndiag - 1)];
-      dst[q] = (row < n && q < ndiag && c >= 0 && c < ncols) ? __ldg(x + c) : 0.0;
+  // stage s and its full-barrier parity advance incrementally (G < nstages)
+  int s = g;
+  uint32_t ph = 0;
+  auto advance = [&] {
+    s += G;
+    if (s >= nstages) {
+      s -= nstages;
+      ph ^= 1u;
     }
   };
-  if (FMT == 2 && blockIdx.x + int64_t(g) * gridDim.x < num_tiles)
-    load_x(blockIdx.x + int64_t(g) * gridDim.x, xnext);
-  for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
-       tile += int64_t(G) * gridDim.x, it += G) {
-    double xcur[FMT == 2 ? 8 : 1];
-    if (FMT == 2) {
+  auto handoff = [&] {  // z table of stage s complete -> the sketch threads
+    if (sync_mode & 1)
+      asm volatile("bar.arrive %0, %1;" ::"r"(8 + s), "n"(kGroup + kSketchThreads) : "memory");
+    else
+      mbar_arrive(&zsr[s]);
+  };
+  if constexpr (FMT == 2) {
+    // Diagonal copy, ND diagonals: x is read at row + offset. Those reads do
+    // not depend on the staged values, so each thread loads the next tile's x
+    // (into the other register buffer) before waiting for this tile's stage.
+    // Interior tiles (every offset in range) skip the bounds checks.
+    int doffr[ND];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) xcur[q] = xnext[q];
-      if (tile + int64_t(G) * gridDim.x < num_tiles) load_x(tile + int64_t(G) * gridDim.x, xnext);
+    for (int q = 0; q < ND; ++q) doffr[q] = doff_s[q];
+    auto load_x = [&](int64_t tl, double* dst) {
+      const int64_t r0 = tl * kTileRows, row = r0 + rl;
+      if (r0 + doffr[0] >= 0 && r0 + kTileRows - 1 + doffr[ND - 1] < ncols && r0 + kTileRows <= n) {
+        const double* xr = x + row;
+#pragma unroll
+        for (int q = 0; q < ND; ++q) dst[q] = __ldg(xr + doffr[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < ND; ++q) {
+          const int64_t c = row + doffr[q];
+          dst[q] = (row < n && c >= 0 && c < ncols) ? __ldg(x + c) : 0.0;
+        }
+      }
+    };
+    auto step = [&](int64_t tile, const double* xc, double* xn) {
+      const int64_t nt = tile + int64_t(G) * gridDim.x;
+      if (nt < num_tiles) load_x(nt, xn);
+      mbar_wait(&full[s], ph);
+      unsigned char* st = smem + s * L.stride;
+      if (!(debug & 4)) {
+        const int64_t row = tile * kTileRows + rl;
+        const bool live = row < n;
+        const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < ND; ++q) sum += vt[q * kTileRows] * xc[q];
+        sum *= xs;
+        if (live && z) z[row] = sum;
+        const double zt = live ? sum * sscale : 0.0;
+        double* zs = reinterpret_cast<double*>(st + L.zs);
+        zs[rl] = zt;
+        zs[kTileRows + rl] = -zt;
+      }
+      handoff();
+      advance();
+    };
+    double xa[ND], xb[ND];
+    int64_t tile = blockIdx.x + int64_t(g) * gridDim.x;
+    if (tile < num_tiles) load_x(tile, xa);
+    for (; tile < num_tiles; tile += 2 * int64_t(G) * gridDim.x) {
+      step(tile, xa, xb);
+      const int64_t t2 = tile + int64_t(G) * gridDim.x;
+      if (t2 < num_tiles) step(t2, xb, xa);
     }
-    mbar_wait(&full[s], uint32_t(it / nstages) & 1u);
+    return;
+  } else {
+  // CSR: adjacent lanes of a row take its nonzeros round-robin and combine
+  // their partial sums with a fixed butterfly (deterministic). 8 gathers per
+  // thread are in flight before the first FMA; lanes past the row end re-read
+  // the row's last column (a valid index the row already uses) and contribute
+  // a zero product.
+  for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
+       tile += int64_t(G) * gridDim.x) {
+    mbar_wait(&full[s], ph);
     unsigned char* st = smem + s * L.stride;
     if (!(debug & 4)) {
       const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
@@ -258,17 +317,11 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       const int64_t row = tile * kTileRows + rl;
       const bool live = row < n;
       int lo = 0, hi = 0;
-      if (!FMT && live && rp) {
+      if (live && rp) {
         lo = int((long long)rps[rl] - meta.rs);
         hi = int((long long)rps[rl + 1] - meta.rs);
       }
-      double sum = (!FMT && !rp && live && part == 0) ? x[row] : 0.0;  // sketch-only: z = x
-      if (FMT == 2 && live) {
-        const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < ndiag) sum += vt[q * kTileRows] * xcur[q];
-      }
+      double sum = (!rp && live && part == 0) ? x[row] : 0.0;  // sketch-only: z = x
       for (int e = lo + part; e < hi; e += 8 * TPR) {
         double v[8], xv[8];
 #pragma unroll
@@ -290,9 +343,9 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
         zs[kTileRows + rl] = -zt;
       }
     }
-    mbar_arrive(&zsr[s]);
-    s += G;
-    while (s >= nstages) s -= nstages;
+    handoff();
+    advance();
+  }
   }
 }
 
@@ -324,6 +377,20 @@ int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather
   return v;
 }
 
+// RKMF_PIPE_SYNC bits: 1 (default) the SpMV -> sketch handoff on named
+// barriers 8 + s (bar.arrive / bar.sync: the sketch warps wait in hardware
+// instead of polling an mbarrier, which takes issue slots in this
+// issue-bound kernel) and one empty arrival per tile; 0 = mbarriers;
+// 2 = also one warp per SpMV group polls the TMA barrier (slower)
+int env_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_PIPE_SYNC");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 int env_stages() {
   static int v = -1;
   if (v < 0) {
@@ -345,13 +412,13 @@ int sms() {
   return v;
 }
 
-template <typename RP, int TPR, int G, int FMT = 0>
+template <typename RP, int TPR, int G, int FMT = 0, int ND = 1>
 bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
                    int step, cudaStream_t st) {
   constexpr int kThreads = block_threads<TPR, G>();
   const int off_stride = int(tile_off_stride(S->d));
-  auto fn = spmv_sketch_pipe_kernel<RP, TPR, G, FMT>;
+  auto fn = spmv_sketch_pipe_kernel<RP, TPR, G, FMT, ND>;
   const int cap = FMT ? A->ndiag * kTileRows : A->cap;
   // Pick the stage count. G stages feed the SpMV groups and one the sketch,
   // so (stages - G - 1) x resident blocks x stage bytes are in flight ahead
@@ -362,7 +429,8 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   static thread_local int64_t keys[4] = {-1, -1, -1, -1};
   static thread_local int bests[4][2];
   static thread_local int next_slot = 0;
-  const int64_t key = (int64_t(cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP) ^ (FMT << 4);
+  const int64_t key = (int64_t(cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP) ^
+                      (FMT << 4) ^ (int64_t(ND) << 32);
   int slot = -1;
   for (int i = 0; i < 4; ++i)
     if (keys[i] == key) slot = i;
@@ -405,7 +473,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    static_cast<const RP*>(A->row_ptr), A->col, FMT ? A->dval : A->val, x,
                    xscale_dev, z, tiles, cap, int(S->d), int(S->zeta), off_stride, S->tile_off,
                    S->tile_ent, S->scale, pacc, stop, step, stages, env_l2_hints(), env_debug(),
-                   A->doff, A->ndiag, A->n_cols);
+                   A->doff, A->ndiag, A->n_cols, env_sync());
   return true;
 }
 
@@ -484,8 +552,16 @@ bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double*
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z, double* pacc,
                              const int32_t* stop_flag, int step, cudaStream_t st) {
-  if (A->ndiag > 0 && A->dval)  // diagonal copy (at most 8 diagonals), x prefetched
-    return launch_pipe_t<int32_t, 1, 1, 2>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
+  if (A->ndiag > 0 && A->dval) {  // diagonal copy (at most 8 diagonals), x prefetched
+#define RKMF_DIA(NDV) \
+  case NDV: return launch_pipe_t<int32_t, 1, 1, 2, NDV>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
+    switch (A->ndiag) {
+      RKMF_DIA(1); RKMF_DIA(2); RKMF_DIA(3); RKMF_DIA(4);
+      RKMF_DIA(5); RKMF_DIA(6); RKMF_DIA(7); RKMF_DIA(8);
+      default: break;
+    }
+#undef RKMF_DIA
+  }
   if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
   return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
                  : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
