@@ -312,7 +312,19 @@ template <int UNR, int LD>
 __global__ void __launch_bounds__(kUpdThreads)
     basis_update_kernel(int64_t n, int k, int64_t ldw, double* W, const double* __restrict__ z,
                         const double* __restrict__ Rbar, int64_t ldr, const SolveState* st,
-                        int rev) {
+                        int rev, int pf) {
+  // PDL prologue: W[:,0..k] and z are final before K3 runs (only r comes
+  // from it), so while K3 computes on one SM the resident blocks pull their
+  // first rows of every column into L2 (one prefetch per 128-byte line).
+  if (pf && (threadIdx.x & 7) == 0 && blockIdx.x < unsigned(pf) * 148u) {
+    const int64_t i2 = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x;
+    const int64_t j2 = rev ? n / 2 - 1 - i2 : i2;
+    if (j2 >= 0 && j2 < n / 2) {
+      for (int c = 0; c <= k; ++c)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(W + int64_t(c) * ldw + 2 * j2));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(z + 2 * j2));
+    }
+  }
   pdl_wait_then_trigger();
   if (st->stopped <= k) return;  // no update at (or after) a breakdown step
   __shared__ double coef[kMaxCoef];
@@ -523,9 +535,10 @@ void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double*
   static const int ldm = [] { const char* e = getenv("RKMF_K4_LOAD"); return e ? atoi(e) : 2; }();
   static const int order = [] { const char* e = getenv("RKMF_K4_ORDER"); return e ? atoi(e) : 0; }();
   const int rev = order == 1 ? (k & 1) : (order == 2 ? 1 : 0);
+  static const int pf = [] { const char* e = getenv("RKMF_K4_PREFETCH"); return e ? atoi(e) : 1; }();
 #define RKMF_K4(U, L)                                                                       \
   launch_maybe_pdl(basis_update_kernel<U, L>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, \
-                   W, z, Rbar, ldr, st_dev, rev)
+                   W, z, Rbar, ldr, st_dev, rev, pf)
   if (unr == 8) {
     RKMF_K4(8, 2);
   } else if (unr == 2) {

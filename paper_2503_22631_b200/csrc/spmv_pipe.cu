@@ -120,11 +120,31 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
   }
   for (int b = t; b < d; b += block_threads<TPR, G>()) acc[b] = 0.0;
   __syncthreads();
-  pdl_wait_then_trigger();  // x, pacc and the stop flag come from earlier kernels
-  if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
+  // The matrix and the sketch layout are constant, so the producer fills the
+  // first nstages stages before waiting on the previous kernel (PDL: that
+  // overlaps the basis update's tail); x, pacc and the stop flag come from
+  // earlier kernels, so every other thread waits first.
+  const bool producer = t == kSpmv + kSketchThreads;
+  if (!producer) {
+    pdl_wait_then_trigger();
+    if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
+  }
 
   if (t >= kSpmv + kSketchThreads) {  // ---------------- producer warp ----------------
-    if (t != kSpmv + kSketchThreads) return;
+    if (!producer) return;
+    bool waited = false;
+    // after the early stages: wait for the previous kernel; if this step is
+    // past a breakdown, let the issued copies land (the block's shared
+    // memory must not be released under them) and leave
+    auto wait_prev = [&](int issued) {
+      waited = true;
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (stop != nullptr && *stop <= step) {
+        for (int i = 0; i < issued; ++i) mbar_wait(&full[i], 0u);
+        return true;
+      }
+      return false;
+    };
     const uint64_t pol = l2_policy(l2_hints >= 1 ? 1 : 0);
     // the sketch tile layout is re-read every step: ask L2 to keep it
     const uint64_t mpol = l2_policy(l2_hints);
@@ -146,6 +166,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
         nrs = (long long)rp[nt * kTileRows];
         nre = (long long)rp[min(n, nt * kTileRows + kTileRows)];
       }
+      if (it == nstages && !waited && wait_prev(it)) return;
       if (it >= nstages) mbar_wait(&empty[s], eph);
       unsigned char* st = smem + s * L.stride;
       const int64_t r0 = tile * kTileRows;
@@ -185,6 +206,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
         if (it >= nstages) eph ^= 1u;  // rounds 1, 2, ... of each stage
       }
     }
+    if (!waited) wait_prev(it);
     return;
   }
 
