@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, FMT);
   __shared__ __align__(8) uint64_t full[kStages], zsr[kStages], empty[kStages];
   __shared__ int32_t doff_s[FMT ? kMaxDiag : 1];
-  if (FMT)
-    for (int q = threadIdx.x; q < ndiag; q += blockDim.x) doff_s[q] = doff[q];
+  if (FMT)  // doff == nullptr: the identity (sketch of x alone)
+    for (int q = threadIdx.x; q < ndiag; q += blockDim.x) doff_s[q] = doff ? doff[q] : 0;
   double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d], sketch threads
   const int t = threadIdx.x;
   if (t == 0) {
@@ -150,9 +150,8 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     const uint64_t mpol = l2_policy(l2_hints);
     // row-pointer pair of the next tile, prefetched one iteration ahead so the
     // bulk copies of a tile are issued without a dependent global round trip
-    // rp == nullptr: sketch of x only (the start vector), no matrix stream
     long long nrs = 0, nre = 0;
-    if (!FMT && rp && blockIdx.x < num_tiles) {
+    if (!FMT && blockIdx.x < num_tiles) {
       const int64_t r0 = int64_t(blockIdx.x) * kTileRows;
       nrs = (long long)rp[r0];
       nre = (long long)rp[min(n, r0 + kTileRows)];
@@ -162,7 +161,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const long long rs = nrs, re = nre;
       const int64_t nt = tile + gridDim.x;
-      if (!FMT && rp && nt < num_tiles) {
+      if (!FMT && nt < num_tiles) {
         nrs = (long long)rp[nt * kTileRows];
         nre = (long long)rp[min(n, nt * kTileRows + kTileRows)];
       }
@@ -173,13 +172,13 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       const long long vs0 = rs & ~1LL, cs0 = rs & ~3LL;
       const uint32_t vbytes = uint32_t(((re - vs0) * 8 + 15) & ~15LL);
       const uint32_t cbytes = uint32_t(((re - cs0) * 4 + 15) & ~15LL);
-      const uint32_t rbytes = !rp ? 0u : (sizeof(RP) == 4 ? 528u : 1040u);
+      const uint32_t rbytes = sizeof(RP) == 4 ? 528u : 1040u;
       const uint32_t obytes = uint32_t(off_stride) * 2u;
       const uint32_t ebytes = uint32_t(kTileRows * zeta);
       if (FMT) {  // one contiguous block of ndiag x 128 values
-        const uint32_t dbytes = uint32_t(cap) * 8u;
+        const uint32_t dbytes = val ? uint32_t(cap) * 8u : 0u;
         mbar_expect_tx(&full[s], dbytes + obytes + ebytes);
-        bulk_g2s(st + L.val, val + tile * int64_t(cap), dbytes, &full[s], pol);
+        if (val) bulk_g2s(st + L.val, val + tile * int64_t(cap), dbytes, &full[s], pol);
         bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], mpol);
         bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], mpol);
         if (++s == nstages) {
@@ -194,7 +193,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       meta->cshift = int(rs - cs0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&full[s], rbytes + (re > rs ? vbytes + cbytes : 0u) + obytes + ebytes);
-      if (rp) bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s], pol);
+      bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s], pol);
       if (re > rs) {
         bulk_g2s(st + L.val, val + vs0, vbytes, &full[s], pol);
         bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s], pol);
@@ -299,8 +298,12 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
         const bool live = row < n;
         const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
         double sum = 0.0;
+        if (val) {
 #pragma unroll
-        for (int q = 0; q < ND; ++q) sum += vt[q * kTileRows] * xc[q];
+          for (int q = 0; q < ND; ++q) sum += vt[q * kTileRows] * xc[q];
+        } else {  // identity: z = x
+          sum = xc[0];
+        }
         sum *= xs;
         if (live && z) z[row] = sum;
         const double zt = live ? sum * sscale : 0.0;
@@ -339,11 +342,11 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
       const int64_t row = tile * kTileRows + rl;
       const bool live = row < n;
       int lo = 0, hi = 0;
-      if (live && rp) {
+      if (live) {
         lo = int((long long)rps[rl] - meta.rs);
         hi = int((long long)rps[rl + 1] - meta.rs);
       }
-      double sum = (!rp && live && part == 0) ? x[row] : 0.0;  // sketch-only: z = x
+      double sum = 0.0;
       for (int e = lo + part; e < hi; e += 8 * TPR) {
         double v[8], xv[8];
 #pragma unroll
@@ -557,18 +560,13 @@ bool launch_pipe_rp(const CsrView* A, const SketchView* S, const double* x,
 // vector's S*start (basis.cpp:103-104), mode 2 of launch_spmv_sketch
 bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double* xscale_dev,
                              double* pacc, cudaStream_t st) {
+  // the diagonal path with one diagonal of ones: x staged by the same
+  // prefetching SpMV threads, no matrix stream
   CsrView v{};
   v.n_rows = S->n;
   v.n_cols = S->n;
-  v.nnz = 0;
-  v.row_ptr = nullptr;
-  v.rp64 = false;
-  v.col = nullptr;
-  v.val = nullptr;
-  v.cap = 8;
-  v.max_tile_nnz = 0;
-  v.padded = true;
-  return launch_pipe_t<int32_t, 1, 1>(&v, S, x, xscale_dev, nullptr, pacc, nullptr, 0, st);
+  v.ndiag = 1;
+  return launch_pipe_t<int32_t, 1, 1, 2, 1>(&v, S, x, xscale_dev, nullptr, pacc, nullptr, 0, st);
 }
 
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
