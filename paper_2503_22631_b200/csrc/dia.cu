@@ -5,7 +5,9 @@
 // one of a few diagonals (col - row in a small set — the stencil matrices of
 // the BASELINE configs: 5/7/27-point Laplacians, Q1, convection-diffusion),
 // the same matrix is stored here as [tile][diag][128 rows] fp64 values with
-// the sorted offsets on the side: 8 bytes per stored slot and no indices, and
+// each tile's sorted offsets on the side ([tile][8] int32; the offsets may
+// differ per tile, e.g. the halo columns of a row-partitioned slab sit on
+// their own diagonal): 8 bytes per stored slot and no indices, and
 // the x reads at row + offset are coalesced across a warp instead of gathers
 // (and issued a tile ahead: they do not depend on the streamed values).
 // Slots where the CSR row has no entry hold 0.0, and each row's entries keep
@@ -13,7 +15,7 @@
 // padding term adds exactly 0.0).
 //
 // Eligibility (checked on device, one pass over the nonzeros): at most
-// kMaxDiag = 8 distinct offsets (27-point stencils stay on the CSR kernel,
+// kMaxDiag = 8 distinct offsets per 128-row tile (27-point stencils stay on the CSR kernel,
 // which splits their rows over two threads and measured faster), columns strictly increasing within each row, and
 // the padded DIA stream smaller than 0.85x the CSR stream. Otherwise the matrix
 // keeps the CSR path only. RKMF_DIA=0 disables the copy at creation;
@@ -32,77 +34,75 @@ namespace rkmf_b200 {
 
 namespace {
 
-constexpr int kSetSlots = 32;      // per-block offset set (shared memory)
-constexpr int kGlobalSlots = 256;  // merged set (global memory)
 constexpr int32_t kEmpty = INT_MIN;
 
-__device__ __forceinline__ uint32_t hash_off(int32_t v) {
-  return (uint32_t(v) * 2654435761u) >> 8;
-}
-
-// Insert v into an open-addressed set of `slots` int32 keys; returns false
-// when the set is full.
-__device__ bool set_insert(int32_t* set, int slots, int32_t v) {
-  uint32_t h = hash_off(v) & uint32_t(slots - 1);
-  for (int probe = 0; probe < slots; ++probe) {
-    const int32_t cur = set[h];
-    if (cur == v) return true;
-    if (cur == kEmpty) {
-      const int32_t old = atomicCAS(set + h, kEmpty, v);
-      if (old == kEmpty || old == v) return true;
-    }
-    h = (h + 1) & uint32_t(slots - 1);
-  }
-  return false;
-}
-
-// flags[0]: a row's columns are not strictly increasing; flags[1]: more
-// distinct offsets than the sets hold. gset: the merged offsets.
+// One block (128 threads = the tile's rows) per tile: the distinct column
+// offsets of the tile's rows, sorted, into toff[tile][kMaxDiag] (slots past
+// the tile's count repeat its largest offset: a duplicate slot keeps 0.0
+// values and adds an exact zero). flags[0]: a row's columns are not strictly
+// increasing; flags[1]: a tile has more than kMaxDiag offsets; flags[2]: the
+// largest per-tile count.
 template <typename RP>
-__global__ void dia_offsets_kernel(int64_t n, const RP* __restrict__ rp,
-                                   const int32_t* __restrict__ ci, int32_t* gset, int32_t* flags) {
-  __shared__ int32_t set[kSetSlots];
-  __shared__ int bad;
-  for (int i = threadIdx.x; i < kSetSlots; i += blockDim.x) set[i] = kEmpty;
-  if (threadIdx.x == 0) bad = 0;
+__global__ void dia_tile_offsets_kernel(int64_t n, const RP* __restrict__ rp,
+                                        const int32_t* __restrict__ ci, int32_t* toff,
+                                        int32_t* flags) {
+  __shared__ int32_t set[kMaxDiag];
+  __shared__ int over;
+  const int64_t tile = blockIdx.x;
+  const int64_t row = tile * kTileRows + threadIdx.x;
+  if (threadIdx.x < kMaxDiag) set[threadIdx.x] = kEmpty;
+  if (threadIdx.x == 0) over = 0;
   __syncthreads();
-  for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < n;
-       row += int64_t(gridDim.x) * blockDim.x) {
-    if (bad) break;  // racy read is fine: only an early exit
+  if (row < n) {
     const int64_t lo = int64_t(rp[row]), hi = int64_t(rp[row + 1]);
     int32_t prev = -1;
     for (int64_t e = lo; e < hi; ++e) {
       const int32_t c = ci[e];
-      if (c <= prev) {
-        atomicExch(flags + 0, 1);
-        bad = 1;
-        break;
-      }
+      if (c <= prev) atomicExch(flags + 0, 1);
       prev = c;
-      if (!set_insert(set, kSetSlots, int32_t(int64_t(c) - row))) {
-        atomicExch(flags + 1, 1);
-        bad = 1;
-        break;
+      const int32_t o = int32_t(int64_t(c) - row);
+      bool done = false;
+      for (int q = 0; q < kMaxDiag && !done; ++q) {
+        const int32_t cur = set[q];
+        if (cur == o) {
+          done = true;
+        } else if (cur == kEmpty) {
+          const int32_t old = atomicCAS(set + q, kEmpty, o);
+          done = old == kEmpty || old == o;
+        }
       }
+      if (!done) over = 1;
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kSetSlots; i += blockDim.x)
-    if (set[i] != kEmpty && !set_insert(gset, kGlobalSlots, set[i])) atomicExch(flags + 1, 1);
+  if (threadIdx.x == 0) {
+    if (over) atomicExch(flags + 1, 1);
+    int32_t v[kMaxDiag];
+    int cnt = 0;
+    for (int q = 0; q < kMaxDiag; ++q)
+      if (set[q] != kEmpty) v[cnt++] = set[q];
+    for (int a = 1; a < cnt; ++a) {  // insertion sort
+      const int32_t key = v[a];
+      int b = a - 1;
+      while (b >= 0 && v[b] > key) { v[b + 1] = v[b]; --b; }
+      v[b + 1] = key;
+    }
+    for (int q = 0; q < kMaxDiag; ++q) toff[tile * kMaxDiag + q] = cnt ? v[min(q, cnt - 1)] : 0;
+    atomicMax(flags + 2, cnt);
+  }
 }
 
-// dval[(tile * ndiag + q) * 128 + r] = A(row, row + doff[q]) (0.0 where absent)
+// dval[(tile * nd + q) * 128 + r] = A(row, row + toff[tile][q]) (0.0 where absent)
 template <typename RP>
 __global__ void dia_fill_kernel(int64_t n, const RP* __restrict__ rp,
                                 const int32_t* __restrict__ ci, const double* __restrict__ val,
-                                const int32_t* __restrict__ doff, int ndiag, double* dval) {
-  __shared__ int32_t offs[kMaxDiag];
-  for (int q = threadIdx.x; q < ndiag; q += blockDim.x) offs[q] = doff[q];
-  __syncthreads();
+                                const int32_t* __restrict__ toff, int64_t stride, int nd,
+                                double* dval) {
   for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < n;
        row += int64_t(gridDim.x) * blockDim.x) {
     const int64_t tile = row / kTileRows, r = row % kTileRows;
-    double* base = dval + tile * int64_t(ndiag) * kTileRows + r;
+    const int32_t* offs = toff + tile * stride;
+    double* base = dval + tile * int64_t(nd) * kTileRows + r;
     const int64_t lo = int64_t(rp[row]), hi = int64_t(rp[row + 1]);
     int q = 0;
     for (int64_t e = lo; e < hi; ++e) {  // columns increase, so offsets do too
@@ -114,14 +114,16 @@ __global__ void dia_fill_kernel(int64_t n, const RP* __restrict__ rp,
 }
 
 template <typename RP>
-void launch_offsets(const CsrView& v, int32_t* gset, int32_t* flags, cudaStream_t st) {
-  dia_offsets_kernel<RP><<<1184, 256, 0, st>>>(v.n_rows, static_cast<const RP*>(v.row_ptr), v.col,
-                                               gset, flags);
+void launch_offsets(const CsrView& v, int32_t* toff, int32_t* flags, cudaStream_t st) {
+  const int64_t tiles = (v.n_rows + kTileRows - 1) / kTileRows;
+  dia_tile_offsets_kernel<RP><<<unsigned(tiles), kTileRows, 0, st>>>(
+      v.n_rows, static_cast<const RP*>(v.row_ptr), v.col, toff, flags);
 }
 template <typename RP>
-void launch_fill(const CsrView& v, const int32_t* doff, int ndiag, double* dval, cudaStream_t st) {
+void launch_fill(const CsrView& v, const int32_t* toff, int64_t stride, int nd, double* dval,
+                 cudaStream_t st) {
   dia_fill_kernel<RP><<<1184, 256, 0, st>>>(v.n_rows, static_cast<const RP*>(v.row_ptr), v.col,
-                                            v.val, doff, ndiag, dval);
+                                            v.val, toff, stride, nd, dval);
 }
 
 }  // namespace
@@ -134,6 +136,7 @@ void drop_dia(rkmf_matrix* M) {
   M->view.dval = nullptr;
   M->view.doff = nullptr;
   M->view.ndiag = 0;
+  M->view.dstride = 0;
 }
 
 // Builds the diagonal copy when the matrix qualifies; leaves the CSR-only
@@ -142,55 +145,71 @@ void build_dia(rkmf_matrix* M) {
   drop_dia(M);
   const CsrView& v = M->view;
   if (v.n_rows == 0 || v.nnz == 0 || !v.row_ptr) return;
+  if (v.n_rows >= (int64_t(1) << 31) - kTileRows) return;
   rkmf_context* ctx = M->ctx;
   cudaStream_t st = ctx->stream;
-  char* scr = static_cast<char*>(ctx->scratch.ensure(sizeof(int32_t) * (kGlobalSlots + 4)));
-  int32_t* gset = reinterpret_cast<int32_t*>(scr);
-  int32_t* flags = gset + kGlobalSlots;
-  std::vector<int32_t> init(kGlobalSlots + 4, kEmpty);
-  init[kGlobalSlots] = init[kGlobalSlots + 1] = 0;
-  RKMF_CUDA(cudaMemcpyAsync(gset, init.data(), sizeof(int32_t) * init.size(),
-                            cudaMemcpyHostToDevice, st));
-  if (v.rp64) launch_offsets<int64_t>(v, gset, flags, st);
-  else launch_offsets<int32_t>(v, gset, flags, st);
+  const int64_t tiles = (v.n_rows + kTileRows - 1) / kTileRows;
+  // per-tile offsets first (small): [tiles][kMaxDiag]
+  if (cudaMalloc(&M->dia_off, sizeof(int32_t) * size_t(tiles) * kMaxDiag) != cudaSuccess) {
+    cudaGetLastError();
+    M->dia_off = nullptr;
+    return;
+  }
+  int32_t* flags = static_cast<int32_t*>(ctx->scratch.ensure(sizeof(int32_t) * 4));
+  RKMF_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 4, st));
+  if (v.rp64) launch_offsets<int64_t>(v, M->dia_off, flags, st);
+  else launch_offsets<int32_t>(v, M->dia_off, flags, st);
   RKMF_CUDA(cudaGetLastError());
   ctx->launches++;
-  std::vector<int32_t> h(kGlobalSlots + 4);
-  RKMF_CUDA(cudaMemcpyAsync(h.data(), gset, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost,
-                            st));
+  int32_t h[4];
+  RKMF_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st));
   RKMF_CUDA(cudaStreamSynchronize(st));
-  if (h[kGlobalSlots] || h[kGlobalSlots + 1]) return;
-  std::vector<int32_t> offs;
-  for (int i = 0; i < kGlobalSlots; ++i)
-    if (h[i] != kEmpty) offs.push_back(h[i]);
-  if (offs.empty() || int(offs.size()) > kMaxDiag) return;
-  std::sort(offs.begin(), offs.end());
-  const int ndiag = int(offs.size());
-  const int64_t tiles = (v.n_rows + kTileRows - 1) / kTileRows;
-  const double dia_bytes = 8.0 * double(ndiag) * double(tiles * kTileRows);
+  int nd = h[2];
+  auto fail = [&] { drop_dia(M); };
+  if (h[0] || h[1] || nd < 1 || nd > kMaxDiag) return fail();
+  // Usually every tile draws from one set of <= 8 offsets (a single-domain
+  // stencil): then store that union once (stride 0; the kernel keeps it in
+  // shared memory). Otherwise (the halo diagonals of a row slab) keep the
+  // per-tile lists (stride 8; read per tile, one tile ahead).
+  int64_t stride = kMaxDiag;
+  {
+    std::vector<int32_t> ht(size_t(tiles) * kMaxDiag);
+    RKMF_CUDA(cudaMemcpy(ht.data(), M->dia_off, sizeof(int32_t) * ht.size(),
+                         cudaMemcpyDeviceToHost));
+    std::vector<int32_t> uni(ht);
+    std::sort(uni.begin(), uni.end());
+    uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
+    if (int(uni.size()) <= kMaxDiag) {
+      nd = int(uni.size());
+      std::vector<int32_t> u8(kMaxDiag, uni.back());
+      std::copy(uni.begin(), uni.end(), u8.begin());
+      RKMF_CUDA(cudaMemcpy(M->dia_off, u8.data(), sizeof(int32_t) * kMaxDiag,
+                           cudaMemcpyHostToDevice));
+      stride = 0;
+    }
+  }
+  const double dia_bytes = 8.0 * double(nd) * double(tiles * kTileRows);
   const double csr_bytes = 12.0 * double(v.nnz) + (v.rp64 ? 8.0 : 4.0) * double(v.n_rows);
-  if (dia_bytes > 0.85 * csr_bytes) return;
+  if (dia_bytes > 0.85 * csr_bytes) return fail();
   size_t free_b = 0, total_b = 0;
   RKMF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  if (dia_bytes > 0.25 * double(free_b)) return;  // leave room for the basis
-  const size_t nval = size_t(ndiag) * size_t(tiles) * kTileRows;
+  if (dia_bytes > 0.25 * double(free_b)) return fail();  // leave room for the basis
+  const size_t nval = size_t(nd) * size_t(tiles) * kTileRows;
   if (cudaMalloc(&M->dia_val, sizeof(double) * nval) != cudaSuccess) {
     cudaGetLastError();
     M->dia_val = nullptr;
-    return;
+    return fail();
   }
-  RKMF_CUDA(cudaMalloc(&M->dia_off, sizeof(int32_t) * size_t(ndiag)));
-  RKMF_CUDA(cudaMemcpyAsync(M->dia_off, offs.data(), sizeof(int32_t) * size_t(ndiag),
-                            cudaMemcpyHostToDevice, st));
   RKMF_CUDA(cudaMemsetAsync(M->dia_val, 0, sizeof(double) * nval, st));
-  if (v.rp64) launch_fill<int64_t>(v, M->dia_off, ndiag, M->dia_val, st);
-  else launch_fill<int32_t>(v, M->dia_off, ndiag, M->dia_val, st);
+  if (v.rp64) launch_fill<int64_t>(v, M->dia_off, stride, nd, M->dia_val, st);
+  else launch_fill<int32_t>(v, M->dia_off, stride, nd, M->dia_val, st);
   RKMF_CUDA(cudaGetLastError());
   ctx->launches++;
   RKMF_CUDA(cudaStreamSynchronize(st));
   M->view.dval = M->dia_val;
   M->view.doff = M->dia_off;
-  M->view.ndiag = ndiag;
+  M->view.ndiag = nd;
+  M->view.dstride = int(stride);
 }
 
 bool dia_enabled_by_env() {

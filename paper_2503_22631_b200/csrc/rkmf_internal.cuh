@@ -107,8 +107,9 @@ struct CsrView {
   // optional diagonal copy (dia.cu): [tile][diag][128] values at the sorted
   // column offsets doff; ndiag == 0 when the matrix has none
   const double* dval;
-  const int32_t* doff;
+  const int32_t* doff;  // offsets: [8] for every tile (dstride 0) or [tile][8] (dstride 8)
   int ndiag;
+  int dstride;
 };
 constexpr int kMaxDiag = 8;
 // Row-pointer tail padding (entries) and value/column padding (elements)

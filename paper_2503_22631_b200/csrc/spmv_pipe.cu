@@ -84,8 +84,8 @@ template <int TPR, int G>
 constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads + 32; }
 
 // FMT 2 streams a diagonal (DIA) copy of the matrix instead of the CSR arrays
-// (build_dia, dia.cu): val = [tile][diag][128] values, doff = the ndiag <= 8
-// sorted column offsets; x is read at row + doff[q] (coalesced across a warp)
+// (build_dia, dia.cu): val = [tile][diag][128] values, doff = [tile][8] sorted
+// column offsets (ndiag <= 8 used); x is read at row + off (coalesced)
 // one tile ahead of the stage it multiplies. (FMT 1 was the same without the
 // x prefetch; at 27 diagonals either DIA variant loses to the CSR kernel with
 // two threads per row, 875 vs 465 us on cfg3, so the copy is limited to 8.)
@@ -99,15 +99,14 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
                             const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
                             double sscale, double* pacc, const int32_t* stop, int step,
                             int nstages, int l2_hints, int debug, const int32_t* __restrict__ doff,
-                            int ndiag, int64_t ncols, int sync_mode) {
+                            int ndiag, int64_t ncols, int sync_mode, int dstride) {
   constexpr int kSpmv = spmv_threads<TPR, G>();
   constexpr int kGroup = kTileRows * TPR;
   extern __shared__ __align__(128) unsigned char smem[];
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, FMT);
   __shared__ __align__(8) uint64_t full[kStages], zsr[kStages], empty[kStages];
-  __shared__ int32_t doff_s[FMT ? kMaxDiag : 1];
-  if (FMT)  // doff == nullptr: the identity (sketch of x alone)
-    for (int q = threadIdx.x; q < ndiag; q += blockDim.x) doff_s[q] = doff ? doff[q] : 0;
+  __shared__ int32_t doff_s[kMaxDiag];  // FMT 2 with one offset list (dstride 0)
+  if (FMT && threadIdx.x < kMaxDiag) doff_s[threadIdx.x] = doff ? doff[threadIdx.x] : 0;
   double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d], sketch threads
   const int t = threadIdx.x;
   if (t == 0) {
@@ -271,10 +270,24 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     // not depend on the staged values, so each thread loads the next tile's x
     // (into the other register buffer) before waiting for this tile's stage.
     // Interior tiles (every offset in range) skip the bounds checks.
-    int doffr[ND];
-#pragma unroll
-    for (int q = 0; q < ND; ++q) doffr[q] = doff_s[q];
     auto load_x = [&](int64_t tl, double* dst) {
+      // the sorted offsets: one list for all tiles (shared memory), or the
+      // tile's own ([tile][kMaxDiag], the same line in every thread);
+      // nullptr = the identity
+      int doffr[ND];
+      if (dstride == 0) {
+#pragma unroll
+        for (int q = 0; q < ND; ++q) doffr[q] = doff_s[q];
+      } else if (doff) {
+        const int4* p = reinterpret_cast<const int4*>(doff + tl * kMaxDiag);
+        const int4 a = __ldg(p), b = __ldg(p + 1);
+        const int all[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int q = 0; q < ND; ++q) doffr[q] = all[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < ND; ++q) doffr[q] = 0;
+      }
       const int64_t r0 = tl * kTileRows, row = r0 + rl;
       if (r0 + doffr[0] >= 0 && r0 + kTileRows - 1 + doffr[ND - 1] < ncols && r0 + kTileRows <= n) {
         const double* xr = x + row;
@@ -498,7 +511,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    static_cast<const RP*>(A->row_ptr), A->col, FMT ? A->dval : A->val, x,
                    xscale_dev, z, tiles, cap, int(S->d), int(S->zeta), off_stride, S->tile_off,
                    S->tile_ent, S->scale, pacc, stop, step, stages, env_l2_hints(), env_debug(),
-                   A->doff, A->ndiag, A->n_cols, env_sync());
+                   A->doff, A->ndiag, A->n_cols, env_sync(), A->dstride);
   return true;
 }
 

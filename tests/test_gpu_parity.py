@@ -115,6 +115,33 @@ def test_dia_eligibility(rk, torch):
     assert rel(z1, T @ x) <= 1e-14
 
 
+def test_dia_per_tile_offsets(rk, torch):
+    """Offsets that differ per 128-row tile (the halo columns of a row slab:
+    9 distinct diagonals overall, at most 8 in any tile) keep the copy."""
+    from paper_2503_22631_b200 import configs
+    N = 16
+    P = configs.build("cfg2", N)
+    n, plane = P.n, N * N
+    A = sp.csr_matrix((P.values, P.col_idx, P.row_ptr), shape=(n, n)).tolil()
+    A.resize((n, n + 2 * plane))
+    rng = np.random.default_rng(9)
+    for r in range(plane):  # lower halo plane: column n + r
+        A[r, n + r] = rng.standard_normal()
+    for r in range(n - plane, n):  # upper halo plane: column n + plane + (r - (n - plane))
+        A[r, n + plane + r - (n - plane)] = rng.standard_normal()
+    A = A.tocsr()
+    A.sort_indices()
+    M = rk.SparseMatrix.from_scipy(A)
+    assert M.ndiag == 7  # at most 6 stencil diagonals + the halo one in a boundary tile
+    x = rng.standard_normal(n + 2 * plane)
+    S = rk.make_sketch(32, n, 4, 3)
+    z1, p1 = rk.spmv_sketch(M, S, x)
+    M.set_diagonal_copy(False)
+    z0, p0 = rk.spmv_sketch(M, S, x)
+    assert torch.equal(z1, z0) and rel(p1, p0) <= 1e-14
+    assert rel(z1, A @ x) <= 1e-14
+
+
 def test_dia_solve_identical(rk, torch):
     """A whole restarted solve agrees to rounding with and without the copy."""
     from paper_2503_22631_b200 import configs
