@@ -193,7 +193,9 @@ def setup_single(args, ctx, dev):
     w.opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
     w.b_host = P.b
     w.b_dev = torch.tensor(P.b, device=dev)
-    w.config = dict(workload_desc(P, args.config), parallelism="single")
+    w.config = dict(workload_desc(P, args.config), parallelism="single",
+                    matrix_stream=(f"diagonal copy, {w.A.ndiag} diagonals (uploaded as CSR)"
+                                   if w.A.ndiag else "CSR"))
     return w
 
 
@@ -225,7 +227,9 @@ def setup_partitioned(args, ctx_device, world, rank, dev):
                 "l2_policy": "inputs larger than L2 (CSR + basis W exceed 126 MB)",
                 "parallelism": f"row-partitioned x{world} ({transport}: halo send/recv + "
                                f"sketch allreduce per Krylov step)",
-                "unit_note": "basis vectors counted per rank slab (value = world x m_k / s)"}
+                "unit_note": "basis vectors counted per rank slab (value = world x m_k / s)",
+                "matrix_stream": (f"diagonal copy, {part.A.ndiag} diagonals" if part.A.ndiag
+                                  else "CSR")}
     return w
 
 
