@@ -21,6 +21,8 @@
 // rule in u converges geometrically (poles at distance (pi-|arg z|)/2).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -102,6 +104,76 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       const int64_t r = row0 + tx + 16 * a, c = col0 + ty + 16 * b;
+      if (r < N && c < N) {
+        const int64_t o = c * N + r;
+        double v = acc[a][b];
+        if (r == c) v += c0;
+        if (P1) v += c1 * P1[o];
+        if (P2) v += c2 * P2[o];
+        if (P3) v += c3 * P3[o];
+        C[o] = v;
+      }
+    }
+}
+
+// The same product on 16 x 16 output tiles (64 threads, 2 x 2 outputs each):
+// the matrices here are small (N = number of Krylov vectors so far, 90-180 on
+// the BASELINE configs), so 32 x 32 tiles left most SMs idle (25 blocks at
+// N = 150, 15 us per product); 16 x 16 tiles give 100 blocks. The next K
+// tile is loaded into registers while the current one is used. Same
+// summation order per output (k ascending).
+constexpr int kT16 = 16, kK16 = 32;
+__global__ void __launch_bounds__(64)
+    dgemm16_epi_kernel(int64_t N, const double* __restrict__ A, const double* __restrict__ B,
+                       double* __restrict__ C, double c0, double c1, const double* __restrict__ P1,
+                       double c2, const double* __restrict__ P2, double c3,
+                       const double* __restrict__ P3) {
+  __shared__ double As[kT16][kK16 + 1];  // [row][k]
+  __shared__ double Bs[kK16][kT16 + 1];  // [k][col]
+  const int t = threadIdx.x, tx = t & 7, ty = t >> 3;  // 8 x 8 threads
+  const int64_t row0 = int64_t(blockIdx.x) * kT16, col0 = int64_t(blockIdx.y) * kT16;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  pdl_wait_then_trigger();  // the operands come from the previous product
+  // per K tile each thread loads 8 A and 8 B elements (16 x 32 each)
+  double ra[8], rb[8];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = t + 64 * j;             // 0..511
+      const int r = e & 15, c = e >> 4;     // A tile: row r (fast), k c
+      const int64_t gr = row0 + r, gk = k0 + c;
+      ra[j] = (gr < N && gk < N) ? A[gk * N + gr] : 0.0;
+      const int bk = e & 31, bc = e >> 5;   // B tile: k bk (fast), col bc
+      const int64_t gbk = k0 + bk, gbc = col0 + bc;
+      rb[j] = (gbk < N && gbc < N) ? B[gbc * N + gbk] : 0.0;
+    }
+  };
+  load(0);
+  for (int64_t k0 = 0; k0 < N; k0 += kK16) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = t + 64 * j;
+      As[e & 15][e >> 4] = ra[j];
+      Bs[e & 31][e >> 5] = rb[j];
+    }
+    __syncthreads();
+    if (k0 + kK16 < N) load(k0 + kK16);
+#pragma unroll 8
+    for (int kk = 0; kk < kK16; ++kk) {
+      const double a0 = As[tx][kk], a1 = As[tx + 8][kk];
+      const double b0 = Bs[kk][ty], b1 = Bs[kk][ty + 8];
+      acc[0][0] += a0 * b0;
+      acc[1][0] += a1 * b0;
+      acc[0][1] += a0 * b1;
+      acc[1][1] += a1 * b1;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int64_t r = row0 + tx + 8 * a, c = col0 + ty + 8 * b;
       if (r < N && c < N) {
         const int64_t o = c * N + r;
         double v = acc[a][b];
@@ -402,9 +474,15 @@ void dense_expneg_e1(const double* R, int64_t ldr, int64_t N, double t, int s, d
   const dim3 gg(unsigned((N + kT - 1) / kT), unsigned((N + kT - 1) / kT));
   const double scale = -t * std::ldexp(1.0, -s);
   dense_scale_kernel<<<grid_for(NN), 256, 0, st>>>(R, ldr, N, scale, A);
+  static const int g16 = [] { const char* e = getenv("RKMF_DGEMM16"); return e ? atoi(e) : 1; }();
+  const dim3 g16g(unsigned((N + kT16 - 1) / kT16), unsigned((N + kT16 - 1) / kT16));
   auto gemm = [&](const double* X, const double* Y, double* Z, double e0, double e1,
                   const double* P1, double e2, const double* P2, double e3, const double* P3) {
-    dgemm_epi_kernel<<<gg, 256, 0, st>>>(N, X, Y, Z, e0, e1, P1, e2, P2, e3, P3);
+    if (g16)
+      launch_maybe_pdl(dgemm16_epi_kernel, g16g, dim3(64), 0, st, N, X, Y, Z, e0, e1, P1, e2, P2,
+                       e3, P3);
+    else
+      dgemm_epi_kernel<<<gg, 256, 0, st>>>(N, X, Y, Z, e0, e1, P1, e2, P2, e3, P3);
     ++*launches;
   };
   gemm(A, A, A2, 0, 0, nullptr, 0, nullptr, 0, nullptr);
