@@ -411,6 +411,34 @@ int rkmf_context_kernel_times(rkmf_context* ctx, double* ms, int64_t* launches, 
   });
 }
 
+// Developer diagnostic (not in the public header; tools/trace_steps.py):
+// enable != 0 (re)arms the per-step device timeline of K2/K3/K4 (zeroed),
+// enable == 0 copies it out (steps x kTraceSlots stamps) and disarms it.
+int rkmf_debug_trace(rkmf_context* ctx, int enable, uint64_t* h_out, int64_t steps) {
+  static unsigned long long* buf = nullptr;
+  static int64_t cap = 0;
+  return guarded(ctx, [&] {
+    if (enable) {
+      if (steps > cap) {
+        if (buf) cudaFree(buf);
+        RKMF_CUDA(cudaMalloc(&buf, sizeof(unsigned long long) * steps * rkmf_b200::kTraceSlots));
+        cap = steps;
+      }
+      RKMF_CUDA(cudaMemset(buf, 0, sizeof(unsigned long long) * cap * rkmf_b200::kTraceSlots));
+      rkmf_b200::trace_bind_krylov(buf);
+      rkmf_b200::trace_bind_spmv_pipe(buf);
+    } else {
+      RKMF_CUDA(cudaDeviceSynchronize());
+      if (h_out && buf)
+        RKMF_CUDA(cudaMemcpy(h_out, buf,
+                             sizeof(unsigned long long) * std::min(steps, cap) * rkmf_b200::kTraceSlots,
+                             cudaMemcpyDeviceToHost));
+      rkmf_b200::trace_bind_krylov(nullptr);
+      rkmf_b200::trace_bind_spmv_pipe(nullptr);
+    }
+  });
+}
+
 void rkmf_restart_options_default(rkmf_restart_options* o) {  // restart.hpp:20-26
   o->m_r = 20;
   o->tol = 1e-10;

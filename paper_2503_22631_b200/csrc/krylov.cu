@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(kRgsThreads)
   // range, inside the allocations (engine.cu pads U; G holds (m+1)^2).
   const uint32_t ubytes = uint32_t(ucnt * 8);
   const uint32_t gbytes = uint32_t((int64_t(k) * (k - 1) / 2 + 1) / 2 * 2 * 8);
+  if (t == 0) trace_max(k, 2);
   if (t == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(kRgsThreads)
     if (k >= 2) bulk_g2s(Gs, G, gbytes, &bar);
   }
   pdl_wait_then_trigger();
+  if (t == 0) trace_max(k, 3);
   if (st->stopped <= k) return;
   for (int64_t b = t; b < d; b += kRgsThreads) {
     ps[b] = pacc[b];
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(kRgsThreads)
   }
   mbar_wait(&bar, 0);
   __syncthreads();
+  if (t == 0) trace_max(k, 4);
   // 2k+1 dots: task q < kk is c_q = <u_q, p>; task kk + j is G_kj = <u_k, u_j>
   const double* uk = Us + int64_t(k) * d;
   constexpr int kW = kRgsThreads / 32;
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(kRgsThreads)
     }
   }
   __syncthreads();
+  if (t == 0) trace_max(k, 5);
   if (w == 0) {  // unit lower-triangular solve (I + L) r = c, column by column
     if (kk <= 64) {  // c in registers (lanes l, l+32); r_i broadcast by shuffle
       const int m0 = l, m1 = l + 32;
@@ -263,6 +267,7 @@ __global__ void __launch_bounds__(kRgsThreads)
     }
   }
   __syncthreads();
+  if (t == 0) trace_max(k, 6);
   double ss = 0.0;
   for (int64_t b = t; b < d; b += kRgsThreads) {
     double v = ps[b];
@@ -287,6 +292,7 @@ __global__ void __launch_bounds__(kRgsThreads)
   }
   for (int64_t b = t; b < d; b += kRgsThreads) U[int64_t(k + 1) * d + b] = ps[b] / rkk;
   if (t == 0) Rbar[int64_t(k) * ldr + k + 1] = rkk;
+  if (t == 0) trace_max(k, 7);
 }
 
 constexpr int kUpdThreads = 256;
@@ -316,6 +322,7 @@ __global__ void __launch_bounds__(kUpdThreads)
   // PDL prologue: W[:,0..k] and z are final before K3 runs (only r comes
   // from it), so while K3 computes on one SM the resident blocks pull their
   // first rows of every column into L2 (one prefetch per 128-byte line).
+  if (threadIdx.x == 0) trace_first(k, 11);
   if (pf && (threadIdx.x & 7) == 0 && blockIdx.x < unsigned(pf) * 148u) {
     const int64_t i2 = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x;
     const int64_t j2 = rev ? n / 2 - 1 - i2 : i2;
@@ -326,6 +333,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     }
   }
   pdl_wait_then_trigger();
+  if (threadIdx.x == 0) trace_first(k, 8);
   if (st->stopped <= k) return;  // no update at (or after) a breakdown step
   __shared__ double coef[kMaxCoef];
   for (int c = threadIdx.x; c <= k; c += kUpdThreads)
@@ -368,6 +376,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     for (int c = 0; c <= k; ++c) a += W[int64_t(c) * ldw + i] * coef[c];
     out[i] = (z[i] - a) / rkk;
   }
+  if (threadIdx.x == 0) trace_max(k, 9);
 }
 
 // K5: the last basis update of the cycle fused with the restart update
@@ -469,6 +478,8 @@ int stream_grid(int64_t work, int threads) {
 }
 
 }  // namespace
+
+void trace_bind_krylov(unsigned long long* p) { trace_bind_tu(p); }
 
 void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev, bool first,
                          int m_eff, cudaStream_t st) {

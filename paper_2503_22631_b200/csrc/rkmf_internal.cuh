@@ -62,6 +62,30 @@ void launch_maybe_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
     throw Error(RKMF_DEVICE_ERROR, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 }
 
+// ---- optional device timeline of the step kernels (tools/trace_steps.py) ----
+// Per step k, kTraceSlots globaltimer stamps (ns), merged with atomicMax, so
+// a buffer armed before a solve holds its last cycle; "first" stamps are
+// taken by block 0 only. Off (null pointer) unless rkmf_debug_trace armed it;
+// the pointer is per translation unit (trace_bind_*).
+constexpr int kTraceSlots = 16;
+static __device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_max(int k, int slot) {
+  if (g_trace) atomicMax(g_trace + k * kTraceSlots + slot, gtime());
+}
+__device__ __forceinline__ void trace_first(int k, int slot) {
+  if (g_trace && blockIdx.x == 0) atomicMax(g_trace + k * kTraceSlots + slot, gtime());
+}
+static inline void trace_bind_tu(unsigned long long* p) {
+  cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+}
+void trace_bind_krylov(unsigned long long* p);
+void trace_bind_spmv_pipe(unsigned long long* p);
+
 // Tile geometry shared by the SpMV, sketch and update kernels: one tile is
 // kTileRows consecutive rows handled by one 128-thread block iteration.
 constexpr int kTileRows = 128;

@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
   // overlaps the basis update's tail); x, pacc and the stop flag come from
   // earlier kernels, so every other thread waits first.
   const bool producer = t == kSpmv + kSketchThreads;
+  if (t == 0 && stop) trace_first(step, 10);
   if (!producer) {
     pdl_wait_then_trigger();
+    if (t == 0 && stop) trace_first(step, 0);
     if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
   }
 
@@ -237,6 +239,7 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
     }
     if (!(debug & 8))
       for (int b = u; b < d; b += kSketchThreads) atomicAdd(pacc + b, acc[b]);
+    if (u == 0 && stop) trace_max(step, 1);
     return;
   }
 
@@ -568,6 +571,8 @@ bool launch_pipe_rp(const CsrView* A, const SketchView* S, const double* x,
 }
 
 }  // namespace
+
+void trace_bind_spmv_pipe(unsigned long long* p) { trace_bind_tu(p); }
 
 // sketch of x alone through the same pipeline (no matrix stream): the start
 // vector's S*start (basis.cpp:103-104), mode 2 of launch_spmv_sketch
