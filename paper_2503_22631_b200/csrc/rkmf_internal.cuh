@@ -74,11 +74,18 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Compiled in only with -DRKMF_TRACE (make trace: _lib/librkmf_b200_trace.so):
+// the product kernels carry no stamps (K2 and K4 are sensitive to code
+// generation; the stamps cost ~1.5% of the cfg2 solve).
 __device__ __forceinline__ void trace_max(int k, int slot) {
+#ifdef RKMF_TRACE
   if (g_trace) atomicMax(g_trace + k * kTraceSlots + slot, gtime());
+#endif
 }
 __device__ __forceinline__ void trace_first(int k, int slot) {
+#ifdef RKMF_TRACE
   if (g_trace && blockIdx.x == 0) atomicMax(g_trace + k * kTraceSlots + slot, gtime());
+#endif
 }
 static inline void trace_bind_tu(unsigned long long* p) {
   cudaMemcpyToSymbol(g_trace, &p, sizeof(p));

@@ -5,8 +5,9 @@
 Arms rkmf_debug_trace, runs one device-resident solve, and prints per step
 the phases (microseconds) of K2 (fused SpMV + sketch), K3 (sketched
 Gram-Schmidt) and K4 (basis update), from the stamps of the last cycle.
-The stamps add a few atomics per block; use for the breakdown, not for the
-bench number.
+The stamps are compiled only into the trace build of the library
+(`make -C paper_2503_22631_b200/csrc trace`), which this script selects; use
+it for the breakdown, not for the bench number.
 """
 import ctypes as C
 import os
@@ -15,6 +16,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+
+os.environ.setdefault("RKMF_LIB_PATH", os.path.join(
+    ROOT, "paper_2503_22631_b200", "_lib", "librkmf_b200_trace.so"))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
