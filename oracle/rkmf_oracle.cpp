@@ -175,15 +175,37 @@ void make_sketch(int64_t d, int64_t n, int64_t zeta, uint64_t seed, int64_t* row
 }
 
 // sketch_apply (vector): sketch.cpp:51-63 (column order, zero entries skipped)
-void sketch_apply(const Sketch& S, const double* x, double* y) {
-  std::fill(y, y + S.d, 0.0);
+void sketch_apply_range(const Sketch& S, const double* x, double* y, int64_t j0, int64_t j1) {
   const size_t z = size_t(S.zeta);
-  for (int64_t j = 0; j < S.n; ++j) {
+  for (int64_t j = j0; j < j1; ++j) {
     const double xj = S.scale * x[j];
     if (xj == 0.0) continue;
     const size_t base = size_t(j) * z;
     for (size_t k = 0; k < z; ++k) y[S.rows[base + k]] += S.signs[base + k] > 0 ? xj : -xj;
   }
+}
+
+// threads <= 1: the reference's column-sequential order exactly. threads > 1
+// (the CPU baseline only): contiguous column ranges into per-thread partial
+// sketches, summed in range order (deterministic; rounding differs from the
+// sequential order at the 1e-16 level).
+void sketch_apply(const Sketch& S, const double* x, double* y, int threads = 1) {
+  std::fill(y, y + S.d, 0.0);
+  if (threads <= 1 || S.n < 65536) {
+    sketch_apply_range(S, x, y, 0, S.n);
+    return;
+  }
+  std::vector<std::vector<double>> part(size_t(threads), std::vector<double>(size_t(S.d), 0.0));
+  std::vector<std::thread> pool;
+  const int64_t chunk = (S.n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    const int64_t lo = std::min<int64_t>(S.n, int64_t(t) * chunk);
+    const int64_t hi = std::min<int64_t>(S.n, lo + chunk);
+    pool.emplace_back([&, t, lo, hi] { sketch_apply_range(S, x, part[size_t(t)].data(), lo, hi); });
+  }
+  for (auto& th : pool) th.join();
+  for (int t = 0; t < threads; ++t)
+    for (int64_t i = 0; i < S.d; ++i) y[i] += part[size_t(t)][size_t(i)];
 }
 
 // ---- small dense helpers (column-major), replacing Eigen ----
@@ -442,7 +464,7 @@ Dec randomized_arnoldi(const Csr& A, const Sketch& S, const double* b, int64_t m
   if (S.d < need) param("randomized_arnoldi: sketch dimension d too small for m");
   const int64_t d = S.d;
   std::vector<double> sb(static_cast<size_t>(d));
-  sketch_apply(S, b, sb.data());
+  sketch_apply(S, b, sb.data(), threads);
   const double alpha = std::sqrt(dot(sb.data(), sb.data(), d));
   if (alpha == 0.0) param("randomized_arnoldi: zero start vector after sketching");
 
@@ -461,7 +483,7 @@ Dec randomized_arnoldi(const Csr& A, const Sketch& S, const double* b, int64_t m
   for (int64_t k = 0; k < m; ++k) {
     spmv(A, dec.W.data() + size_t(k) * size_t(n), z.data(), threads);
     dec.ctr.matvecs++;
-    sketch_apply(S, z.data(), p.data());
+    sketch_apply(S, z.data(), p.data(), threads);
     r.assign(size_t(k + 1), 0.0);
     for (int64_t i = 0; i <= k; ++i) {  // MGS in sketch space, basis.cpp:123-128
       const double* u = dec.U.data() + size_t(i) * size_t(d);
