@@ -19,6 +19,7 @@
 // bounds.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "rkmf_internal.cuh"
@@ -90,16 +91,19 @@ constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads +
 // x prefetch; at 27 diagonals either DIA variant loses to the CSR kernel with
 // two threads per row, 875 vs 465 us on cfg3, so the copy is limited to 8.)
 // (a 4-blocks-per-SM register cap, 56 registers with spills, measured slower)
-template <typename RP, int TPR, int G, int FMT, int ND = 1>
-__global__ void __launch_bounds__(block_threads<TPR, G>())
-    spmv_sketch_pipe_kernel(int64_t n, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
-                            const double* __restrict__ val, const double* __restrict__ x,
-                            const double* xscale, double* __restrict__ z, int64_t num_tiles,
-                            int cap, int d, int zeta, int off_stride,
-                            const uint16_t* __restrict__ toff, const uint8_t* __restrict__ tent,
-                            double sscale, double* pacc, const int32_t* stop, int step,
-                            int nstages, int l2_hints, int debug, const int32_t* __restrict__ doff,
-                            int ndiag, int64_t ncols, int sync_mode, int dstride) {
+#define RKMF_PIPE_PARAMS                                                                       \
+  int64_t n, const RP *__restrict__ rp, const int32_t *__restrict__ ci,                        \
+      const double *__restrict__ val, const double *__restrict__ x, const double *xscale,      \
+      double *__restrict__ z, int64_t num_tiles, int cap, int d, int zeta, int off_stride,     \
+      const uint16_t *__restrict__ toff, const uint8_t *__restrict__ tent, double sscale,      \
+      double *pacc, const int32_t *stop, int step, int nstages, int l2_hints, int debug,        \
+      const int32_t *__restrict__ doff, int ndiag, int64_t ncols, int sync_mode, int dstride
+#define RKMF_PIPE_ARGS                                                                       \
+  n, rp, ci, val, x, xscale, z, num_tiles, cap, d, zeta, off_stride, toff, tent, sscale, pacc, \
+      stop, step, nstages, l2_hints, debug, doff, ndiag, ncols, sync_mode, dstride
+
+template <typename RP, int TPR, int G, int FMT, int ND>
+__device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
   constexpr int kSpmv = spmv_threads<TPR, G>();
   constexpr int kGroup = kTileRows * TPR;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -390,6 +394,24 @@ __global__ void __launch_bounds__(block_threads<TPR, G>())
   }
 }
 
+// The diagonal kernel runs three or four 288-thread blocks per SM and is left
+// to ptxas's register heuristics (it is sensitive to code generation). The CSR
+// kernel runs one 544-672-thread block per SM (its stages fill shared
+// memory): its own bounds (min one block) let it keep a thread's eight x
+// gathers in flight; left to the heuristics, ptxas squeezed it to 40
+// registers for a second block that never fits and interleaved the gathers
+// with the FMA chain (cfg3 K2 502 vs 462 us).
+template <typename RP, int TPR, int G, int FMT, int ND = 1>
+__global__ void __launch_bounds__(block_threads<TPR, G>())
+    spmv_sketch_pipe_kernel(RKMF_PIPE_PARAMS) {
+  pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS);
+}
+template <typename RP, int TPR, int G, int FMT, int ND = 1>
+__global__ void __launch_bounds__(block_threads<TPR, G>(), 1)
+    spmv_sketch_pipe_csr_kernel(RKMF_PIPE_PARAMS) {
+  pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS);
+}
+
 template <typename RP>
 size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages, int fmt) {
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, fmt);
@@ -459,7 +481,10 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                    int step, cudaStream_t st) {
   constexpr int kThreads = block_threads<TPR, G>();
   const int off_stride = int(tile_off_stride(S->d));
-  auto fn = spmv_sketch_pipe_kernel<RP, TPR, G, FMT, ND>;
+  auto fn = [] {
+    if constexpr (FMT != 0) return spmv_sketch_pipe_kernel<RP, TPR, G, FMT, ND>;
+    else return spmv_sketch_pipe_csr_kernel<RP, TPR, G, FMT, ND>;
+  }();
   const int cap = FMT ? A->ndiag * kTileRows : A->cap;
   // Pick the stage count. G stages feed the SpMV groups and one the sketch,
   // so (stages - G - 1) x resident blocks x stage bytes are in flight ahead
@@ -498,6 +523,9 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
         best_s = s;
       }
     }
+    if (getenv("RKMF_PIPE_VERBOSE"))
+      fprintf(stderr, "[rkmf] K2 pipe RP=%d TPR=%d G=%d FMT=%d ND=%d: stages=%d blocks/SM=%d stride=%lld\n",
+              int(sizeof(RP)), TPR, G, FMT, ND, best_s, best_per, (long long)stride);
     slot = next_slot;
     next_slot = (next_slot + 1) & 3;
     keys[slot] = key;

@@ -48,6 +48,7 @@ for _ in range(reps):
     r = rk.restarted_krylov(A, b, f, opts, S)
 torch.cuda.synchronize()
 steps = P.m
+opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=int(os.environ.get("TRACE_KMAX", P.k_max)))
 assert L.rkmf_debug_trace(A.ctx.h, 1, None, steps) == 0
 r = rk.restarted_krylov(A, b, f, opts, S)
 out = np.zeros((steps, SLOTS), dtype=np.uint64)
