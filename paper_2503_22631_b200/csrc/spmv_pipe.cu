@@ -150,6 +150,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
       }
       return false;
     };
+    if ((debug & 16) && wait_prev(0)) return;  // ablation: no early stage fill
     const uint64_t pol = l2_policy(l2_hints >= 1 ? 1 : 0);
     // the sketch tile layout is re-read every step: ask L2 to keep it
     const uint64_t mpol = l2_policy(l2_hints);
@@ -431,7 +432,7 @@ int env_l2_hints() {
   return v;
 }
 
-int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather, 4 no SpMV, 8 no pacc flush)
+int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather, 4 no SpMV, 8 no pacc flush, 16 producer waits before filling)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("RKMF_PIPE_DEBUG");
