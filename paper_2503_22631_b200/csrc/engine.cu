@@ -29,6 +29,19 @@
 using namespace rkmf_b200;
 
 namespace rkmf_b200 {
+// RKMF_ROWSKETCH=1: build the coloured row-major sketch layout and run the
+// row-sketch K2 (spmv_rowsketch.cu). Off by default: at parity with the
+// warp-specialised K2 on cfg2 (39.9 vs 40.2 us b2b, 47.5 vs 47.3 us in the
+// solve) for 9 more bytes per row and a slower setup.
+bool rowsketch_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RKMF_ROWSKETCH");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 bool pdl_enabled() {  // RKMF_PDL=0 launches the step kernels without PDL
   static int v = -1;
   if (v < 0) {
@@ -594,6 +607,20 @@ int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_globa
       launch_sketch_generate(d, n, col_begin, zeta, seed, S->rows, S->signs, ctx->stream);
       launch_sketch_tiles(d, n, zeta, S->rows, S->signs, S->tile_off, S->tile_ent, ctx->stream);
       ctx->launches += 2;
+      if (zeta == 8 && d <= 255 && rowsketch_enabled()) {  // one allocation: rbin | sbit
+        const int64_t tiles_pad = tiles * kTileRows + kTileRows;
+        const size_t bytes = size_t(round_up(tiles_pad * 8, 256) + round_up(tiles_pad, 256) +
+                                    tiles_pad / 32 + 256);
+        void* rb = nullptr;
+        RKMF_CUDA(cudaMalloc(&rb, bytes));
+        RKMF_CUDA(cudaMemsetAsync(rb, 0, bytes, ctx->stream));
+        S->rbin = static_cast<uint8_t*>(rb);
+        S->sbit = S->rbin + round_up(tiles_pad * 8, 256);
+        S->wslow = S->sbit + round_up(tiles_pad, 256);
+        launch_sketch_rowbins(n, int(d), S->rows, S->signs, S->rbin, S->sbit, S->wslow,
+                              ctx->stream);
+        ctx->launches++;
+      }
       RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
       if (S->rows) cudaFree(S->rows);
@@ -612,6 +639,7 @@ int rkmf_sketch_destroy(rkmf_sketch* S) {
   cudaFree(S->rows);
   cudaFree(S->signs);
   cudaFree(S->tile_off);  // also holds tile_ent
+  if (S->rbin) cudaFree(S->rbin);  // also holds sbit
   delete S;
   return RKMF_OK;
 }

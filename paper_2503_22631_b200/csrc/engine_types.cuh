@@ -153,6 +153,9 @@ struct rkmf_sketch {
   uint16_t* tile_off = nullptr;  // one allocation: header, then entries
   uint8_t* tile_ent = nullptr;
   size_t layout_bytes = 0;
+  uint8_t* rbin = nullptr;  // row-major copy for the row-sketch K2 (+ sbit), or null
+  uint8_t* sbit = nullptr;
+  uint8_t* wslow = nullptr;
   SketchView view() const {
     SketchView v;
     v.d = d;
@@ -161,6 +164,9 @@ struct rkmf_sketch {
     v.tile_off = tile_off;
     v.tile_ent = tile_ent;
     v.scale = scale;
+    v.rbin = rbin;
+    v.sbit = sbit;
+    v.wslow = wslow;
     return v;
   }
 };

@@ -122,6 +122,10 @@ void launch_sketch_generate(int64_t d, int64_t n, int64_t j0, int64_t zeta, uint
 void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
                          const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
                          cudaStream_t st);
+// row-major (rbin [n][8] uint8 rows, sbit [n] sign bits) copy for zeta 8,
+// d <= 256, slots edge-coloured per 32-column warp tile (wslow[]: not coloured)
+void launch_sketch_rowbins(int64_t n, int d, const uint16_t* rows, const int8_t* signs,
+                           uint8_t* rbin, uint8_t* sbit, uint8_t* wslow, cudaStream_t st);
 void launch_sketch_export(int64_t count, const uint16_t* rows, const int8_t* signs,
                           int64_t* rows64, cudaStream_t st);
 
@@ -152,6 +156,9 @@ struct SketchView {
   const uint16_t* tile_off;  // [num_tiles][tile_off_stride(d)]: slot offsets, slot bins
   const uint8_t* tile_ent;   // [num_tiles][kTileRows*zeta]: local row | sign<<7
   double scale;
+  const uint8_t* rbin = nullptr;  // row-major copy (zeta 8, d <= 256), or null
+  const uint8_t* sbit = nullptr;
+  const uint8_t* wslow = nullptr;  // per 32-column warp tile: 1 = slots not coloured
 };
 // Per-tile sketch header (uint16): off[d+1] slot offsets, then bin[d] (the
 // sketch row of each slot), padded to 16 bytes.
@@ -191,6 +198,11 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
                         const double* xscale_dev, double* z, double* pacc,
                         const int32_t* stop_flag, int step, int grid, cudaStream_t st);
 int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode);
+// K2 with the sketch in the SpMV threads (spmv_rowsketch.cu): diagonal copy
+// (or the identity: A->dval null, ndiag 1) and a sketch with the row-major copy
+bool launch_spmv_rowsketch(const CsrView* A, const SketchView* S, const double* x,
+                           const double* xscale_dev, double* z, double* pacc,
+                           const int32_t* stop_flag, int step, cudaStream_t st);
 // the same pipeline for the sketch of x alone (mode 2)
 bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double* xscale_dev,
                              double* pacc, cudaStream_t st);

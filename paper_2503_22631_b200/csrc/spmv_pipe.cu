@@ -613,12 +613,16 @@ bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double*
   v.n_rows = S->n;
   v.n_cols = S->n;
   v.ndiag = 1;
+  if (launch_spmv_rowsketch(&v, S, x, xscale_dev, nullptr, pacc, nullptr, 0, st)) return true;
   return launch_pipe_t<int32_t, 1, 1, 2, 1>(&v, S, x, xscale_dev, nullptr, pacc, nullptr, 0, st);
 }
 
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z, double* pacc,
                              const int32_t* stop_flag, int step, cudaStream_t st) {
+  if (A->ndiag > 0 && A->dval &&
+      launch_spmv_rowsketch(A, S, x, xscale_dev, z, pacc, stop_flag, step, st))
+    return true;
   if (A->ndiag > 0 && A->dval) {  // diagonal copy (at most 8 diagonals), x prefetched
 #define RKMF_DIA(NDV) \
   case NDV: return launch_pipe_t<int32_t, 1, 1, 2, NDV>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
