@@ -359,6 +359,37 @@ __global__ void sketch_rowbins_kernel(int64_t n, int d, const uint16_t* __restri
         ++hw[c >> 4][use][b & 15];
       }
     }
+    // local search: swap two slots of one column when both bins stay unique
+    // in their new slots and the half-warp's residue counts get flatter
+    // (sum of squares), i.e. fewer bank conflicts in the kernel
+    for (int pass = 0; pass < 4 && ok; ++pass) {
+      bool moved = false;
+      for (int c = 0; c < nc; ++c) {
+        const int h = c >> 4;
+        for (int q1 = 0; q1 < 8; ++q1)
+          for (int q2 = q1 + 1; q2 < 8; ++q2) {
+            const int b1 = col[c][q1], b2 = col[c][q2];
+            if (binc[b1][q2] >= 0 || binc[b2][q1] >= 0) continue;
+            const int r1 = b1 & 15, r2 = b2 & 15;
+            if (r1 == r2) continue;
+            const int a11 = hw[h][q1][r1], a21 = hw[h][q2][r1];
+            const int a12 = hw[h][q1][r2], a22 = hw[h][q2][r2];
+            // r1 moves q1 -> q2, r2 moves q2 -> q1
+            const int delta = ((a11 - 1) * (a11 - 1) - a11 * a11) + ((a21 + 1) * (a21 + 1) - a21 * a21) +
+                              ((a22 - 1) * (a22 - 1) - a22 * a22) + ((a12 + 1) * (a12 + 1) - a12 * a12);
+            if (delta >= 0) continue;
+            --hw[h][q1][r1]; ++hw[h][q2][r1]; --hw[h][q2][r2]; ++hw[h][q1][r2];
+            binc[b1][q1] = -1; binc[b2][q2] = -1;
+            binc[b1][q2] = int8_t(c); binc[b2][q1] = int8_t(c);
+            col[c][q1] = uint8_t(b2); col[c][q2] = uint8_t(b1);
+            const int8_t t = sgn[c][q1];
+            sgn[c][q1] = sgn[c][q2];
+            sgn[c][q2] = t;
+            moved = true;
+          }
+      }
+      if (!moved) break;
+    }
     // self-check of the colouring before it is trusted: every slot holds
     // distinct bins across the warp tile, and every column holds exactly its
     // own 8 (row, sign) entries
