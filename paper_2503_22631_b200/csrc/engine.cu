@@ -875,25 +875,40 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
 
     // dense-f state
     const int64_t Ncap = std::min<int64_t>(opts.budget_total_m, opts.k_max * m_eff);
-    int64_t ldR = 0;
+    // R_accum lives in the context's buffer (capacity ctx->racc_cap, kept
+    // across solves so a solve does not allocate, free and synchronise as
+    // R_accum grows); the stripes a cycle adds are zeroed on the stream
+    int64_t ldR = 0, used = 0;
     double* Racc = nullptr;
     auto ensure_racc = [&](int64_t N) {
-      if (N <= ldR) return;
-      int64_t newld = std::min<int64_t>(Ncap, std::max<int64_t>(N, 2 * ldR));
-      newld = std::max(newld, N);
-      DevBuf nb;
-      nb.ensure(sizeof(double) * size_t(newld) * size_t(newld));
-      RKMF_CUDA(cudaMemsetAsync(nb.p, 0, sizeof(double) * size_t(newld) * size_t(newld), st));
-      if (ldR > 0)
-        RKMF_CUDA(cudaMemcpy2DAsync(nb.p, sizeof(double) * size_t(newld), Racc,
-                                    sizeof(double) * size_t(ldR), sizeof(double) * size_t(ldR),
-                                    size_t(ldR), cudaMemcpyDeviceToDevice, st));
-      RKMF_CUDA(cudaStreamSynchronize(st));
-      ctx->Racc.release();
-      ctx->Racc = nb;
-      nb.p = nullptr;
-      Racc = ctx->Racc.as<double>();
-      ldR = newld;
+      if (N > ctx->racc_cap) {  // grow geometrically, up to the budget
+        int64_t newld = std::min<int64_t>(Ncap, std::max<int64_t>(N, 2 * ctx->racc_cap));
+        newld = std::max(newld, N);
+        DevBuf nb;
+        nb.ensure(sizeof(double) * size_t(newld) * size_t(newld));
+        if (Racc && used > 0)
+          RKMF_CUDA(cudaMemcpy2DAsync(nb.p, sizeof(double) * size_t(newld), Racc,
+                                      sizeof(double) * size_t(ldR), sizeof(double) * size_t(used),
+                                      size_t(used), cudaMemcpyDeviceToDevice, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+        ctx->Racc.release();
+        ctx->Racc = nb;
+        nb.p = nullptr;
+        ctx->racc_cap = newld;
+        Racc = nullptr;
+      }
+      if (!Racc) {
+        Racc = ctx->Racc.as<double>();
+        ldR = ctx->racc_cap;
+      }
+      if (N > used) {  // rows [used, N) of columns [0, N), then columns [used, N) above them
+        RKMF_CUDA(cudaMemset2DAsync(Racc + used, sizeof(double) * size_t(ldR), 0,
+                                    sizeof(double) * size_t(N - used), size_t(N), st));
+        if (used > 0)
+          RKMF_CUDA(cudaMemset2DAsync(Racc + used * ldR, sizeof(double) * size_t(ldR), 0,
+                                      sizeof(double) * size_t(used), size_t(N - used), st));
+        used = N;
+      }
     };
     QuadState q{};
     double* partial = nullptr;

@@ -69,7 +69,8 @@ struct rkmf_context {
   SolveState* st_host = nullptr;  // pinned
   DevBuf z, pacc, sacc, W, U, Rbar, Racc, ws, u, g, fhat, ref, partial, qshift, qweight, qpi,
       qemx, scratch, gram, cl, diag;
-  int64_t racc_ld = 0;
+  int64_t racc_ld = 0;   // leading dimension of the last solve's R_accum
+  int64_t racc_cap = 0;  // allocated leading dimension of Racc (kept across solves)
   std::vector<double> last_R;
   int64_t last_M = 0;
   std::vector<cudaEvent_t> events;
