@@ -152,7 +152,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
     };
     if ((debug & 16) && wait_prev(0)) return;  // ablation: no early stage fill
     const uint64_t pol = l2_policy(l2_hints >= 1 ? 1 : 0);
-    // the sketch tile layout is re-read every step: ask L2 to keep it
+    // the sketch tile layout's policy (RKMF_L2_HINTS, env_l2_hints)
     const uint64_t mpol = l2_policy(l2_hints);
     // row-pointer pair of the next tile, prefetched one iteration ahead so the
     // bulk copies of a tile are issued without a dependent global round trip
@@ -419,15 +419,17 @@ size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages, int fmt) 
   return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
 }
 
-// RKMF_L2_HINTS: 0 no L2 hints, 1 evict_first on the matrix and sketch
-// streams, 2 (default) evict_first on the matrix and evict_last on the sketch
-// tile layout, which every step re-reads.
+// RKMF_L2_HINTS: 0 no L2 hints, 1 (default) evict_first on the matrix and
+// sketch streams, 2 evict_first on the matrix and evict_last on the sketch
+// tile layout (re-read every step). Keeping the layout in L2 helps K2 less than
+// the L2 it takes from K4's streams costs: cfg2 solve 8590 vs 8540 vec/s
+// (five alternating runs each) with 1.
 int env_l2_hints() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("RKMF_L2_HINTS");
-    v = e ? atoi(e) : 2;
-    if (v < 0 || v > 2) v = 2;
+    v = e ? atoi(e) : 1;
+    if (v < 0 || v > 2) v = 1;
   }
   return v;
 }

@@ -266,7 +266,7 @@ bool launch_rs_t(const CsrView* A, const SketchView* S, const double* x, const d
   launch_maybe_pdl(fn, dim3(grid), dim3(kRsThreads), smem, st, A->n_rows, A->dval, x, xscale_dev,
                    z, tiles, int(S->d), S->rbin, S->sbit, S->wslow, S->scale, pacc, stop, step,
                    stages,
-                   A->doff, A->n_cols, A->dstride, 2);
+                   A->doff, A->n_cols, A->dstride, 1);
   return true;
 }
 
