@@ -1,19 +1,28 @@
 #!/usr/bin/env python
 """bench.py — restarted randomized-Arnoldi f(A)b on B200.
 
-One "step" = one full restarted f(A)b solve of the workload (default BASELINE
-configs[1] = cfg2: 3D 7-point Laplacian 128^3, exp(-tA)b, m=50, s=200, zeta=8,
-tol 1e-8 relative) with A, S and b resident in HBM. The metric is Krylov basis
-vectors per second (sum of m_k over cycles / solve time), whole job.
+One "step" = one full restarted f(A)b solve of the workload with A, S and b
+resident in HBM; the metric is Krylov basis vectors per second (sum of m_k
+over the solve's cycles / solve time), whole job.
+
+Workloads (BASELINE.json configs; --config overrides):
+  * N = 1 (default): cfg4 — 3D upwind convection-diffusion 256^3 (16.8M rows,
+    117M nnz), exp(-tA)b, m=30, s=120: the largest single-GPU config whose
+    reference CPU path fits a bounded sample (configs[3]).
+  * N > 1: cfg5 strong-scaled — the 512^3 Q1 27-point matrix (134M rows, 3.6e9
+    nnz) row-partitioned over the N GPUs (whole x-planes per rank, generated
+    in HBM), halo send/recv + sketch allreduce over NCCL every Krylov step
+    (configs[4]).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config cfg1..cfg5]
 
-N > 1 (torchrun, one rank per GPU): one row-partitioned solve over all ranks
-(weak scaling: each rank owns a cfg2-sized x-slab of a 128N x 128 x 128 grid;
-halo send/recv + sketch allreduce over NCCL every Krylov step).
-`--impl reference` times the CPU restatement of the reference solver (the
-reference itself cannot be built here: Eigen3 is absent) on the host cores.
+`--gpus N` with N > 1 re-executes itself under torch.distributed.run (one rank
+per GPU) unless it already runs under a launcher. `--impl reference` times the
+reference's CPU solver path on the host cores (the Eigen-free restatement in
+oracle/: the reference itself is not buildable here) on the same
+config; that arm never loads the product library (its inputs come from the
+oracle's own generators, oracle/problems_oracle.cpp).
 """
 from __future__ import annotations
 
@@ -21,6 +30,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,6 +41,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Krylov basis vectors/sec (restarted randomized-Arnoldi f(A)b)"
 UNIT = "basis_vectors/s"
+L2_POLICY = "inputs larger than L2 (the matrix and the basis W exceed the 126 MB L2)"
 
 
 def env_rank():
@@ -38,12 +49,22 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def workload_desc(P, name):
-    return {"workload": f"{name}: BASELINE configs[{int(name[-1]) - 1}]", "matrix_rows": P.n,
-            "nnz": P.nnz, "function": P.fn, "t": P.t, "m": P.m, "sketch_d": P.d,
-            "zeta": P.zeta, "tol_abs": P.tol, "tol_rel": P.tol / float(sum(P.b * P.b)) ** 0.5,
-            "k_max": P.k_max, "b_seed": 1, "sketch_seed": 1,
-            "l2_policy": "inputs larger than L2 (CSR + basis W exceed 126 MB)"}
+def default_config(gpus: int) -> str:
+    return "cfg4" if gpus <= 1 else "cfg5"
+
+
+def workload_config(name: str, meta: dict, world: int) -> dict:
+    """The `config` dict both arms print (identical for the same workload)."""
+    from paper_2503_22631_b200 import configs
+    cfg = configs.CONFIGS[name]
+    d = {"workload": f"{name}: BASELINE configs[{int(name[-1]) - 1}]",
+         "matrix_rows": int(meta["n"]), "nnz": int(meta["nnz"]), "function": cfg["fn"],
+         "t": float(meta["t"]), "m": cfg["m"], "sketch_d": cfg["d"], "zeta": cfg["zeta"],
+         "tol_rel": cfg["tol_rel"], "tol_abs": float(meta["tol"]), "k_max": int(meta["k_max"]),
+         "b_seed": configs.B_SEED, "sketch_seed": configs.SKETCH_SEED, "l2_policy": L2_POLICY,
+         "parallelism": "single GPU" if world == 1 else
+                        f"row-partitioned over {world} GPUs (whole x-planes per rank)"}
+    return d
 
 
 class ClockSampler:
@@ -106,13 +127,11 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def class_bytes(w, total_m, cycles):
+def class_bytes(n, nnz, m, total_m, cycles):
     """Algorithmic bytes per solve (per rank) for each kernel class (SURVEY.md
-    §8(d) terms)."""
-    n, nnz, m = w.n, w.nnz, w.m
+    §8(d) terms; CSR definition: 12 nnz + row pointers per SpMV)."""
     rp = 4 if nnz < 2**31 - 1 else 8
-    steps = total_m
-    spmv = steps * (12 * nnz + rp * (n + 1) + 8 * n + 8 * n)
+    spmv = total_m * (12 * nnz + rp * (n + 1) + 8 * n + 8 * n)
     upd = 0
     for _ in range(cycles):
         for k in range(m - 1):
@@ -123,22 +142,48 @@ def class_bytes(w, total_m, cycles):
             "start_sketch_init": start}
 
 
+def k2_streamed_bytes(n, nnz, ndiag, d, zeta):
+    """Bytes K2 streams by design per launch: the matrix stream it actually
+    reads (the diagonal copy: 8 ndiag per row; else CSR 12 nnz + 4 (n+1)), the
+    sketch tile layout (per 128-row tile a uint16 header of 2 off_stride and
+    128 zeta entry bytes), x read and z written."""
+    tiles = (n + 127) // 128
+    off_stride = (2 * d + 1 + 7) // 8 * 8
+    mat = 8 * ndiag * tiles * 128 if ndiag else 12 * nnz + 4 * (n + 1)
+    return mat + tiles * (2 * off_stride + 128 * zeta) + 16 * n
+
+
+# ------------------------------ reference arm ------------------------------
 _ORACLE_SKETCH = {}
 
 
-def cpu_baseline_sample(P, threads: int, cycles: int = 1, m_r: int | None = None):
-    """Oracle port on the host: `cycles` full restart cycles of the workload."""
+def oracle_cycle(P, threads: int, cycles: int = 1, m_r=None):
+    """The oracle port on the host: `cycles` full restart cycles of P."""
     from oracle import oracle as O
     key = (P.d, P.n, P.zeta)
     if key not in _ORACLE_SKETCH:
         _ORACLE_SKETCH[key] = O.make_sketch(P.d, P.n, P.zeta, 1)
-    S = _ORACLE_SKETCH[key]
     kind = O.KIND_EXP_NEG if P.fn == "exp_neg" else O.KIND_INV_SQRT
     t0 = time.perf_counter()
     r = O.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, kind, P.t, m_r=m_r or P.m,
-                           tol=1e-300, k_max=cycles, S=S, threads=threads)
-    dt = time.perf_counter() - t0
-    return r.total_m / dt, dt, r
+                           tol=1e-300, k_max=cycles, S=_ORACLE_SKETCH[key], threads=threads)
+    return r.total_m, time.perf_counter() - t0
+
+
+def reference_sample(name: str):
+    """(problem to time, scale, description). cfg1-4: the config itself. cfg5
+    (3.6e9 nonzeros, ~100 GB of host memory for the oracle) is sampled on its
+    own operator family at 128^3 nodes (1/64 of the rows): the solver's work
+    per basis vector is linear in the rows (SpMV, sketch, Gram-Schmidt and
+    updates all stream n-vectors; the dense f does not depend on n), so the
+    sample's vectors/s are scaled by n_sample / n."""
+    from paper_2503_22631_b200 import configs
+    if name != "cfg5":
+        return configs.build(name, backend="oracle"), 1.0, f"{name} itself"
+    N = 128
+    P = configs.build("cfg5", N, backend="oracle")
+    n_full = configs.CONFIGS["cfg5"]["N"] ** 3
+    return P, P.n / n_full, f"cfg5's operator on {N}^3 nodes, vectors/s x n_sample/n"
 
 
 def run_reference(args):
@@ -146,91 +191,152 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_2503_22631_b200 import configs
-    P = configs.build(args.config)
+    name = args.config
+    P, scale, what = reference_sample(name)
+    if name == "cfg5":
+        meta = full_meta(name)
+    else:
+        meta = {"n": P.n, "nnz": P.nnz, "t": P.t, "tol": P.tol, "k_max": P.k_max}
     threads = os.cpu_count() or 1
-    vals = []
-    for _ in range(args.warmup):  # cache/page warm-up: short 5-vector cycles
-        cpu_baseline_sample(P, threads, 1, m_r=5)
-    for _ in range(args.steps):
-        v, dt, r = cpu_baseline_sample(P, threads, 1)
-        vals.append((r.total_m, dt))
+    for _ in range(args.warmup):  # page-in / thread warm-up: short 5-vector cycles
+        oracle_cycle(P, threads, 1, m_r=5)
+    vals = [oracle_cycle(P, threads, 1) for _ in range(args.steps)]
     tot_m = sum(v[0] for v in vals)
     tot_t = sum(v[1] for v in vals)
-    value = tot_m / tot_t
-    sample = (f"one restart cycle (m={P.m} basis vectors, incl. per-cycle validate/norm1 and the "
-              f"full dense f) of {args.config} per step, oracle port, {threads} threads")
+    value = tot_m / tot_t * scale
+    maps = open("/proc/self/maps").read()
+    assert "librkmf_b200" not in maps, "the reference arm must not map the product library"
+    sample = (f"one restart cycle (m={P.m} basis vectors, incl. the reference's per-cycle "
+              f"validate/norm1 and full dense f) per step on {what}; oracle port of the "
+              f"reference solver path, {threads} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / len(vals), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_desc(P, args.config),
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, BASELINE.json shapes)",
+            "config": workload_config(name, meta, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
+            "libraries_mapped": sorted({ln.split()[-1] for ln in maps.splitlines()
+                                        if ln.endswith(".so") and ("oracle" in ln
+                                                                   or ROOT in ln)}),
             "note": "the reference (Eigen-based C++) is not buildable in this image; its CPU "
-                    "path is the Eigen-free restatement in oracle/ (DESIGN.md)"}
+                    "path is the Eigen-free restatement in oracle/ (DESIGN.md §4)"}
     print(json.dumps(line), flush=True)
     return 0
 
 
+def full_meta(name: str) -> dict:
+    """n, nnz, t, tol, k_max of a config without building it (cfg5)."""
+    from paper_2503_22631_b200 import configs
+    cfg = configs.CONFIGS[name]
+    N = cfg["N"]
+    n = N ** 3
+    nnz = (3 * N - 2) ** 3
+    norm2 = configs.frozen_norm2(name, N)
+    return {"n": n, "nnz": nnz, "t": cfg["c"] / norm2 if norm2 else float("nan"),
+            "tol": configs.frozen_tol(name, N), "k_max": configs.BUDGET_TOTAL_M // cfg["m"]}
+
+
+# ------------------------------ our arm ------------------------------
 class Workload:
-    """What one rank solves: the device objects plus the sizes the byte model
-    and the JSON line need."""
+    """What one rank solves: device objects, host b, sizes for the byte model."""
 
 
-def setup_single(args, ctx, dev):
+def setup_single(name, ctx, dev):
     import torch
 
     import paper_2503_22631_b200 as rk
     from paper_2503_22631_b200 import configs
-    P = configs.build(args.config)
     w = Workload()
-    w.P, w.n, w.nnz, w.m = P, P.n, P.nnz, P.m
-    w.A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values, ctx=ctx)
-    w.S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, ctx=ctx)
-    w.f = rk.FunctionSpec.exp_neg(P.t) if P.fn == "exp_neg" else rk.FunctionSpec.inv_sqrt()
-    w.opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
-    w.b_host = P.b
-    w.b_dev = torch.tensor(P.b, device=dev)
-    w.config = dict(workload_desc(P, args.config), parallelism="single",
-                    matrix_stream=(f"diagonal copy, {w.A.ndiag} diagonals (uploaded as CSR)"
-                                   if w.A.ndiag else "CSR"))
+    t0 = time.perf_counter()
+    if name == "cfg5":  # 3.6e9 nonzeros: generated in HBM, never on the host
+        P = configs.build_device(name, ctx=ctx)
+        w.P = None
+        w.A, w.b_dev = P.A, P.b
+        w.b_host = P.b.cpu().numpy()
+        t, tol, k_max, m, d, zeta, fn = P.t, P.tol, P.k_max, P.m, P.d, P.zeta, P.fn
+        n, nnz = P.n, P.nnz
+    else:
+        P = configs.build(name)
+        w.P = P
+        w.A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values, ctx=ctx)
+        w.b_host = P.b
+        w.b_dev = torch.tensor(P.b, device=dev)
+        t, tol, k_max, m, d, zeta, fn = P.t, P.tol, P.k_max, P.m, P.d, P.zeta, P.fn
+        n, nnz = P.n, P.nnz
+    torch.cuda.synchronize()
+    w.setup_s = {"matrix_s": time.perf_counter() - t0}
+    t1 = time.perf_counter()
+    w.S = rk.make_sketch(d, n, zeta, configs.SKETCH_SEED, ctx=ctx)
+    torch.cuda.synchronize()
+    w.setup_s["sketch_s"] = time.perf_counter() - t1
+    w.n, w.nnz, w.m, w.d, w.zeta = n, nnz, m, d, zeta
+    w.f = rk.FunctionSpec.exp_neg(t) if fn == "exp_neg" else rk.FunctionSpec.inv_sqrt()
+    w.opts = rk.RestartOptions(m_r=m, tol=tol, k_max=k_max)
+    w.meta = {"n": n, "nnz": nnz, "t": t, "tol": tol, "k_max": k_max}
+    w.world_vectors = 1
     return w
 
 
-def setup_partitioned(args, ctx_device, world, rank, dev):
-    """Weak scaling: rank r owns an x-slab of cfg2's size (configs.build_slab);
-    one distributed solve over all ranks (halo exchange + sketch allreduce)."""
+def setup_partitioned(name, local, world, rank, dev):
+    """cfg5 strong-scaled: rank r owns whole x-planes [r N/world, (r+1) N/world)
+    of the 512^3 Q1 matrix, generated in HBM with its halo plan; b's slice and
+    the sketch's column range on device."""
     import torch
 
     import paper_2503_22631_b200 as rk
     from paper_2503_22631_b200 import configs
     from paper_2503_22631_b200 import distributed as D
     transport = os.environ.get("RKMF_BENCH_TRANSPORT", "nccl")
-    ctx = D.make_context(ctx_device, world, rank, transport)
-    Sl = configs.build_slab(world, rank)
-    part = D.partition_local(ctx, Sl.n_global, Sl.row_starts, Sl.row_ptr, Sl.col_idx, Sl.values,
-                             Sl.b, Sl.d, Sl.zeta, configs.SKETCH_SEED, rank)
+    cfg = configs.CONFIGS[name]
+    N = int(os.environ.get("RKMF_BENCH_N", cfg["N"]))  # smaller grids: functional runs only
+    if cfg["kind"] != "q1":
+        raise SystemExit(f"--gpus > 1 runs the Q1 configs (cfg3/cfg5), not {name}")
+    ctx = D.make_context(local, world, rank, transport)
+    plane = N * N
+    row_starts = [plane * (N * q // world) for q in range(world + 1)]
+    t0 = time.perf_counter()
+    A = rk.SparseMatrix.q1_hex_partitioned(ctx, N, row_starts, cfg["lognormal"],
+                                           configs.COEF_SEED, cfg["dirichlet"])
+    rb, re = row_starts[rank], row_starts[rank + 1]
+    b_dev = rk.gen_gaussian_device(configs.B_SEED, rb, re - rb, ctx)
+    torch.cuda.synchronize()
+    setup = {"matrix_s": time.perf_counter() - t0}
+    t1 = time.perf_counter()
+    S = rk.partitioned_sketch(ctx, cfg["d"], N ** 3, cfg["zeta"], configs.SKETCH_SEED, rb, re - rb)
+    torch.cuda.synchronize()
+    setup["sketch_s"] = time.perf_counter() - t1
+    norm2, tol = configs.frozen_norm2(name, N), configs.frozen_tol(name, N)
+    if norm2 is None or tol is None:
+        if N > 160:
+            raise SystemExit(f"{name} at N={N}: no frozen ||A||_2 / ||b|| (configs.NORM2_FROZEN)")
+        Ph = configs.build(name, N)  # small functional grids: the host definition
+        norm2, tol = Ph.norm2, Ph.tol
     w = Workload()
-    w.ctx, w.P, w.n, w.nnz, w.m = ctx, None, part.n_local, Sl.nnz, Sl.m
-    w.A, w.S = part.A, part.S
-    w.f = rk.FunctionSpec.exp_neg(Sl.t)
-    w.opts = rk.RestartOptions(m_r=Sl.m, tol=Sl.tol, k_max=Sl.k_max)
-    w.b_host = part.b
-    w.b_dev = torch.tensor(part.b, device=dev)
-    w.config = {"workload": f"cfg2 weak-scaled: 3D 7-point Laplacian {128 * world}x128x128, "
-                            f"one {128}^3 x-slab (cfg2's rows) per GPU",
-                "matrix_rows": Sl.n_global, "nnz": Sl.nnz_global, "rows_per_gpu": part.n_local,
-                "function": "exp_neg", "t": Sl.t, "m": Sl.m, "sketch_d": Sl.d, "zeta": Sl.zeta,
-                "tol_abs": Sl.tol, "k_max": Sl.k_max, "b_seed": 1, "sketch_seed": 1,
-                "l2_policy": "inputs larger than L2 (CSR + basis W exceed 126 MB)",
-                "parallelism": f"row-partitioned x{world} ({transport}: halo send/recv + "
-                               f"sketch allreduce per Krylov step)",
-                "unit_note": "basis vectors counted per rank slab (value = world x m_k / s)",
-                "matrix_stream": (f"diagonal copy, {part.A.ndiag} diagonals" if part.A.ndiag
-                                  else "CSR")}
+    w.ctx, w.P, w.A, w.S, w.b_dev = ctx, None, A, S, b_dev
+    w.b_host = b_dev.cpu().numpy()
+    w.n, w.nnz, w.m, w.d, w.zeta = re - rb, A.nnz, cfg["m"], cfg["d"], cfg["zeta"]
+    w.f = rk.FunctionSpec.exp_neg(cfg["c"] / norm2)
+    w.opts = rk.RestartOptions(m_r=cfg["m"], tol=tol, k_max=configs.BUDGET_TOTAL_M // cfg["m"])
+    w.meta = {"n": N ** 3, "nnz": (3 * N - 2) ** 3, "t": cfg["c"] / norm2, "tol": tol,
+              "k_max": configs.BUDGET_TOTAL_M // cfg["m"]}
+    w.setup_s = setup
+    w.transport = transport
+    w.world_vectors = 1  # strong scaling: one solve's basis vectors, not per rank
     return w
+
+
+def load_traffic(name, kernel):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tj = json.load(fh)
+        ent = tj.get(name, {}).get(kernel)
+        return (ent["bytes"], ent.get("capture")) if ent else (None, None)
+    except Exception:
+        return None, None
 
 
 def run_ours(args):
@@ -240,21 +346,23 @@ def run_ours(args):
     import paper_2503_22631_b200 as rk
 
     rank, world, local = env_rank()
-    if os.environ.get("RKMF_BENCH_ONE_GPU"):  # functional runs of N ranks on one GPU
-        local = 0                             # (with RKMF_BENCH_TRANSPORT=host); not timing
+    one_gpu = bool(os.environ.get("RKMF_BENCH_ONE_GPU"))
+    if one_gpu:  # functional runs of N ranks on one GPU (host transport); not timing
+        local = 0
     torch.cuda.set_device(local)
-    if world > 1 and os.environ.get("RKMF_BENCH_ONE_GPU"):
+    if world > 1 and one_gpu:
         dist.init_process_group("gloo")  # NCCL refuses two ranks on one device
     elif world > 1:
         # CPU tensors (host transport, timing reductions) over gloo, CUDA over NCCL
         dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
+    name = args.config
     if world > 1:
-        w = setup_partitioned(args, local, world, rank, dev)
+        w = setup_partitioned(name, local, world, rank, dev)
         ctx = w.ctx
     else:
         ctx = rk.Context.default(local)
-        w = setup_single(args, ctx, dev)
+        w = setup_single(name, ctx, dev)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream)
     A, S, f, opts, b_dev = w.A, w.S, w.f, w.opts, w.b_dev
@@ -286,60 +394,37 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    value = world * total_m / (max_ms / 1e3)
-
-    # ---- setup (once per matrix, outside both timed regions, reported):
-    #      CSR upload from pinned host memory + validation, device sketch ----
-    setup = None
-    A2, S2 = A, S
-    if world == 1:
-        from paper_2503_22631_b200 import configs
-        P = w.P
-        rp_h = torch.from_numpy(P.row_ptr).pin_memory()
-        ci_h = torch.from_numpy(P.col_idx).pin_memory()
-        v_h = torch.from_numpy(P.values).pin_memory()
-        torch.cuda.synchronize()
-        s0 = time.perf_counter()
-        A2 = rk.SparseMatrix.from_csr(rp_h.numpy(), ci_h.numpy(), v_h.numpy(), ctx=ctx)
-        s1 = time.perf_counter()
-        S2 = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, ctx=ctx)
-        torch.cuda.synchronize()
-        s2 = time.perf_counter()
-        setup = {"matrix_upload_validate_s": s1 - s0, "sketch_generate_s": s2 - s1,
-                 "h2d_bytes": 8 * (P.n + 1) + 12 * P.nnz}
+    value = w.world_vectors * total_m / (max_ms / 1e3)
 
     # ---- e2e: the reference-facing call with HOST vectors: every step copies
     #      b host->device (pinned) and f device->host inside the timed region ----
     b_h = torch.from_numpy(w.b_host).pin_memory()
     f_h = torch.empty(w.n, dtype=torch.float64).pin_memory()
-    e2e_steps = max(1, args.steps)
-    rk.restarted_krylov(A2, b_h.numpy(), f, opts, S2, out=f_h.numpy())  # warm-up
+    rk.restarted_krylov(A, b_h.numpy(), f, opts, S, out=f_h.numpy())  # warm-up
     barrier()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     e2e_m = 0
-    for _ in range(e2e_steps):
-        r2 = rk.restarted_krylov(A2, b_h.numpy(), f, opts, S2, out=f_h.numpy())
+    for _ in range(max(1, args.steps)):
+        r2 = rk.restarted_krylov(A, b_h.numpy(), f, opts, S, out=f_h.numpy())
         e2e_m += r2.total_m
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
-    del A2, S2
     et = torch.tensor([e2e_s], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = world * e2e_m / float(et.item())
-    h2d = 8 * w.n
-    d2h = 8 * w.n
+    e2e_value = w.world_vectors * e2e_m / float(et.item())
 
     # ---- per-kernel breakdown (separate diagnostic solve, events per launch;
     #      every rank runs it so the collectives match) ----
     ctx.kernel_timing(True)
     ctx.kernel_times(reset=True)
-    rb = rk.restarted_krylov(A, b_dev, f, opts, S)
+    rb_ = rk.restarted_krylov(A, b_dev, f, opts, S)
     kt = ctx.kernel_times(reset=True)
     ctx.kernel_timing(False)
+    comm = ctx.comm_info()
     if rank == 0:
-        cb = class_bytes(w, rb.total_m, rb.cycles)
+        cb = class_bytes(w.n, w.nnz, w.m, rb_.total_m, rb_.cycles)
         peak, peak_src = measured_peaks()
         kernels = {}
         for cls, (kms, cnt) in kt.items():
@@ -348,53 +433,65 @@ def run_ours(args):
                 gbs = cb[cls] / (kms / 1e3) / 1e9
                 ent.update({"alg_bytes": cb[cls], "achieved_gbs": gbs, "frac": gbs / peak})
             kernels[cls] = ent
+        k2 = kernels["spmv_sketch"]
+        if k2["launches"]:
+            sb = k2_streamed_bytes(w.n, w.nnz, A.ndiag, w.d, w.zeta)
+            gbs = sb * k2["launches"] / (k2["ms"] / 1e3) / 1e9
+            k2.update({"streamed_bytes_per_launch": sb, "streamed_gbs": gbs,
+                       "streamed_frac": gbs / peak,
+                       "stream": (f"diagonal copy ({A.ndiag} diagonals)" if A.ndiag else "CSR")
+                       + " + sketch tile layout + x + z"})
         dom = max((c for c in cb if kernels[c]["ms"] > 0), key=lambda c: kernels[c]["ms"])
         dk = kernels[dom]
-        cyc_bytes = sum(cb.values())
-        traffic = None  # per-launch DRAM bytes of the committed ncu --set full capture
-        try:
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-                tj = json.load(fh)
-            if world == 1 and args.config == "cfg2" and dom in tj:
-                traffic = tj[dom]["bytes"]
-        except Exception:
-            pass
+        traffic, capture = (load_traffic(name, dom) if world == 1 else (None, None))
         roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"],
                     "peak": peak, "unit": "GB/s", "frac": dk["frac"],
-                    "traffic": traffic, "alg_bytes_per_launch": dk["alg_bytes"] / dk["launches"],
+                    "traffic": traffic, "traffic_capture": capture,
+                    "alg_bytes_per_launch": dk["alg_bytes"] / dk["launches"],
                     "avg_launch_ms": dk["ms"] / dk["launches"], "peak_source": peak_src,
-                    "whole_solve_gbs": cyc_bytes / (max_ms / args.steps / 1e3) / 1e9,
+                    "whole_solve_gbs": sum(cb.values()) / (max_ms / args.steps / 1e3) / 1e9,
                     "per_kernel_frac": {c: kernels[c]["frac"] for c in cb
                                         if "frac" in kernels[c]}}
         cpu = None
-        if world == 1:
-            cv, cdt, cr = cpu_baseline_sample(w.P, 1, 1)
-            cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"one restart cycle (m={w.m}) of {args.config}, single thread, "
+        if world == 1 and w.P is not None:
+            cm, cdt = oracle_cycle(w.P, 1, 1)
+            cpu = {"value": cm / cdt, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"one restart cycle (m={w.m}) of {name}, single thread, "
                              f"{cdt:.1f} s"}
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+               "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generators, BASELINE.json shapes)",
-               "config": w.config,
+               "config": workload_config(name, w.meta, world),
+               "device_config": {"matrix_stream": (f"diagonal copy, {A.ndiag} diagonals"
+                                                   if A.ndiag else "CSR"),
+                                 "rows_per_gpu": w.n, "nnz_per_gpu": w.nnz},
+               "comm": comm,
                "solve": {"cycles": res.cycles, "total_m": res.total_m,
-                         "converged": res.converged,
-                         "solve_ms": max_ms / args.steps,
+                         "converged": res.converged, "solve_ms": max_ms / args.steps,
                          "update_norms": [h.update_norm for h in res.history],
-                         "dense_f_ms": [h.funm_ms for h in rb.history]},
+                         "dense_f_ms": [h.funm_ms for h in rb_.history]},
                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
-               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h,
+               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * w.n,
+                       "d2h_bytes_per_step": 8 * w.n,
                        "note": "restarted_krylov(A, b_host, ...) per step with A and S "
-                               "resident; setup reported separately",
-                       "ms_per_step": 1e3 * float(et.item()) / e2e_steps},
-               "setup": setup,
-               "gpu_launches": gpu_launches, "clocks": clk.summary()}
+                               "resident (per-rank bytes); setup reported separately",
+                       "ms_per_step": 1e3 * float(et.item()) / max(1, args.steps)},
+               "setup": w.setup_s, "gpu_launches": gpu_launches, "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -403,10 +500,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default=None)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: W >= 3
+    if args.config is None:
+        args.config = default_config(args.gpus)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

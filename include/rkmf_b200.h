@@ -32,6 +32,7 @@ extern "C" {
 #define RKMF_NUMERICAL_ERROR 3 /* rkmf::NumericalError */
 #define RKMF_DEVICE_ERROR 4    /* CUDA / NCCL failure (rkmf::Error) */
 #define RKMF_INTERNAL_ERROR 5  /* rkmf::Error */
+#define RKMF_PARSE_ERROR 6     /* rkmf::ParseError (Matrix Market / vector files) */
 
 /* ---- function kinds: densefun.hpp:20 FunctionSpec::Kind. EXP_NEG is the
  *      reference's ExpNeg(t): f(z) = exp(-t z). INV_SQRT (f(z) = z^{-1/2}) is
@@ -140,9 +141,14 @@ int rkmf_matrix_info(const rkmf_matrix* A, int64_t* n_rows, int64_t* n_cols, int
  * diagonal copy on creation, streamed by the fused SpMV + sketch instead of the
  * CSR arrays (8 bytes per slot, no indices; results bit-identical). enable = 0
  * drops the copy (CSR path only), 1 builds it if the matrix qualifies, 2
- * only queries; *ndiag (optional) receives the diagonal count, 0 = CSR only. The
- * environment variable RKMF_DIA=0 disables the copy at creation. */
+ * only queries; *ndiag (optional) receives the diagonal count, 0 = CSR only. */
 int rkmf_matrix_dia(rkmf_matrix* A, int enable, int* ndiag);
+/* Copies the device CSR to the host: h_row_ptr[n_rows+1] (int64),
+ * h_col_idx[nnz], h_values[nnz] (sizes from rkmf_matrix_info; any pointer may
+ * be NULL). A partitioned matrix exports its local rows in the local column
+ * numbering [owned | halo]. Backs save_matrix_market (sparse.cpp:196-211). */
+int rkmf_matrix_export(rkmf_context* ctx, const rkmf_matrix* A, int64_t* h_row_ptr,
+                       int32_t* h_col_idx, double* h_values);
 
 /* ---- sketch operator: make_sketch (sketch.cpp:13-49), generated on device,
  *      bit-identical to the reference's SplitMix64/Floyd definition ---- */
@@ -216,6 +222,10 @@ typedef struct rkmf_host_comm {
 } rkmf_host_comm;
 int rkmf_context_init_host_comm(rkmf_context* ctx, int32_t nranks, int32_t rank,
                                 const rkmf_host_comm* callbacks);
+/* The communicator as the library sees it: ranks (ncclCommCount for NCCL),
+ * this rank, transport 0 none / 1 NCCL / 2 host callbacks. */
+int rkmf_context_comm_info(const rkmf_context* ctx, int32_t* nranks, int32_t* rank,
+                           int32_t* transport);
 int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const int64_t* row_starts,
                                    const int64_t* h_row_ptr_local, const int32_t* h_col_global,
                                    const double* h_values, rkmf_matrix** out);
@@ -234,9 +244,68 @@ int rkmf_partition_halo(int32_t nranks, int32_t rank, const int64_t* row_starts,
 int rkmf_matrix_gen_q1_hex(rkmf_context* ctx, int64_t N, int32_t lognormal, uint64_t coef_seed,
                            int32_t dirichlet, rkmf_matrix** out);
 int rkmf_matrix_gen_laplacian(rkmf_context* ctx, int32_t dim, int64_t N, rkmf_matrix** out);
+/* cfg4's upwind convection-diffusion, entries identical to rkmf_gen_convdiff_upwind */
+int rkmf_matrix_gen_convdiff(rkmf_context* ctx, int64_t N, double peclet, double vx, double vy,
+                             double vz, rkmf_matrix** out);
+/* One rank's rows of the Q1 matrix (cfg5 partitioned) generated in HBM, with
+ * the halo plan rkmf_matrix_create_partitioned would build from the same host
+ * rows; row_starts[nranks+1] must be increasing multiples of N^2 (whole
+ * x-planes per rank). Needs the communicator (rkmf_context_init_*comm). */
+int rkmf_matrix_gen_q1_hex_partitioned(rkmf_context* ctx, int64_t N, int32_t lognormal,
+                                       uint64_t coef_seed, int32_t dirichlet,
+                                       const int64_t* row_starts, rkmf_matrix** out);
 /* d_out[i] = gaussian(seed, i0 + i) on the device (rng.hpp:47-59) */
 int rkmf_gen_gaussian_device(rkmf_context* ctx, uint64_t seed, int64_t i0, int64_t n,
                              double* d_out);
+
+/* ---- CycleObserver / CycleInfo (restart.hpp:42-54, restart.cpp:91-92):
+ * test-only hook fired after each cycle's update, fed by device->host copies
+ * (it adds synchronisations; leave it unset on timed runs). All arrays are
+ * host memory owned by the library and valid during the call only:
+ *   W        n x w_cols column-major (ld n): the cycle's basis block as built,
+ *            column 0 = start / alpha_k; w_cols = m_k, +1 when a next vector
+ *            exists (restart.hpp:46)
+ *   R_accum  total_m x total_m column-major, or NULL when R_accum is not kept
+ *            (budget beyond the dense-f capacity)
+ *   update   y_k = f_hat - f_hat_prev (the difference of the two host copies)
+ *   f_hat    the running approximation
+ * When partitioned, n and the vectors are the rank's local rows. ---- */
+typedef struct {
+  int64_t cycle; /* 1-based */
+  int64_t n;
+  int64_t m_k;
+  int64_t w_cols;
+  const double* W;
+  int64_t total_m;
+  const double* R_accum;
+  const double* update;
+  const double* f_hat;
+  double alpha; /* global scale from cycle 1 */
+} rkmf_cycle_info;
+typedef void (*rkmf_cycle_observer)(void* user, const rkmf_cycle_info* info);
+/* Observer for the following solves on ctx (NULL clears it). */
+int rkmf_context_set_observer(rkmf_context* ctx, rkmf_cycle_observer fn, void* user);
+
+/* ---- Matrix Market / vector interchange (sparse.cpp:140-242,
+ * sparse.hpp:55-66): "coordinate real {general|symmetric}", symmetric
+ * expanded, 1-based indices converted, duplicates summed, rows sorted;
+ * vectors one value per line ('%' comments and blank lines skipped); writes
+ * at %.17g. Host-only (no GPU needed). Parse failures return
+ * RKMF_PARSE_ERROR with "path:line: what" in err (err_cap bytes). Arrays
+ * returned by the loaders are malloc'ed by the library: free them with
+ * rkmf_host_free. ---- */
+int rkmf_mtx_load(const char* path, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
+                  int64_t** h_row_ptr, int32_t** h_col_idx, double** h_values, char* err,
+                  int64_t err_cap);
+int rkmf_mtx_save(const char* path, int64_t n_rows, int64_t n_cols, const int64_t* h_row_ptr,
+                  const int32_t* h_col_idx, const double* h_values, char* err, int64_t err_cap);
+int rkmf_vector_load(const char* path, int64_t* n, double** h_out, char* err, int64_t err_cap);
+int rkmf_vector_save(const char* path, int64_t n, const double* h_v, char* err, int64_t err_cap);
+void rkmf_host_free(void* p);
+/* load_matrix_market straight into a validated device matrix / a device
+ * matrix written back out (its CSR copied to the host first) */
+int rkmf_matrix_load_mtx(rkmf_context* ctx, const char* path, rkmf_matrix** out);
+int rkmf_matrix_save_mtx(rkmf_context* ctx, const rkmf_matrix* A, const char* path);
 
 /* R_accum of the last solve on this context (total_m x total_m, column-major,
  * host); n_cap is the caller's capacity in rows. */

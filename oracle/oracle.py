@@ -80,6 +80,12 @@ def lib():
                                          P, P, P, P, P, C.c_char_p]
         L.orc_restarted_krylov.argtypes = [i64, P, P, P, P, i32, d, i64, d, i64, i64, d, i32, i64,
                                            i64, P, P, d, P, i32, P, P, P, i64, P, i64, C.c_char_p]
+        for name, nargs in (("orc_gen_laplacian", [i32, i64]),
+                            ("orc_gen_q1_hex", [i64, i32, u64, i32]),
+                            ("orc_gen_convdiff_upwind", [i64, d, d, d, d])):
+            fn = getattr(L, name)
+            fn.restype = i32
+            fn.argtypes = nargs + [P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -120,6 +126,33 @@ def gaussian_vector(seed: int, n: int) -> np.ndarray:
     out = np.empty(n, np.float64)
     lib().orc_gaussian_vector(seed, n, _p(out))
     return out
+
+
+def _gen(fn, *args):
+    n, nnz = C.c_int64(), C.c_int64()
+    if fn(*args, C.byref(n), C.byref(nnz), None, None, None) != 0:
+        raise OracleError(1, "generator: invalid parameters")
+    rp = np.empty(n.value + 1, np.int64)
+    ci = np.empty(nnz.value, np.int32)
+    v = np.empty(nnz.value, np.float64)
+    fn(*args, C.byref(n), C.byref(nnz), _p(rp), _p(ci), _p(v))
+    return rp, ci, v
+
+
+# BASELINE problem generators restated independently of the product's
+# (problems_oracle.cpp): the reference arm's inputs and the tests' second
+# implementation of the same definitions.
+def gen_laplacian(dim: int, N: int):
+    return _gen(lib().orc_gen_laplacian, dim, N)
+
+
+def gen_q1_hex(N: int, lognormal: bool = False, coef_seed: int = 1, dirichlet: bool = False):
+    return _gen(lib().orc_gen_q1_hex, N, int(lognormal), C.c_uint64(coef_seed), int(dirichlet))
+
+
+def gen_convdiff_upwind(N: int, peclet: float = 10.0, v=(1.0, 0.5, 0.25)):
+    return _gen(lib().orc_gen_convdiff_upwind, N, float(peclet), float(v[0]), float(v[1]),
+                float(v[2]))
 
 
 @dataclass

@@ -66,7 +66,8 @@ class DeviceError(Error):
     """CUDA / NCCL failure inside the device library."""
 
 
-_CODE = {1: ParameterError, 2: ShapeError, 3: NumericalError, 4: DeviceError, 5: Error}
+_CODE = {1: ParameterError, 2: ShapeError, 3: NumericalError, 4: DeviceError, 5: Error,
+         6: ParseError}
 
 
 class RestartOptionsC(C.Structure):
@@ -91,6 +92,15 @@ class RestartResultC(C.Structure):
                 ("peak_basis_cols", C.c_int64), ("n_records", C.c_int64),
                 ("solve_ms", C.c_double)]
 
+
+class CycleInfoC(C.Structure):
+    _fields_ = [("cycle", C.c_int64), ("n", C.c_int64), ("m_k", C.c_int64),
+                ("w_cols", C.c_int64), ("W", C.POINTER(C.c_double)), ("total_m", C.c_int64),
+                ("R_accum", C.POINTER(C.c_double)), ("update", C.POINTER(C.c_double)),
+                ("f_hat", C.POINTER(C.c_double)), ("alpha", C.c_double)]
+
+
+_OBSERVER_CB = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(CycleInfoC))
 
 # Every symbol declared in include/rkmf_b200.h: (name, restype, argtypes)
 _P, _I64, _U64, _D, _I32 = C.c_void_p, C.c_int64, C.c_uint64, C.c_double, C.c_int32
@@ -122,6 +132,7 @@ SYMBOLS = [
     ("rkmf_restarted_krylov", C.c_int,
      [_P, _P, _P, _P, C.c_int, _I32, _D, _P, _P, C.c_int, _P, _P, _P, _I64]),
     ("rkmf_last_r_accum", C.c_int, [_P, _P, _I64, _P]),
+    ("rkmf_context_set_observer", C.c_int, [_P, _OBSERVER_CB, _P]),
     ("rkmf_nccl_unique_id", C.c_int, [_P]),
     ("rkmf_context_init_comm", C.c_int, [_P, _I32, _I32, _P]),
     ("rkmf_context_init_host_comm", C.c_int, [_P, _I32, _I32, _P]),
@@ -137,6 +148,17 @@ SYMBOLS = [
     ("rkmf_matrix_gen_q1_hex", C.c_int, [_P, _I64, _I32, _U64, _I32, _PP]),
     ("rkmf_matrix_gen_laplacian", C.c_int, [_P, _I32, _I64, _PP]),
     ("rkmf_gen_gaussian_device", C.c_int, [_P, _U64, _I64, _I64, _P]),
+    ("rkmf_matrix_export", C.c_int, [_P, _P, _P, _P, _P]),
+    ("rkmf_matrix_gen_convdiff", C.c_int, [_P, _I64, _D, _D, _D, _D, _PP]),
+    ("rkmf_matrix_gen_q1_hex_partitioned", C.c_int, [_P, _I64, _I32, _U64, _I32, _P, _PP]),
+    ("rkmf_context_comm_info", C.c_int, [_P, _P, _P, _P]),
+    ("rkmf_mtx_load", C.c_int, [C.c_char_p, _P, _P, _P, _P, _P, _P, C.c_char_p, _I64]),
+    ("rkmf_mtx_save", C.c_int, [C.c_char_p, _I64, _I64, _P, _P, _P, C.c_char_p, _I64]),
+    ("rkmf_vector_load", C.c_int, [C.c_char_p, _P, _P, C.c_char_p, _I64]),
+    ("rkmf_vector_save", C.c_int, [C.c_char_p, _I64, _P, C.c_char_p, _I64]),
+    ("rkmf_host_free", None, [_P]),
+    ("rkmf_matrix_load_mtx", C.c_int, [_P, C.c_char_p, _PP]),
+    ("rkmf_matrix_save_mtx", C.c_int, [_P, _P, C.c_char_p]),
 ]
 
 _lib = None
@@ -186,6 +208,7 @@ class Context:
 
     def __init__(self, device: int = 0):
         self.device = device
+        self.solves = 0  # solves run on this context (RestartResult.R_accum guard)
         h = C.c_void_p()
         code = lib().rkmf_context_create(device, C.byref(h))
         if code != RKMF_OK:
@@ -208,6 +231,13 @@ class Context:
         """Launch on a torch.cuda.Stream / raw cudaStream_t (None = own stream)."""
         raw = None if stream is None else getattr(stream, "cuda_stream", stream)
         self.check(lib().rkmf_context_set_stream(self.h, raw))
+
+    def comm_info(self) -> dict:
+        """The communicator as the library sees it (NCCL: ncclCommCount)."""
+        n, r, t = C.c_int32(), C.c_int32(), C.c_int32()
+        self.check(lib().rkmf_context_comm_info(self.h, C.byref(n), C.byref(r), C.byref(t)))
+        return {"nranks": n.value, "rank": r.value,
+                "transport": {0: "none", 1: "nccl", 2: "host"}.get(t.value, "?")}
 
     @property
     def launch_count(self) -> int:
@@ -304,6 +334,48 @@ class SparseMatrix:
         h = C.c_void_p()
         ctx.check(lib().rkmf_matrix_gen_laplacian(ctx.h, dim, N, C.byref(h)))
         return cls(ctx, h)
+
+    @classmethod
+    def convdiff(cls, N: int, peclet: float = 10.0, v=(1.0, 0.5, 0.25),
+                 ctx: Optional[Context] = None) -> "SparseMatrix":
+        """3D upwind convection-diffusion (cfg4), generated in HBM."""
+        ctx = ctx or Context.default()
+        h = C.c_void_p()
+        ctx.check(lib().rkmf_matrix_gen_convdiff(ctx.h, N, float(peclet), float(v[0]), float(v[1]),
+                                                 float(v[2]), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def q1_hex_partitioned(cls, ctx: Context, N: int, row_starts, lognormal: bool = False,
+                           coef_seed: int = 1, dirichlet: bool = False) -> "SparseMatrix":
+        """This rank's whole x-planes of the Q1 matrix (cfg5 partitioned), in HBM."""
+        rs = np.ascontiguousarray(row_starts, np.int64)
+        h = C.c_void_p()
+        ctx.check(lib().rkmf_matrix_gen_q1_hex_partitioned(ctx.h, N, int(lognormal),
+                                                           C.c_uint64(coef_seed), int(dirichlet),
+                                                           _ptr(rs), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_mtx(cls, path: str, ctx: Optional[Context] = None) -> "SparseMatrix":
+        """sparse::load_matrix_market (sparse.cpp:140-192) into HBM."""
+        ctx = ctx or Context.default()
+        h = C.c_void_p()
+        ctx.check(lib().rkmf_matrix_load_mtx(ctx.h, os.fsencode(path), C.byref(h)))
+        return cls(ctx, h)
+
+    def export(self):
+        """(row_ptr int64, col_idx int32, values float64) host copies of the
+        device CSR (local numbering when partitioned)."""
+        rp = np.empty(self.n_rows + 1, np.int64)
+        ci = np.empty(self.nnz, np.int32)
+        v = np.empty(self.nnz, np.float64)
+        self.ctx.check(lib().rkmf_matrix_export(self.ctx.h, self.h, _ptr(rp), _ptr(ci), _ptr(v)))
+        return rp, ci, v
+
+    def save_mtx(self, path: str) -> None:
+        """sparse::save_matrix_market (sparse.cpp:194-211) of the device matrix."""
+        self.ctx.check(lib().rkmf_matrix_save_mtx(self.ctx.h, self.h, os.fsencode(path)))
 
     @classmethod
     def from_scipy(cls, A, ctx: Optional[Context] = None) -> "SparseMatrix":
@@ -447,6 +519,7 @@ def randomized_arnoldi(A: SparseMatrix, S: SketchOperator, b, m: int) -> KrylovD
     R = np.zeros((m, m + 1))  # column-major (m+1) x m
     sn, mk, bk = C.c_double(), C.c_int64(), C.c_int64()
     ctr = np.zeros(5, np.int64)
+    A.ctx.solves += 1
     A.ctx.check(lib().rkmf_randomized_arnoldi(A.ctx.h, A.h, S.h, bd.data_ptr(), m, W.data_ptr(),
                                               n, U.data_ptr(), _ptr(R), C.byref(sn), C.byref(mk),
                                               C.byref(bk), _ptr(ctr)))
@@ -514,6 +587,40 @@ class CycleRecord:
 
 
 @dataclass
+class CycleInfo:
+    """restart::CycleInfo (restart.hpp:42-54), host copies made for the
+    observer: W is the cycle's basis block as built (n x w_cols, column 0 =
+    start / alpha_k, one extra column when a next vector exists), R_accum the
+    accumulated compression (None when not kept), update = y_k, f_hat the
+    running approximation, alpha the global scale from cycle 1."""
+    cycle: int
+    W: np.ndarray
+    m_k: int
+    R_accum: Optional[np.ndarray]
+    update: np.ndarray
+    f_hat: np.ndarray
+    alpha: float
+
+
+def _observer_callback(fn):
+    def cb(_user, pinfo):
+        i = pinfo.contents
+        n, wc, M = int(i.n), int(i.w_cols), int(i.total_m)
+        W = np.ctypeslib.as_array(i.W, shape=(wc, n)).T.copy() if wc * n else np.zeros((n, wc))
+        R = (np.ctypeslib.as_array(i.R_accum, shape=(M, M)).T.copy()
+             if bool(i.R_accum) and M else None)
+        y = np.ctypeslib.as_array(i.update, shape=(n,)).copy()
+        f = np.ctypeslib.as_array(i.f_hat, shape=(n,)).copy()
+        try:
+            fn(CycleInfo(cycle=int(i.cycle), W=W, m_k=int(i.m_k), R_accum=R, update=y, f_hat=f,
+                         alpha=float(i.alpha)))
+        except Exception:  # noqa: BLE001 - an observer must not unwind through C
+            import traceback
+            traceback.print_exc()
+    return _OBSERVER_CB(cb)
+
+
+@dataclass
 class RestartResult:
     """restart::RestartResult (restart.hpp:56-65)."""
     f_hat: object
@@ -526,10 +633,19 @@ class RestartResult:
     solve_ms: float
     _ctx: Context = field(repr=False, default=None)
     _R: Optional[np.ndarray] = field(repr=False, default=None)
+    _solve_id: int = field(repr=False, default=-1)
 
     @property
     def R_accum(self) -> np.ndarray:
+        """The accumulated compression (restart.cpp:61-70), read from the
+        context's device buffer on first access. That buffer belongs to the
+        context's latest solve: after another solve on the same context the
+        property raises instead of returning the newer solve's matrix (pass
+        keep_R_accum=True to restarted_krylov to copy it out eagerly)."""
         if self._R is None:
+            if self._ctx is None or self._ctx.solves != self._solve_id:
+                raise Error("R_accum: the context has run another solve since this result; "
+                            "use restarted_krylov(..., keep_R_accum=True)")
             M = self.total_m
             R = np.zeros((M, M), order="F")
             tm = C.c_int64()
@@ -539,9 +655,12 @@ class RestartResult:
 
 
 def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions = None,
-                     S: SketchOperator = None, reference=None, out=None) -> RestartResult:
+                     S: SketchOperator = None, reference=None, out=None,
+                     keep_R_accum: bool = False, observer=None) -> RestartResult:
     """restart::restarted_krylov (restart.hpp:74-79): the randomized builder with a
     SketchOperator S, the classical builder (CGS2 on device) with S = None.
+    observer(CycleInfo) is the reference's test-only CycleObserver (device->host
+    copies every cycle; not for timed runs).
 
     b may be a numpy array (host: the host<->device copies are part of the call)
     or a CUDA tensor (device-resident); f_hat comes back in the same residency
@@ -571,10 +690,19 @@ def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions =
     cap = int(opts.k_max) + 1
     recs = (CycleRecordC * cap)()
     oc = opts.to_c()
-    ctx.check(lib().rkmf_restarted_krylov(ctx.h, A.h, S.h if S is not None else None, bptr, 1 if on_dev else 0, f.kind,
-                                          f.t, C.byref(oc), fptr, 1 if on_dev else 0,
-                                          _ptr(ref), C.byref(res), C.cast(recs, C.c_void_p),
-                                          cap))
+    ctx.solves += 1
+    cb = None
+    if observer is not None:  # test-only CycleObserver (restart.hpp:53)
+        cb = _observer_callback(observer)
+        ctx.check(lib().rkmf_context_set_observer(ctx.h, cb, None))
+    try:
+        ctx.check(lib().rkmf_restarted_krylov(ctx.h, A.h, S.h if S is not None else None, bptr,
+                                              1 if on_dev else 0, f.kind, f.t, C.byref(oc), fptr,
+                                              1 if on_dev else 0, _ptr(ref), C.byref(res),
+                                              C.cast(recs, C.c_void_p), cap))
+    finally:
+        if cb is not None:
+            lib().rkmf_context_set_observer(ctx.h, _OBSERVER_CB(), None)
     hist = []
     for i in range(res.n_records):
         r = recs[i]
@@ -582,12 +710,15 @@ def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions =
         if math.isnan(d["error_vs_reference"]):
             d["error_vs_reference"] = None
         hist.append(CycleRecord(**d))
-    return RestartResult(f_hat=fout, history=hist, converged=bool(res.converged), alpha=res.alpha,
+    out_res = RestartResult(f_hat=fout, history=hist, converged=bool(res.converged), alpha=res.alpha,
                          cycles=res.cycles, total_m=res.total_m,
                          counters=dict(matvecs=res.matvecs, dot_n=res.dot_n, dot_d=res.dot_d,
                                        basis_updates=res.basis_updates,
                                        peak_basis_cols=res.peak_basis_cols),
-                         solve_ms=res.solve_ms, _ctx=ctx)
+                         solve_ms=res.solve_ms, _ctx=ctx, _solve_id=ctx.solves)
+    if keep_R_accum:
+        _ = out_res.R_accum
+    return out_res
 
 
 # ---- multi-GPU: row-block partition ----
@@ -707,6 +838,65 @@ def partitioned_sketch(ctx: Context, d: int, n_global: int, zeta: int, seed: int
     return SketchOperator(ctx, h, d, n_local, zeta, seed)
 
 
+# ---- Matrix Market / vector interchange: sparse.cpp:140-242 (host only) ----
+def _io_check(code: int, err) -> None:
+    if code != RKMF_OK:
+        raise _CODE.get(code, Error)(err.value.decode(errors="replace"))
+
+
+def load_matrix_market(path: str):
+    """sparse::load_matrix_market: (row_ptr int64, col_idx int32, values, n_rows, n_cols)."""
+    nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+    rp, ci, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    err = C.create_string_buffer(1024)
+    _io_check(lib().rkmf_mtx_load(os.fsencode(path), C.byref(nr), C.byref(nc), C.byref(nz),
+                                  C.byref(rp), C.byref(ci), C.byref(v), err, 1024), err)
+    try:
+        n, k = nr.value, nz.value
+        out = (np.ctypeslib.as_array(C.cast(rp, C.POINTER(C.c_int64)), (n + 1,)).copy(),
+               np.ctypeslib.as_array(C.cast(ci, C.POINTER(C.c_int32)), (max(k, 1),))[:k].copy(),
+               np.ctypeslib.as_array(C.cast(v, C.POINTER(C.c_double)), (max(k, 1),))[:k].copy(),
+               n, nc.value)
+    finally:
+        for p in (rp, ci, v):
+            lib().rkmf_host_free(p)
+    return out
+
+
+def save_matrix_market(A, path: str) -> None:
+    """sparse::save_matrix_market of a SparseMatrix (device) or a host CSR
+    tuple (row_ptr, col_idx, values[, n_cols])."""
+    if isinstance(A, SparseMatrix):
+        A.save_mtx(path)
+        return
+    rp = np.ascontiguousarray(A[0], np.int64)
+    ci = np.ascontiguousarray(A[1], np.int32)
+    v = np.ascontiguousarray(A[2], np.float64)
+    nc = int(A[3]) if len(A) > 3 else len(rp) - 1
+    err = C.create_string_buffer(1024)
+    _io_check(lib().rkmf_mtx_save(os.fsencode(path), len(rp) - 1, nc, _ptr(rp), _ptr(ci), _ptr(v),
+                                  err, 1024), err)
+
+
+def load_vector(path: str) -> np.ndarray:
+    """sparse::load_vector (sparse.cpp:213-231)."""
+    n, p = C.c_int64(), C.c_void_p()
+    err = C.create_string_buffer(1024)
+    _io_check(lib().rkmf_vector_load(os.fsencode(path), C.byref(n), C.byref(p), err, 1024), err)
+    try:
+        k = n.value
+        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), (max(k, 1),))[:k].copy()
+    finally:
+        lib().rkmf_host_free(p)
+
+
+def save_vector(v, path: str) -> None:
+    """sparse::save_vector (sparse.cpp:233-242), %.17g per line."""
+    x = np.ascontiguousarray(v.cpu().numpy() if hasattr(v, "cpu") else v, np.float64)
+    err = C.create_string_buffer(1024)
+    _io_check(lib().rkmf_vector_save(os.fsencode(path), len(x), _ptr(x), err, 1024), err)
+
+
 # ---- synthetic inputs (host; need only the shared library, not a GPU) ----
 def _gen(fn, *args):
     n, nnz = C.c_int64(), C.c_int64()
@@ -762,7 +952,8 @@ def gen_gaussian(seed: int, n: int) -> np.ndarray:
 
 __all__ = ["Context", "SparseMatrix", "SketchOperator", "make_sketch", "spmv", "sketch_apply",
            "spmv_sketch", "randomized_arnoldi", "KrylovDecomposition", "FunctionSpec",
-           "RestartOptions", "RestartResult", "CycleRecord", "restarted_krylov", "gen_laplacian",
-           "gen_q1_hex", "gen_convdiff_upwind", "gen_gaussian", "Error", "ShapeError",
+           "RestartOptions", "RestartResult", "CycleRecord", "CycleInfo", "restarted_krylov", "gen_laplacian",
+           "gen_q1_hex", "gen_convdiff_upwind", "gen_gaussian", "load_matrix_market",
+           "save_matrix_market", "load_vector", "save_vector", "Error", "ShapeError",
            "ParameterError", "ParseError", "NumericalError", "DeviceError", "build", "lib",
            "SYMBOLS"]

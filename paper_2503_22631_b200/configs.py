@@ -13,6 +13,12 @@ Conventions (documented in DESIGN.md):
     fixed-seed, fixed-iteration power iteration (on A^T A when nonsymmetric),
     as the reference's acceptance test does (acceptance.cpp:429-437).
   * k_max = floor(budget_total_m / m) with the reference's budget 4000.
+
+Two interchangeable generator backends build the same arrays bit-for-bit
+(tests/test_generators.py): "product" (the library's host generators,
+csrc/problems.cpp) and "oracle" (oracle/problems_oracle.cpp, test
+infrastructure). bench.py's reference arm uses the oracle backend so that its
+process never maps the product library.
 """
 from __future__ import annotations
 
@@ -22,7 +28,6 @@ from typing import Optional
 
 import numpy as np
 
-from . import gen_convdiff_upwind, gen_gaussian, gen_laplacian, gen_q1_hex
 
 CONFIGS = {
     "cfg1": dict(kind="lap2d", N=256, fn="exp_neg", c=100.0, m=30, d=120, zeta=8, tol_rel=1e-8),
@@ -36,6 +41,54 @@ CONFIGS = {
 }
 BUDGET_TOTAL_M = 4000
 B_SEED, SKETCH_SEED, COEF_SEED = 1, 1, 1
+POWER_SEED, POWER_ITERS = 7, 60
+
+# ||A||_2 estimates of the full-size configs whose t comes from the power
+# iteration (60 fixed-seed iterations, power_norm2 / device_power_norm2),
+# computed once and frozen so that every process (both bench arms, the
+# device-generated problems) uses the same t without re-running a 117M- or
+# 3.6G-nonzero power iteration at start-up. tests/test_generators.py and
+# tests/test_gpu_fullsize.py recompute them.
+NORM2_FROZEN = {
+    ("cfg4", 256): 1046.860307424342,  # power_norm2 (A^T A), host scipy
+    ("cfg5", 512): None,
+}
+# ||b||_2 of the full-size cfg5 right-hand side (134M entries), so the
+# row-partitioned runs and the one-GPU run use one tol without a global
+# reduction at set-up (np.linalg.norm of gen_gaussian(B_SEED, 512^3)).
+BNORM_FROZEN = {
+    ("cfg5", 512): 11584.694751146742,
+}
+
+
+class _Gen:
+    """The generator backend: the product library's host generators or the
+    oracle's independent restatement (same arrays bit-for-bit)."""
+
+    def __init__(self, backend: str):
+        if backend not in ("product", "oracle"):
+            raise ValueError(f"unknown generator backend {backend!r}")
+        self.backend = backend
+
+    def _mod(self):
+        if self.backend == "product":
+            import paper_2503_22631_b200 as m
+            return m
+        from oracle import oracle as m
+        return m
+
+    def laplacian(self, dim, N):
+        return self._mod().gen_laplacian(dim, N)
+
+    def q1_hex(self, N, lognormal, seed, dirichlet):
+        return self._mod().gen_q1_hex(N, lognormal, seed, dirichlet)
+
+    def convdiff(self, N, peclet, v):
+        return self._mod().gen_convdiff_upwind(N, peclet, v)
+
+    def gaussian(self, seed, n):
+        m = self._mod()
+        return m.gen_gaussian(seed, n) if self.backend == "product" else m.gaussian_vector(seed, n)
 
 
 @dataclass
@@ -66,11 +119,12 @@ def lap_lambda_max(dim: int, N: int) -> float:
     return (4.0 * dim / (h * h)) * math.sin(N * math.pi / (2 * N + 2)) ** 2
 
 
-def power_norm2(rp, ci, v, n, symmetric: bool, iters: int = 60, seed: int = 7) -> float:
+def power_norm2(rp, ci, v, n, symmetric: bool, iters: int = POWER_ITERS, seed: int = POWER_SEED,
+                backend: str = "product") -> float:
     """Deterministic power iteration for ||A||_2 (host, scipy)."""
     import scipy.sparse as sp
     A = sp.csr_matrix((v, ci, rp), shape=(n, n))
-    x = gen_gaussian(seed, n)
+    x = _Gen(backend).gaussian(seed, n)
     x /= np.linalg.norm(x)
     lam = 0.0
     for _ in range(iters):
@@ -80,27 +134,46 @@ def power_norm2(rp, ci, v, n, symmetric: bool, iters: int = 60, seed: int = 7) -
     return lam if symmetric else math.sqrt(lam)
 
 
-def build(name: str, N: Optional[int] = None, with_b: bool = True) -> Problem:
-    """Build config `name`; N overrides the grid size (scaled-down parity cases)."""
+def frozen_norm2(name: str, N: int) -> Optional[float]:
+    return NORM2_FROZEN.get((name, int(N)))
+
+
+def frozen_tol(name: str, N: int) -> Optional[float]:
+    """tol_rel * ||b||_2 from BNORM_FROZEN, or None."""
+    bn = BNORM_FROZEN.get((name, int(N)))
+    return None if bn is None else CONFIGS[name]["tol_rel"] * bn
+
+
+def build(name: str, N: Optional[int] = None, with_b: bool = True,
+          backend: str = "product", frozen: bool = True) -> Problem:
+    """Build config `name`; N overrides the grid size (scaled-down parity
+    cases). backend: "product" or "oracle" generators (identical arrays).
+    frozen: use NORM2_FROZEN for ||A||_2 where recorded."""
     cfg = dict(CONFIGS[name])
     N = int(N or cfg["N"])
     kind = cfg["kind"]
+    G = _Gen(backend)
+    fz = frozen_norm2(name, N) if frozen else None
     if kind == "lap2d":
-        rp, ci, v = gen_laplacian(2, N)
+        rp, ci, v = G.laplacian(2, N)
         norm2 = lap_lambda_max(2, N)
     elif kind == "lap3d":
-        rp, ci, v = gen_laplacian(3, N)
+        rp, ci, v = G.laplacian(3, N)
         norm2 = lap_lambda_max(3, N)
     elif kind == "q1":
-        rp, ci, v = gen_q1_hex(N, cfg["lognormal"], COEF_SEED, cfg["dirichlet"])
-        norm2 = power_norm2(rp, ci, v, len(rp) - 1, True) if cfg["fn"] == "exp_neg" else 0.0
+        rp, ci, v = G.q1_hex(N, cfg["lognormal"], COEF_SEED, cfg["dirichlet"])
+        norm2 = 0.0
+        if cfg["fn"] == "exp_neg":
+            norm2 = fz if fz is not None else power_norm2(rp, ci, v, len(rp) - 1, True,
+                                                          backend=backend)
     elif kind == "convdiff":
-        rp, ci, v = gen_convdiff_upwind(N, cfg["peclet"], cfg["v"])
-        norm2 = power_norm2(rp, ci, v, len(rp) - 1, False)
+        rp, ci, v = G.convdiff(N, cfg["peclet"], cfg["v"])
+        norm2 = fz if fz is not None else power_norm2(rp, ci, v, len(rp) - 1, False,
+                                                      backend=backend)
     else:
         raise ValueError(kind)
     n = len(rp) - 1
-    b = gen_gaussian(B_SEED, n) if with_b else None
+    b = G.gaussian(B_SEED, n) if with_b else None
     t = cfg["c"] / norm2 if cfg["fn"] == "exp_neg" else 1.0
     tol = cfg["tol_rel"] * (float(np.linalg.norm(b)) if with_b else math.sqrt(n))
     return Problem(name=name, n=n, nnz=int(rp[-1]), row_ptr=rp, col_idx=ci, values=v, b=b,
@@ -221,8 +294,10 @@ def device_power_norm2(A, iters: int = 60, seed: int = 7) -> float:
 
 
 def build_device(name: str, N: Optional[int] = None, ctx=None) -> DeviceProblem:
-    """Config `name` generated on the device (Laplacians and Q1; cfg4's
-    upwind operator has no device generator and uses build())."""
+    """Config `name` generated in HBM (Laplacians, Q1, upwind
+    convection-diffusion: the host generators' entries bit-for-bit, the
+    lognormal Q1 coefficients to an ulp). tol uses the same ||b||_2 as build()
+    (numpy on the host copy) or BNORM_FROZEN."""
     from . import Context, SparseMatrix, gen_gaussian_device
     cfg = dict(CONFIGS[name])
     N = int(N or cfg["N"])
@@ -236,12 +311,19 @@ def build_device(name: str, N: Optional[int] = None, ctx=None) -> DeviceProblem:
         norm2 = lap_lambda_max(3, N)
     elif kind == "q1":
         A = SparseMatrix.q1_hex(N, cfg["lognormal"], COEF_SEED, cfg["dirichlet"], ctx)
-        norm2 = device_power_norm2(A) if cfg["fn"] == "exp_neg" else 0.0
+        norm2 = 0.0
+        if cfg["fn"] == "exp_neg":
+            norm2 = frozen_norm2(name, N) or device_power_norm2(A)
+    elif kind == "convdiff":
+        A = SparseMatrix.convdiff(N, cfg["peclet"], cfg["v"], ctx)
+        norm2 = frozen_norm2(name, N)
+        if norm2 is None:  # A^T A needs the transpose: build() on the host
+            norm2 = build(name, N, with_b=False).norm2
     else:
         raise ValueError(f"{name}: no device generator for {kind}")
     b = gen_gaussian_device(B_SEED, 0, A.n_rows, ctx)
     t = cfg["c"] / norm2 if cfg["fn"] == "exp_neg" else 1.0
+    tol = frozen_tol(name, N) or cfg["tol_rel"] * float(np.linalg.norm(b.cpu().numpy()))
     return DeviceProblem(name=name, n=A.n_rows, nnz=A.nnz, A=A, b=b, fn=cfg["fn"], t=t,
-                         m=cfg["m"], d=cfg["d"], zeta=cfg["zeta"],
-                         tol=cfg["tol_rel"] * float(b.norm()), k_max=BUDGET_TOTAL_M // cfg["m"],
-                         norm2=norm2)
+                         m=cfg["m"], d=cfg["d"], zeta=cfg["zeta"], tol=tol,
+                         k_max=BUDGET_TOTAL_M // cfg["m"], norm2=norm2)

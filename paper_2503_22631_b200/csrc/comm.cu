@@ -49,6 +49,12 @@ namespace {
 
 class NcclTransport final : public Transport {
  public:
+  int kind() const override { return 1; }
+  int comm_size() const override {
+    int n = 0;
+    RKMF_NCCL(ncclCommCount(comm_, &n));
+    return n;
+  }
   NcclTransport(int nranks, int rank, const ncclUniqueId& id) : me_(rank), p_(nranks) {
     RKMF_NCCL(ncclCommInitRank(&comm_, nranks, id, rank));
   }
@@ -80,6 +86,8 @@ class NcclTransport final : public Transport {
 
 class HostTransport final : public Transport {
  public:
+  int kind() const override { return 2; }
+  int comm_size() const override { return p_; }
   HostTransport(int nranks, int rank, const rkmf_host_comm& cb) : me_(rank), p_(nranks), cb_(cb) {}
   ~HostTransport() override {
     if (stage_) cudaFreeHost(stage_);
@@ -198,6 +206,36 @@ void comm_halo_exchange(rkmf_context* ctx, const rkmf_matrix* A, double* x) {
   }
   ctx->comm->alltoallv(h.sendbuf, h.send_off, h.send_cnt, x + h.n_local, h.recv_off, h.recv_cnt,
                        true, ctx->stream);
+}
+
+// Global norm1 = max column abs-sum (sparse.cpp:97-102) of a partitioned
+// matrix whose halo plan is set: local column sums, the halo parts returned
+// to their owners (the reverse of the halo exchange), max, allreduce(max).
+void partitioned_norm1(rkmf_context* ctx, rkmf_matrix* M) {
+  const HaloPlan& h = M->halo;
+  const int64_t n_local = h.n_local, n_halo = h.n_halo, nnz = M->view.nnz;
+  cudaStream_t st = ctx->stream;
+  Transport& T = *ctx->comm;
+  DevBuf cs, back, mx;
+  cs.ensure(sizeof(double) * size_t(n_local + n_halo + 1));
+  back.ensure(sizeof(double) * size_t(std::max<int64_t>(h.send_total, 1)));
+  mx.ensure(sizeof(double));
+  RKMF_CUDA(cudaMemsetAsync(cs.p, 0, sizeof(double) * size_t(n_local + n_halo + 1), st));
+  RKMF_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(double), st));
+  if (nnz > 0)
+    colsum_abs_kernel<<<blocks_for(nnz), 256, 0, st>>>(nnz, M->col, M->val, cs.as<double>());
+  T.alltoallv(cs.as<double>() + n_local, h.recv_off, h.recv_cnt, back.p, h.send_off, h.send_cnt,
+              true, st);
+  if (h.send_total > 0)
+    scatter_add_kernel<<<blocks_for(h.send_total), 256, 0, st>>>(h.send_total, h.send_idx,
+                                                                  back.as<double>(), cs.as<double>());
+  if (n_local > 0)
+    max_abs_kernel<<<blocks_for(n_local), 256, 0, st>>>(n_local, cs.as<double>(), mx.as<double>());
+  RKMF_CUDA(cudaGetLastError());
+  T.allreduce(mx.as<double>(), 1, true, st);
+  RKMF_CUDA(cudaMemcpyAsync(&M->norm1, mx.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  RKMF_CUDA(cudaStreamSynchronize(st));
+  ctx->launches += 3;
 }
 
 }  // namespace rkmf_b200
@@ -356,37 +394,87 @@ int rkmf_matrix_create_partitioned(rkmf_context* ctx, int64_t n_global, const in
         if (h.send_total > 0)
           RKMF_CUDA(cudaMemcpyAsync(h.send_idx, sl.data(), sizeof(int32_t) * size_t(h.send_total),
                                     cudaMemcpyHostToDevice, st));
-        // 3) global norm1 = max column abs-sum (sparse.cpp:97-102): local column
-        //    sums, the halo parts returned to their owners (the reverse of the
-        //    halo exchange), max, allreduce(max)
-        DevBuf cs, back, mx;
-        cs.ensure(sizeof(double) * size_t(n_local + n_halo + 1));
-        back.ensure(sizeof(double) * size_t(std::max<int64_t>(h.send_total, 1)));
-        mx.ensure(sizeof(double));
-        RKMF_CUDA(cudaMemsetAsync(cs.p, 0, sizeof(double) * size_t(n_local + n_halo + 1), st));
-        RKMF_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(double), st));
-        if (nnz > 0)
-          colsum_abs_kernel<<<blocks_for(nnz), 256, 0, st>>>(nnz, M->col, M->val, cs.as<double>());
-        T.alltoallv(cs.as<double>() + n_local, h.recv_off, h.recv_cnt, back.p, h.send_off,
-                    h.send_cnt, true, st);
-        if (h.send_total > 0)
-          scatter_add_kernel<<<blocks_for(h.send_total), 256, 0, st>>>(h.send_total, h.send_idx,
-                                                                        back.as<double>(),
-                                                                        cs.as<double>());
-        if (n_local > 0)
-          max_abs_kernel<<<blocks_for(n_local), 256, 0, st>>>(n_local, cs.as<double>(),
-                                                              mx.as<double>());
-        RKMF_CUDA(cudaGetLastError());
-        T.allreduce(mx.as<double>(), 1, true, st);
-        RKMF_CUDA(cudaMemcpyAsync(&M->norm1, mx.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-        RKMF_CUDA(cudaStreamSynchronize(st));
-        ctx->launches += 3;
+        partitioned_norm1(ctx, M);
       }
     } catch (...) {
       rkmf_matrix_destroy(M);
       throw;
     }
     *out = M;
+  });
+}
+
+// Rows of the Q1 matrix on N^3 nodes (BASELINE cfg3/cfg5) generated in HBM
+// for this rank's plane-aligned block: the same local rows,
+// local column numbering [owned | lower plane | upper plane] and halo plan
+// that rkmf_matrix_create_partitioned builds from host CSR (rkmf_partition_halo),
+// without a host copy of the 27-point matrix. row_starts must be strictly
+// increasing multiples of N^2 (every rank owns whole x-planes), so the halo
+// is exactly the x-plane below (owned by rank - 1) and above (rank + 1).
+int rkmf_matrix_gen_q1_hex_partitioned(rkmf_context* ctx, int64_t N, int32_t lognormal,
+                                       uint64_t coef_seed, int32_t dirichlet,
+                                       const int64_t* row_starts, rkmf_matrix** out) {
+  return guarded_c(ctx, [&] {
+    RKMF_CUDA(cudaSetDevice(ctx->device));
+    const int P = ctx->nranks, me = ctx->rank;
+    if (P > 1 && !ctx->comm) param_error("partitioned matrix: initialise the communicator first");
+    if (N < 2) param_error("gen_q1_hex: N must be >= 2");
+    const int64_t plane = N * N, n = N * N * N;
+    if (row_starts[0] != 0 || row_starts[P] != n) shape_error("partition: bad row_starts");
+    for (int q = 0; q < P; ++q)
+      if (row_starts[q + 1] <= row_starts[q] || row_starts[q + 1] % plane != 0)
+        param_error("gen_q1_hex_partitioned: row_starts must be increasing multiples of N^2");
+    const int64_t rb = row_starts[me], re = row_starts[me + 1], n_local = re - rb;
+    const int64_t nlo = me > 0 ? plane : 0, nhi = me < P - 1 ? plane : 0;
+    rkmf_matrix* M = gen_q1_rows(ctx, N, lognormal, coef_seed, dirichlet, rb, re, nlo, nhi);
+    try {
+      HaloPlan& h = M->halo;
+      M->partitioned = true;
+      h.n_global = n;
+      h.row_begin = rb;
+      h.n_local = n_local;
+      h.n_halo = nlo + nhi;
+      h.recv_cnt.assign(size_t(P), 0);
+      h.send_cnt.assign(size_t(P), 0);
+      if (me > 0) h.recv_cnt[size_t(me - 1)] = h.send_cnt[size_t(me - 1)] = plane;
+      if (me < P - 1) h.recv_cnt[size_t(me + 1)] = h.send_cnt[size_t(me + 1)] = plane;
+      h.recv_off.assign(size_t(P), 0);
+      h.send_off.assign(size_t(P), 0);
+      for (int q = 1; q < P; ++q) {
+        h.recv_off[q] = h.recv_off[q - 1] + h.recv_cnt[q - 1];
+        h.send_off[q] = h.send_off[q - 1] + h.send_cnt[q - 1];
+      }
+      h.send_total = h.send_off[P - 1] + h.send_cnt[P - 1];
+      if (P > 1) {
+        // my first plane goes to rank - 1, my last plane to rank + 1 (rank order)
+        std::vector<int32_t> sl;
+        sl.reserve(size_t(h.send_total));
+        if (me > 0)
+          for (int64_t i = 0; i < plane; ++i) sl.push_back(int32_t(i));
+        if (me < P - 1)
+          for (int64_t i = n_local - plane; i < n_local; ++i) sl.push_back(int32_t(i));
+        RKMF_CUDA(cudaMalloc(&h.send_idx, sizeof(int32_t) * size_t(std::max<int64_t>(h.send_total, 1))));
+        RKMF_CUDA(cudaMalloc(&h.sendbuf, sizeof(double) * size_t(std::max<int64_t>(h.send_total, 1))));
+        RKMF_CUDA(cudaMemcpy(h.send_idx, sl.data(), sizeof(int32_t) * sl.size(),
+                             cudaMemcpyHostToDevice));
+        partitioned_norm1(ctx, M);
+      }
+    } catch (...) {
+      rkmf_matrix_destroy(M);
+      throw;
+    }
+    *out = M;
+  });
+}
+
+int rkmf_context_comm_info(const rkmf_context* ctx, int32_t* nranks, int32_t* rank,
+                           int32_t* transport) {
+  if (!ctx) return RKMF_PARAMETER_ERROR;
+  return guarded_c(const_cast<rkmf_context*>(ctx), [&] {
+    const Transport* T = ctx->comm;
+    if (nranks) *nranks = T ? T->comm_size() : ctx->nranks;
+    if (rank) *rank = ctx->rank;
+    if (transport) *transport = T ? T->kind() : 0;
   });
 }
 

@@ -474,7 +474,7 @@ void dense_expneg_e1(const double* R, int64_t ldr, int64_t N, double t, int s, d
   const dim3 gg(unsigned((N + kT - 1) / kT), unsigned((N + kT - 1) / kT));
   const double scale = -t * std::ldexp(1.0, -s);
   dense_scale_kernel<<<grid_for(NN), 256, 0, st>>>(R, ldr, N, scale, A);
-  static const int g16 = [] { const char* e = getenv("RKMF_DGEMM16"); return e ? atoi(e) : 1; }();
+  static const int g16 = [] { const char* e = knob_env("RKMF_DGEMM16"); return e ? atoi(e) : 1; }();
   const dim3 g16g(unsigned((N + kT16 - 1) / kT16), unsigned((N + kT16 - 1) / kT16));
   auto gemm = [&](const double* X, const double* Y, double* Z, double e0, double e1,
                   const double* P1, double e2, const double* P2, double e3, const double* P3) {

@@ -12,11 +12,17 @@
 // (and issued a tile ahead: they do not depend on the streamed values).
 // Slots where the CSR row has no entry hold 0.0, and each row's entries keep
 // the CSR's column order, so z = A x is bit-identical to the CSR kernel (a
-// padding term adds exactly 0.0).
+// padding term adds exactly 0.0). The one exception: a row-partitioned rank's
+// local columns (partition.cpp) put the halo of a lower rank past the owned
+// columns (local index n_local + pos), so that entry comes first in the CSR
+// row and last among the sorted offsets; those boundary rows then sum in a
+// different order than the CSR kernel (rounding-level differences only).
 //
 // Eligibility (checked on device, one pass over the nonzeros): at most
 // kMaxDiag = 8 distinct offsets per 128-row tile (27-point stencils stay on the CSR kernel,
-// which splits their rows over two threads and measured faster), columns strictly increasing within each row, and
+// which splits their rows over two threads and measured faster), no repeated column
+// within a row (validated matrices have strictly increasing columns; partition-local ones
+// may not be monotone, see above), and
 // the padded DIA stream smaller than 0.85x the CSR stream. Otherwise the matrix
 // keeps the CSR path only. RKMF_DIA=0 disables the copy at creation;
 // rkmf_matrix_dia() drops or (re)builds it.
@@ -39,8 +45,7 @@ constexpr int32_t kEmpty = INT_MIN;
 // One block (128 threads = the tile's rows) per tile: the distinct column
 // offsets of the tile's rows, sorted, into toff[tile][kMaxDiag] (slots past
 // the tile's count repeat its largest offset: a duplicate slot keeps 0.0
-// values and adds an exact zero). flags[0]: a row's columns are not strictly
-// increasing; flags[1]: a tile has more than kMaxDiag offsets; flags[2]: the
+// values and adds an exact zero). flags[0]: a row repeats a column; flags[1]: a tile has more than kMaxDiag offsets; flags[2]: the
 // largest per-tile count.
 template <typename RP>
 __global__ void dia_tile_offsets_kernel(int64_t n, const RP* __restrict__ rp,
@@ -58,7 +63,9 @@ __global__ void dia_tile_offsets_kernel(int64_t n, const RP* __restrict__ rp,
     int32_t prev = -1;
     for (int64_t e = lo; e < hi; ++e) {
       const int32_t c = ci[e];
-      if (c <= prev) atomicExch(flags + 0, 1);
+      if (c <= prev)  // not monotone (a partition-local row): look for a repeat
+        for (int64_t f = lo; f < e; ++f)
+          if (ci[f] == c) atomicExch(flags + 0, 1);
       prev = c;
       const int32_t o = int32_t(int64_t(c) - row);
       bool done = false;
@@ -104,10 +111,10 @@ __global__ void dia_fill_kernel(int64_t n, const RP* __restrict__ rp,
     const int32_t* offs = toff + tile * stride;
     double* base = dval + tile * int64_t(nd) * kTileRows + r;
     const int64_t lo = int64_t(rp[row]), hi = int64_t(rp[row + 1]);
-    int q = 0;
-    for (int64_t e = lo; e < hi; ++e) {  // columns increase, so offsets do too
+    for (int64_t e = lo; e < hi; ++e) {
       const int32_t o = int32_t(int64_t(ci[e]) - row);
-      while (offs[q] != o) ++q;
+      int q = 0;
+      while (offs[q] != o) ++q;  // present: the offsets kernel collected it
       base[int64_t(q) * kTileRows] = val[e];
     }
   }
@@ -215,7 +222,7 @@ void build_dia(rkmf_matrix* M) {
 bool dia_enabled_by_env() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_DIA");
+    const char* e = knob_env("RKMF_DIA");
     v = e ? (atoi(e) != 0) : 1;
   }
   return v != 0;

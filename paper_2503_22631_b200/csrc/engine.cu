@@ -29,23 +29,10 @@
 using namespace rkmf_b200;
 
 namespace rkmf_b200 {
-// RKMF_ROWSKETCH=1: build the coloured row-major sketch layout and run the
-// row-sketch K2 (spmv_rowsketch.cu). Off by default: at parity with the
-// warp-specialised K2 on cfg2 (39.9 vs 40.2 us b2b, 47.5 vs 47.3 us in the
-// solve) for 9 more bytes per row and a slower setup.
-bool rowsketch_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("RKMF_ROWSKETCH");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 bool pdl_enabled() {  // RKMF_PDL=0 launches the step kernels without PDL
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_PDL");
+    const char* e = knob_env("RKMF_PDL");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -130,7 +117,7 @@ double host_norm(const double* x, int64_t n) {
 
 struct SolveBuffers {
   int64_t n, n_global, d, m_eff, ldw, ldr;
-  double *W, *U, *Rbar, *G, *z, *pacc, *sacc;
+  double *W, *U, *Rbar, *G, *z;
 };
 
 // n: local rows; n_ext: local rows + halo columns (W columns carry the halo
@@ -150,10 +137,7 @@ SolveBuffers prepare(rkmf_context* ctx, int64_t n, int64_t n_ext, int64_t n_glob
   b.Rbar = static_cast<double*>(ctx->Rbar.ensure(sizeof(double) * size_t(b.ldr) * size_t(m_eff)));
   b.G = static_cast<double*>(ctx->gram.ensure(sizeof(double) * size_t(b.ldr) * size_t(b.ldr)));
   b.z = static_cast<double*>(ctx->z.ensure(sizeof(double) * size_t(b.ldw)));
-  b.pacc = static_cast<double*>(ctx->pacc.ensure(sizeof(double) * size_t(d)));
-  b.sacc = static_cast<double*>(ctx->sacc.ensure(sizeof(double) * size_t(d)));
-  RKMF_CUDA(cudaMemsetAsync(b.pacc, 0, sizeof(double) * size_t(d), ctx->stream));
-  RKMF_CUDA(cudaMemsetAsync(b.sacc, 0, sizeof(double) * size_t(d), ctx->stream));
+  ctx->ensure_red(d);
   RKMF_CUDA(cudaMemsetAsync(b.Rbar, 0, sizeof(double) * size_t(b.ldr) * size_t(m_eff), ctx->stream));
   RKMF_CUDA(cudaMemsetAsync(ctx->st_dev, 0, sizeof(SolveState), ctx->stream));
   return b;
@@ -174,6 +158,19 @@ void check_builder_args(const rkmf_matrix* A, const rkmf_sketch* S, int64_t m) {
   if (S->d < need) param_error("randomized_arnoldi: sketch dimension d too small for m");
 }
 
+// The sketch of one launch for its consumer: on one rank, the group partials
+// as written (the consumer sums them in group order); partitioned, the ranks'
+// sums must be added, so the groups are summed on device first (a one-block
+// kernel, fixed order) and the d doubles allreduced.
+SketchSum sketch_allreduce(rkmf_context* ctx, const DetRed& red, int64_t d, DevBuf& fin) {
+  if (!ctx->comm || ctx->nranks <= 1) return SketchSum{red.gpart, red.groups};
+  double* out = static_cast<double*>(fin.ensure(sizeof(double) * size_t(d)));
+  launch_det_finish(red, d, out, ctx->stream);
+  ctx->launches++;
+  comm_allreduce_sum(ctx, out, size_t(d));
+  return SketchSum{out, 1};
+}
+
 // The m_eff steps of one cycle (basis.cpp:119-139). fuse_last: leave the
 // last basis update to final_update (K5).
 void run_steps(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
@@ -181,16 +178,18 @@ void run_steps(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
   const SketchView sv = S->view();
   const int grid = spmv_sketch_grid(&A->view, &sv, 1);
   int32_t* stop = &ctx->st_dev->stopped;
+  DetRed& red = ctx->red_sketch(b.d);
   for (int64_t k = 0; k < b.m_eff; ++k) {
     double* x = b.W + k * b.ldw;
     comm_halo_exchange(ctx, A, x);  // multi-GPU: off-rank x entries into the halo tail
     ctx->timed(0, [&] {
       launch_spmv_sketch(&A->view, &sv, 1, x, k == 0 ? &ctx->st_dev->sigma : nullptr, b.z,
-                         b.pacc, stop, int(k), grid, ctx->stream);
+                         stop, int(k), grid, red, ctx->stream);
     });
-    comm_allreduce_sum(ctx, b.pacc, size_t(b.d));  // sum of the ranks' sketch partials
+    const SketchSum p = sketch_allreduce(ctx, red, b.d, ctx->pfin_sk);
     ctx->timed(1, [&] {
-      launch_rgs_step(b.d, int(k), b.ldr, b.n_global, tol, b.pacc, b.U, b.Rbar, b.G, b.ldr,
+      launch_rgs_step(b.d, int(k), b.ldr, b.n_global, tol, p.part, p.groups, b.U, b.Rbar,
+                      b.G, b.ldr,
                       ctx->st_dev,
                       ctx->stream);
     });
@@ -221,8 +220,9 @@ void run_steps_classical(rkmf_context* ctx, const rkmf_matrix* A, const SolveBuf
     double* x = b.W + k * b.ldw;
     comm_halo_exchange(ctx, A, x);
     ctx->timed(0, [&] {
+      DetRed none;  // mode 0: no sketch
       launch_spmv_sketch(&A->view, nullptr, 0, x, k == 0 ? &ctx->st_dev->sigma : nullptr, b.z,
-                         nullptr, stop, int(k), grid, st);
+                         stop, int(k), grid, none, st);
     });
     ctx->timed(1, [&] { launch_cl_multidot(b.n, int(k), b.ldw, b.W, b.z, h1, ctx->st_dev, st); });
     comm_allreduce_sum(ctx, h1, size_t(k + 1));
@@ -262,14 +262,16 @@ void start_classical(rkmf_context* ctx, const SolveBuffers& b, double* cl, bool 
   ctx->launches += 2;
 }
 
+// S * start (basis.cpp:103-104) into the start-sketch group partials
+// (ctx->red_st), summed by start_init
 void start_sketch(rkmf_context* ctx, const rkmf_sketch* S, const SolveBuffers& b) {
   const SketchView sv = S->view();
+  DetRed& red = ctx->red_start(b.d);
   ctx->timed(5, [&] {
-    launch_spmv_sketch(nullptr, &sv, 2, b.W, nullptr, nullptr, b.sacc, nullptr, 0, 0,
-                       ctx->stream);
+    launch_spmv_sketch(nullptr, &sv, 2, b.W, nullptr, nullptr, nullptr, 0, 0, red, ctx->stream);
   });
   ctx->launches++;
-  comm_allreduce_sum(ctx, b.sacc, size_t(b.d));
+  ctx->start_sum = sketch_allreduce(ctx, red, b.d, ctx->pfin_st);
 }
 
 void copy_in(rkmf_context* ctx, double* dst, const double* src, int64_t n, bool on_device) {
@@ -377,7 +379,7 @@ int rkmf_context_destroy(rkmf_context* ctx) {
   if (!ctx) return RKMF_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->z, &ctx->pacc, &ctx->sacc, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
+  for (DevBuf* b : {&ctx->redbuf, &ctx->pfin_sk, &ctx->pfin_st, &ctx->z, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
                     &ctx->ws, &ctx->u, &ctx->g, &ctx->fhat, &ctx->ref, &ctx->partial,
                     &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch, &ctx->gram,
                     &ctx->cl, &ctx->diag})
@@ -555,6 +557,76 @@ int rkmf_matrix_dia(rkmf_matrix* M, int enable, int* ndiag) {
   });
 }
 
+int rkmf_matrix_export(rkmf_context* ctx, const rkmf_matrix* M, int64_t* h_rp, int32_t* h_ci,
+                       double* h_v) {
+  if (!M) return RKMF_PARAMETER_ERROR;
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    const CsrView& v = M->view;
+    const int64_t n = v.n_rows, nnz = v.nnz;
+    cudaStream_t st = ctx->stream;
+    if (h_rp) {
+      if (v.rp64) {
+        RKMF_CUDA(cudaMemcpyAsync(h_rp, v.row_ptr, sizeof(int64_t) * size_t(n + 1),
+                                  cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+      } else {
+        std::vector<int32_t> r32(size_t(n + 1));
+        RKMF_CUDA(cudaMemcpyAsync(r32.data(), v.row_ptr, sizeof(int32_t) * size_t(n + 1),
+                                  cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+        for (int64_t i = 0; i <= n; ++i) h_rp[i] = r32[size_t(i)];
+      }
+    }
+    if (h_ci && nnz > 0)
+      RKMF_CUDA(cudaMemcpyAsync(h_ci, v.col, sizeof(int32_t) * size_t(nnz), cudaMemcpyDeviceToHost, st));
+    if (h_v && nnz > 0)
+      RKMF_CUDA(cudaMemcpyAsync(h_v, v.val, sizeof(double) * size_t(nnz), cudaMemcpyDeviceToHost, st));
+    RKMF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int rkmf_matrix_load_mtx(rkmf_context* ctx, const char* path, rkmf_matrix** out) {
+  return guarded(ctx, [&] {
+    set_device(ctx);
+    int64_t nr = 0, nc = 0, nnz = 0;
+    int64_t* rp = nullptr;
+    int32_t* ci = nullptr;
+    double* v = nullptr;
+    char err[512] = {0};
+    const int code = rkmf_mtx_load(path, &nr, &nc, &nnz, &rp, &ci, &v, err, sizeof(err));
+    if (code != RKMF_OK) throw Error(code, err);
+    try {
+      *out = create_matrix_host(ctx, nr, nc, rp, ci, v, true);
+    } catch (...) {
+      rkmf_host_free(rp);
+      rkmf_host_free(ci);
+      rkmf_host_free(v);
+      throw;
+    }
+    rkmf_host_free(rp);
+    rkmf_host_free(ci);
+    rkmf_host_free(v);
+  });
+}
+
+int rkmf_matrix_save_mtx(rkmf_context* ctx, const rkmf_matrix* M, const char* path) {
+  if (!M) return RKMF_PARAMETER_ERROR;
+  return guarded(ctx, [&] {
+    if (M->partitioned) param_error("save_matrix_market: partitioned matrices hold local rows only");
+    const int64_t n = M->view.n_rows, nnz = M->view.nnz;
+    std::vector<int64_t> rp(size_t(n + 1));
+    std::vector<int32_t> ci(size_t(std::max<int64_t>(nnz, 1)));
+    std::vector<double> v(size_t(std::max<int64_t>(nnz, 1)));
+    const int code = rkmf_matrix_export(ctx, M, rp.data(), ci.data(), v.data());
+    if (code != RKMF_OK) throw Error(code, ctx->last_error);
+    char err[512] = {0};
+    const int c2 = rkmf_mtx_save(path, n, M->view.n_cols, rp.data(), ci.data(), v.data(), err,
+                                 sizeof(err));
+    if (c2 != RKMF_OK) throw Error(c2, err);
+  });
+}
+
 int rkmf_matrix_info(const rkmf_matrix* M, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
                      double* norm1) {
   if (!M) return RKMF_PARAMETER_ERROR;
@@ -607,20 +679,6 @@ int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_globa
       launch_sketch_generate(d, n, col_begin, zeta, seed, S->rows, S->signs, ctx->stream);
       launch_sketch_tiles(d, n, zeta, S->rows, S->signs, S->tile_off, S->tile_ent, ctx->stream);
       ctx->launches += 2;
-      if (zeta == 8 && d <= 255 && rowsketch_enabled()) {  // one allocation: rbin | sbit
-        const int64_t tiles_pad = tiles * kTileRows + kTileRows;
-        const size_t bytes = size_t(round_up(tiles_pad * 8, 256) + round_up(tiles_pad, 256) +
-                                    tiles_pad / 32 + 256);
-        void* rb = nullptr;
-        RKMF_CUDA(cudaMalloc(&rb, bytes));
-        RKMF_CUDA(cudaMemsetAsync(rb, 0, bytes, ctx->stream));
-        S->rbin = static_cast<uint8_t*>(rb);
-        S->sbit = S->rbin + round_up(tiles_pad * 8, 256);
-        S->wslow = S->sbit + round_up(tiles_pad, 256);
-        launch_sketch_rowbins(n, int(d), S->rows, S->signs, S->rbin, S->sbit, S->wslow,
-                              ctx->stream);
-        ctx->launches++;
-      }
       RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
       if (S->rows) cudaFree(S->rows);
@@ -639,7 +697,6 @@ int rkmf_sketch_destroy(rkmf_sketch* S) {
   cudaFree(S->rows);
   cudaFree(S->signs);
   cudaFree(S->tile_off);  // also holds tile_ent
-  if (S->rbin) cudaFree(S->rbin);  // also holds sbit
   delete S;
   return RKMF_OK;
 }
@@ -676,7 +733,8 @@ int rkmf_sketch_export(rkmf_context* ctx, const rkmf_sketch* S, int64_t* h_rows,
 int rkmf_spmv(rkmf_context* ctx, const rkmf_matrix* A, const double* d_x, double* d_y) {
   return guarded(ctx, [&] {
     set_device(ctx);
-    launch_spmv_sketch(&A->view, nullptr, 0, d_x, nullptr, d_y, nullptr, nullptr, 0, 0,
+    DetRed none;
+    launch_spmv_sketch(&A->view, nullptr, 0, d_x, nullptr, d_y, nullptr, 0, 0, none,
                        ctx->stream);
     ctx->launches++;
     RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -687,9 +745,10 @@ int rkmf_sketch_apply(rkmf_context* ctx, const rkmf_sketch* S, const double* d_x
   return guarded(ctx, [&] {
     set_device(ctx);
     const SketchView sv = S->view();
-    RKMF_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * size_t(S->d), ctx->stream));
-    launch_spmv_sketch(nullptr, &sv, 2, d_x, nullptr, nullptr, d_y, nullptr, 0, 0, ctx->stream);
-    ctx->launches++;
+    DetRed& red = ctx->red_start(S->d);
+    launch_spmv_sketch(nullptr, &sv, 2, d_x, nullptr, nullptr, nullptr, 0, 0, red, ctx->stream);
+    launch_det_finish(red, S->d, d_y, ctx->stream);
+    ctx->launches += 2;
     RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -700,15 +759,16 @@ int rkmf_spmv_sketch(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch*
     set_device(ctx);
     if (S->n != A->view.n_rows) shape_error("spmv_sketch: sketch width mismatch");
     const SketchView sv = S->view();
-    RKMF_CUDA(cudaMemsetAsync(d_p, 0, sizeof(double) * size_t(S->d), ctx->stream));
-    launch_spmv_sketch(&A->view, &sv, 1, d_x, nullptr, d_z, d_p, nullptr, 0, 0, ctx->stream);
-    ctx->launches++;
+    DetRed& red = ctx->red_sketch(S->d);
+    launch_spmv_sketch(&A->view, &sv, 1, d_x, nullptr, d_z, nullptr, 0, 0, red, ctx->stream);
+    launch_det_finish(red, S->d, d_p, ctx->stream);
+    ctx->launches += 2;
     RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 
 bool flush_l2_between() {  // RKMF_BENCH_FLUSH=1: kernel_bench flushes L2 between launches
-  const char* e = getenv("RKMF_BENCH_FLUSH");
+  const char* e = knob_env("RKMF_BENCH_FLUSH");
   return e && e[0] == '1';
 }
 
@@ -723,10 +783,11 @@ int rkmf_kernel_bench(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch
     if (S) sv = S->view();
     const SketchView* svp = mode == 0 ? nullptr : &sv;
     const int grid = spmv_sketch_grid(mode == 2 ? nullptr : &A->view, svp, mode);
-    if (mode != 0) RKMF_CUDA(cudaMemsetAsync(d_p, 0, sizeof(double) * size_t(S->d), ctx->stream));
+    DetRed none;
+    DetRed& red = mode == 0 ? none : ctx->red_sketch(S->d);
     auto launch = [&] {
-      launch_spmv_sketch(mode == 2 ? nullptr : &A->view, svp, mode, d_x, nullptr, d_z, d_p,
-                         nullptr, 0, grid, ctx->stream);
+      launch_spmv_sketch(mode == 2 ? nullptr : &A->view, svp, mode, d_x, nullptr, d_z, nullptr,
+                         0, grid, red, ctx->stream);
     };
     launch();  // warm-up
     if (flush_l2_between()) {  // cold-L2 variant: a 256 MB write between timed launches
@@ -755,6 +816,11 @@ int rkmf_kernel_bench(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch
       *avg_ms = double(ms) / reps;
     }
     ctx->launches += reps + 1;
+    if (mode != 0) {  // the last launch's sketch as a plain d-vector
+      launch_det_finish(red, S->d, d_p, ctx->stream);
+      ctx->launches++;
+      RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
   });
 }
 
@@ -770,7 +836,8 @@ int rkmf_randomized_arnoldi(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_
     SolveBuffers b = prepare(ctx, n, A->view.n_cols, A->n_rows_global(), S->d, m);
     copy_in(ctx, b.W, d_b, n, true);
     start_sketch(ctx, S, b);
-    launch_start_init_m(b.d, b.sacc, b.U, ctx->st_dev, true, int(m), ctx->stream);
+    launch_start_init_m(b.d, ctx->start_sum.part, ctx->start_sum.groups, b.U, ctx->st_dev, true,
+                        int(m), ctx->stream);
     ctx->launches++;
     ctx->sync_state();
     if (ctx->st_host->zero_start)  // basis.cpp:105-106
@@ -959,7 +1026,8 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
         start_classical(ctx, bb, cl, k == 1);
       } else {
         ctx->timed(5, [&] {
-          launch_start_init_m(bb.d, bb.sacc, bb.U, ctx->st_dev, k == 1, int(m_eff), st);
+          launch_start_init_m(bb.d, ctx->start_sum.part, ctx->start_sum.groups, bb.U, ctx->st_dev,
+                              k == 1, int(m_eff), st);
         });
         ctx->launches++;
       }
@@ -1075,11 +1143,24 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
         }
       }
       RKMF_CUDA(cudaEventRecord(ctx->event(ce.e2), st));
+      // observer (test-only): the basis block as built and f_hat before K5
+      // overwrites column 0 with the next start vector
+      std::vector<double> obs_W, obs_f0;
+      if (ctx->observer) {
+        obs_W.assign(size_t(n) * size_t(m_eff + 1), 0.0);
+        obs_f0.assign(size_t(n), 0.0);
+        RKMF_CUDA(cudaMemcpy2DAsync(obs_W.data(), sizeof(double) * size_t(n), bb.W,
+                                    sizeof(double) * size_t(bb.ldw), sizeof(double) * size_t(n),
+                                    size_t(m_eff), cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaMemcpyAsync(obs_f0.data(), fhat, sizeof(double) * size_t(n),
+                                  cudaMemcpyDeviceToHost, st));
+        RKMF_CUDA(cudaStreamSynchronize(st));
+      }
       ctx->timed(4, [&] {
         // classical: the last step left z' and (h2, beta) in rlast
         launch_final_update(n, int(m_eff), bb.ldw, bb.W, bb.z,
                             classical ? cl + 2 * bb.ldr + 2 : bb.Rbar, bb.ldr, g, fhat, ref_dev,
-                            ctx->st_dev, st);
+                            ctx->st_dev, ctx->red_update(), st);
       });
       ctx->launches++;
       comm_allreduce_sum(ctx, &ctx->st_dev->yn2, 2);  // global ||y||^2, ||f - ref||^2
@@ -1125,6 +1206,39 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       if (first_update < 0.0) first_update = yn;
       else if (yn > opts.divergence_factor * first_update)
         numerical_error("restart divergence (cycle " + std::to_string(k) + ")");
+      if (ctx->observer) {  // restart.cpp:91-92
+        std::vector<double> fh, Rh;
+        fh.resize(size_t(n));
+        const int64_t wc = next ? mk + 1 : mk;
+        if (next)  // w_m, the next start vector, now in column 0
+          RKMF_CUDA(cudaMemcpy(obs_W.data() + size_t(mk) * size_t(n), bb.W,
+                               sizeof(double) * size_t(n), cudaMemcpyDeviceToHost));
+        RKMF_CUDA(cudaMemcpy(fh.data(), fhat, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) {
+          obs_W[size_t(i)] /= h.alpha_k;  // column 0 holds the unscaled start
+          obs_f0[size_t(i)] = fh[size_t(i)] - obs_f0[size_t(i)];
+        }
+        const int64_t Mk = M + mk;
+        const bool have_R = Racc != nullptr && ldR >= Mk;
+        if (have_R) {
+          Rh.resize(size_t(Mk) * size_t(Mk));
+          RKMF_CUDA(cudaMemcpy2D(Rh.data(), sizeof(double) * size_t(Mk), Racc,
+                                 sizeof(double) * size_t(ldR), sizeof(double) * size_t(Mk),
+                                 size_t(Mk), cudaMemcpyDeviceToHost));
+        }
+        rkmf_cycle_info info;
+        info.cycle = k;
+        info.n = n;
+        info.m_k = mk;
+        info.w_cols = wc;
+        info.W = obs_W.data();
+        info.total_m = Mk;
+        info.R_accum = have_R ? Rh.data() : nullptr;
+        info.update = obs_f0.data();
+        info.f_hat = fh.data();
+        info.alpha = res->alpha;
+        ctx->observer(ctx->observer_user, &info);
+      }
       cyc_M.push_back(M);
       cyc_mk.push_back(mk);
       M += mk;
@@ -1164,6 +1278,13 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       for (int64_t i = 0; i < std::min<int64_t>(records_cap, res->n_records); ++i) records[i] = recs[size_t(i)];
     ctx->racc_ld = ldR;
     ctx->last_M = (ldR >= M) ? M : 0;
+  });
+}
+
+int rkmf_context_set_observer(rkmf_context* ctx, rkmf_cycle_observer fn, void* user) {
+  return guarded(ctx, [&] {
+    ctx->observer = fn;
+    ctx->observer_user = user;
   });
 }
 

@@ -9,6 +9,11 @@
 #include "rkmf_internal.cuh"
 
 namespace rkmf_b200 {
+// a sketch as its consumer reads it: `groups` partial d-vectors summed in order
+struct SketchSum {
+  const double* part = nullptr;
+  int groups = 0;
+};
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
@@ -41,6 +46,8 @@ namespace rkmf_b200 {
 // memory into caller callbacks (rkmf_host_comm: MPI, gloo, tests).
 struct Transport {
   virtual ~Transport() {}
+  virtual int kind() const = 0;       // 1 NCCL, 2 host callbacks
+  virtual int comm_size() const = 0;  // ranks of the communicator (ncclCommCount for NCCL)
   // in-place elementwise sum (or max) of count doubles over all ranks
   virtual void allreduce(double* dev, size_t count, bool max, cudaStream_t st) = 0;
   // personalised exchange of 8-byte elements: segment q of the send buffer
@@ -67,12 +74,60 @@ struct rkmf_context {
   int64_t launches = 0;
   SolveState* st_dev = nullptr;
   SolveState* st_host = nullptr;  // pinned
-  DevBuf z, pacc, sacc, W, U, Rbar, Racc, ws, u, g, fhat, ref, partial, qshift, qweight, qpi,
+  DevBuf z, W, U, Rbar, Racc, ws, u, g, fhat, ref, partial, qshift, qweight, qpi,
       qemx, scratch, gram, cl, diag;
+  rkmf_cycle_observer observer = nullptr;  // test-only CycleObserver (restart.hpp:53)
+  void* observer_user = nullptr;
   int64_t racc_ld = 0;   // leading dimension of the last solve's R_accum
   int64_t racc_cap = 0;  // allocated leading dimension of Racc (kept across solves)
   std::vector<double> last_R;
   int64_t last_M = 0;
+  // deterministic-reduction scratch (detred.cuh): block partials (shared:
+  // one producer at a time on the stream), then the group partials and
+  // tickets of the step sketch (K2 -> K3), of the start sketch (-> start_init)
+  // and of the (||y||^2, err^2) pair of K5
+  DevBuf redbuf, pfin_sk, pfin_st;  // pfin: summed sketches of a partitioned solve
+  SketchSum start_sum;               // the start sketch as start_init reads it
+  int64_t red_cap_d = 0;
+  DetRed red_sk, red_st, red_up;
+  void ensure_red(int64_t d) {
+    d = std::max<int64_t>(d, 2);
+    if (d <= red_cap_d && redbuf.p) return;
+    int sms = 0;
+    RKMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int kb = 24 * std::max(sms, 1);  // K2: <= 16 blocks/SM; K5: 24 blocks/SM
+    const int gk = det_groups(kb) + 1;     // enough for any grid <= kb
+    const size_t nd = size_t(kb) * size_t(d) + 2 * size_t(gk) * size_t(d) + size_t(gk) * 2;
+    const size_t bytes = sizeof(double) * nd + sizeof(unsigned) * size_t(3 * (gk + 1));
+    redbuf.ensure(bytes);
+    RKMF_CUDA(cudaMemsetAsync(redbuf.p, 0, bytes, stream));  // tickets start at zero
+    double* p = redbuf.as<double>();
+    unsigned* tk = reinterpret_cast<unsigned*>(p + nd);
+    DetRed* rs[3] = {&red_sk, &red_st, &red_up};
+    double* gp = p + size_t(kb) * size_t(d);
+    for (int i = 0; i < 3; ++i) {
+      rs[i]->part = p;
+      rs[i]->gpart = gp;
+      gp += size_t(gk) * size_t(i < 2 ? d : 2);
+      rs[i]->tick = tk + i * (gk + 1);
+      rs[i]->max_blocks = kb;
+      rs[i]->max_len = int(i < 2 ? d : 2);
+      rs[i]->groups = 0;
+    }
+    red_cap_d = d;
+  }
+  DetRed& red_sketch(int64_t d) {
+    ensure_red(d);
+    return red_sk;
+  }
+  DetRed& red_start(int64_t d) {
+    ensure_red(d);
+    return red_st;
+  }
+  const DetRed& red_update() {
+    ensure_red(2);
+    return red_up;
+  }
   std::vector<cudaEvent_t> events;
   cudaEvent_t event(size_t i) {
     while (events.size() <= i) {
@@ -154,9 +209,6 @@ struct rkmf_sketch {
   uint16_t* tile_off = nullptr;  // one allocation: header, then entries
   uint8_t* tile_ent = nullptr;
   size_t layout_bytes = 0;
-  uint8_t* rbin = nullptr;  // row-major copy for the row-sketch K2 (+ sbit), or null
-  uint8_t* sbit = nullptr;
-  uint8_t* wslow = nullptr;
   SketchView view() const {
     SketchView v;
     v.d = d;
@@ -165,9 +217,6 @@ struct rkmf_sketch {
     v.tile_off = tile_off;
     v.tile_ent = tile_ent;
     v.scale = scale;
-    v.rbin = rbin;
-    v.sbit = sbit;
-    v.wslow = wslow;
     return v;
   }
 };
@@ -195,4 +244,8 @@ rkmf_matrix* create_from_device_rp64(rkmf_context* ctx, int64_t n_rows, int64_t 
                                      int64_t nnz, const int64_t* rp64_dev,
                                      const int32_t* col_dev, const double* val_dev,
                                      bool copy_colval, bool require_sorted);
+// gen.cu: rows [rb, re) of the Q1 matrix on N^3 nodes, local numbering
+// [owned | lower halo (nlo) | upper halo (nhi)] (whole matrix: 0, N^3, 0, 0)
+rkmf_matrix* gen_q1_rows(rkmf_context* ctx, int64_t N, int lognormal, uint64_t coef_seed,
+                         int dirichlet, int64_t rb, int64_t re, int64_t nlo, int64_t nhi);
 }  // namespace rkmf_b200

@@ -41,15 +41,17 @@ __device__ __forceinline__ double block_sum(double v, double* buf) {
 
 // basis.cpp:103-115 on device: alpha = ||S s||, U[:,0] = S s / alpha.
 __global__ void __launch_bounds__(kRgsThreads)
-    start_init_kernel(int64_t d, double* sacc, double* U, SolveState* st, int first, int m_eff) {
+    start_init_kernel(int64_t d, const double* sgpart, int ng, double* U, SolveState* st,
+                      int first, int m_eff) {
   __shared__ double buf[kRgsThreads / 32];
   double ss = 0.0;
-  for (int64_t b = threadIdx.x; b < d; b += kRgsThreads) ss += sacc[b] * sacc[b];
-  const double alpha = sqrt(block_sum<kRgsThreads>(ss, buf));
   for (int64_t b = threadIdx.x; b < d; b += kRgsThreads) {
-    U[b] = sacc[b] / alpha;
-    sacc[b] = 0.0;
+    const double v = det_group_sum(sgpart, ng, d, b);
+    U[b] = v;  // scaled below
+    ss += v * v;
   }
+  const double alpha = sqrt(block_sum<kRgsThreads>(ss, buf));
+  for (int64_t b = threadIdx.x; b < d; b += kRgsThreads) U[b] = U[b] / alpha;
   if (threadIdx.x == 0) {
     st->alpha_k = alpha;
     st->sigma = 1.0 / alpha;
@@ -65,16 +67,16 @@ __global__ void __launch_bounds__(kRgsThreads)
 
 // One modified Gram-Schmidt sweep in the sketch space (basis.cpp:123-138):
 // r_i = <u_i, p>, p -= r_i u_i for i = 0..k, r_kk = ||p||, breakdown test,
-// U[:,k+1] = p / r_kk. The sketch p arrives as the reduced partials in pacc,
-// which this kernel re-zeroes for the next step. One __syncthreads per MGS
+// U[:,k+1] = p / r_kk. The sketch p arrives as the K2 group partials (summed
+// here in group order, detred.cuh). One __syncthreads per MGS
 // iteration (ping-pong reduction slots). U[:,0..k] (contiguous, <= ~80 KB at
 // BASELINE sizes) is staged into shared memory with one coalesced sweep first,
 // so the sequential sweep pays one L2 round trip instead of k+1; when it does
 // not fit, the next column is prefetched from global memory instead.
 template <int PT>
 __global__ void __launch_bounds__(kRgsThreads)
-    rgs_step_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
-                    double* U, double* Rbar, SolveState* st, int staged) {
+    rgs_step_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, const double* pgpart,
+                    int ng, double* U, double* Rbar, SolveState* st, int staged) {
   extern __shared__ __align__(16) double Us[];
   __shared__ double red[2][kRgsThreads / 32];
   __shared__ double rs[1024];
@@ -94,8 +96,7 @@ __global__ void __launch_bounds__(kRgsThreads)
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const int64_t b = t + int64_t(j) * kRgsThreads;
-    p[j] = b < d ? pacc[b] : 0.0;
-    if (b < d) pacc[b] = 0.0;
+    p[j] = b < d ? det_group_sum(pgpart, ng, d, b) : 0.0;
     un[j] = (!staged && b < d) ? U[b] : 0.0;
   }
   if (staged) __syncthreads();
@@ -169,8 +170,8 @@ __global__ void __launch_bounds__(kRgsThreads)
 // p -= U r, r_kk = ||p||, U[:,k+1] = p / r_kk. With U sketch-orthonormal to
 // rounding, r agrees with the sequential sweep to O(eps ||p||).
 __global__ void __launch_bounds__(kRgsThreads)
-    rgs_gram_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
-                    double* U, double* Rbar, double* G, SolveState* st) {
+    rgs_gram_kernel(int64_t d, int k, int64_t ldr, int64_t n, double tol, const double* pgpart,
+                    int ng, double* U, double* Rbar, double* G, SolveState* st) {
   extern __shared__ __align__(16) double sm[];
   const int kk = k + 1;
   const int64_t ucnt = (int64_t(kk) * d + 1) / 2 * 2;  // U[:,0..k], rounded to 16 B
@@ -195,13 +196,16 @@ __global__ void __launch_bounds__(kRgsThreads)
     bulk_g2s(Us, U, ubytes, &bar);
     if (k >= 2) bulk_g2s(Gs, G, gbytes, &bar);
   }
+  __syncthreads();  // the barrier is initialised before any thread polls it
   pdl_wait_then_trigger();
   if (t == 0) trace_max(k, 3);
-  if (st->stopped <= k) return;
-  for (int64_t b = t; b < d; b += kRgsThreads) {
-    ps[b] = pacc[b];
-    pacc[b] = 0.0;
+  if (st->stopped <= k) {
+    // past a breakdown: the issued bulk copies must land before the block
+    // (and its shared memory) retires
+    if (t == 0) mbar_wait(&bar, 0);
+    return;
   }
+  for (int64_t b = t; b < d; b += kRgsThreads) ps[b] = det_group_sum(pgpart, ng, d, b);
   mbar_wait(&bar, 0);
   __syncthreads();
   if (t == 0) trace_max(k, 4);
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     final_update_kernel(int64_t n, int m_eff, int64_t ldw, double* W,
                         const double* __restrict__ z, const double* __restrict__ Rbar,
                         int64_t ldr, const double* __restrict__ g, double* f_hat,
-                        const double* __restrict__ ref, SolveState* st) {
+                        const double* __restrict__ ref, SolveState* st, DetRed red) {
   __shared__ double cg[kMaxCoef], cr[kMaxCoef];
   __shared__ double buf[kUpdThreads / 32], buf2[kUpdThreads / 32];
   const int mk = st->stopped;
@@ -437,11 +441,17 @@ __global__ void __launch_bounds__(kUpdThreads)
   }
   yy = block_sum<kUpdThreads>(yy, buf);
   if (ref) ee = block_sum<kUpdThreads>(ee, buf2);
-  if (threadIdx.x == 0) {
-    atomicAdd(&st->yn2, yy);
-    if (ref) atomicAdd(&st->err2, ee);
-  }
   if (bad) st->nonfinite = 1;
+  // (||y||^2, ||f - ref||^2) of the blocks -> st->yn2, st->err2 (adjacent),
+  // summed in a fixed block order (detred.cuh)
+  __shared__ double mine[2];
+  __shared__ int rflag;
+  if (threadIdx.x == 0) {
+    mine[0] = yy;
+    mine[1] = ee;
+  }
+  __syncthreads();
+  det_reduce<kUpdThreads, 0>(red, 2, mine, &st->yn2, threadIdx.x, &rflag);
   if (blockIdx.x == 0 && threadIdx.x == 0)  // coupling for the next R_accum block
     st->coupling = next ? Rbar[int64_t(km) * ldr + km + 1] : 0.0;
 }
@@ -481,23 +491,23 @@ int stream_grid(int64_t work, int threads) {
 
 void trace_bind_krylov(unsigned long long* p) { trace_bind_tu(p); }
 
-void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev, bool first,
-                         int m_eff, cudaStream_t st) {
-  start_init_kernel<<<1, kRgsThreads, 0, st>>>(d, sacc, U, st_dev, first ? 1 : 0, m_eff);
+void launch_start_init_m(int64_t d, const double* sgpart, int ng, double* U, SolveState* st_dev,
+                         bool first, int m_eff, cudaStream_t st) {
+  start_init_kernel<<<1, kRgsThreads, 0, st>>>(d, sgpart, ng, U, st_dev, first ? 1 : 0, m_eff);
   RKMF_CUDA(cudaGetLastError());
 }
 
 bool rgs_use_gram() {  // RKMF_RGS=mgs selects the sequential sweep (A/B runs)
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_RGS");
+    const char* e = knob_env("RKMF_RGS");
     v = (e && e[0] == 'm') ? 0 : 1;
   }
   return v == 1;
 }
 
-void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, double* pacc,
-                     double* U, double* Rbar, double* G, int64_t ldg, SolveState* st_dev,
+void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, const double* pgpart,
+                     int ng, double* U, double* Rbar, double* G, int64_t ldg, SolveState* st_dev,
                      cudaStream_t st) {
   if (k >= 1024) param_error("randomized_arnoldi: m > 1024 is not supported on device");
   const size_t gbytes = sizeof(double) * (size_t(k + 1) * size_t(d) + size_t(k + 1) * size_t(k) / 2 +
@@ -506,7 +516,7 @@ void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, doubl
     RKMF_CUDA(cudaFuncSetAttribute(rgs_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    200 * 1024));
     launch_maybe_pdl(rgs_gram_kernel, dim3(1), dim3(kRgsThreads), gbytes, st, d, k, ldr, n, tol,
-                     pacc, U, Rbar, G, st_dev);
+                     pgpart, ng, U, Rbar, G, st_dev);
     return;
   }
   const int64_t pt = (d + kRgsThreads - 1) / kRgsThreads;
@@ -518,8 +528,8 @@ void launch_rgs_step(int64_t d, int k, int64_t ldr, int64_t n, double tol, doubl
     auto fn = rgs_step_kernel<P>;                                                      \
     RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                    160 * 1024));                                       \
-    launch_maybe_pdl(fn, dim3(1), dim3(kRgsThreads), smem, st, d, k, ldr, n, tol, pacc, \
-                     U, Rbar, st_dev, staged);                                         \
+    launch_maybe_pdl(fn, dim3(1), dim3(kRgsThreads), smem, st, d, k, ldr, n, tol, pgpart, \
+                     ng, U, Rbar, st_dev, staged);                                     \
   } while (0)
   if (pt <= 1) RKMF_RGS(1);
   else if (pt <= 2) RKMF_RGS(2);
@@ -538,15 +548,15 @@ void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double*
   // 4% on the whole cfg2 solve: the (k+1)-column read streams keep more DRAM
   // pages open with the extra in-flight blocks (read-only microbenchmark of 26
   // streams: 6.49 -> 6.86 TB/s). RKMF_K4_GRIDX / RKMF_K4_UNROLL override.
-  static const int unr = [] { const char* e = getenv("RKMF_K4_UNROLL"); return e ? atoi(e) : 4; }();
-  static const int gx = [] { const char* e = getenv("RKMF_K4_GRIDX"); return e ? atoi(e) : 24; }();
+  static const int unr = [] { const char* e = knob_env("RKMF_K4_UNROLL"); return e ? atoi(e) : 4; }();
+  static const int gx = [] { const char* e = knob_env("RKMF_K4_GRIDX"); return e ? atoi(e) : 24; }();
   const int64_t need = (std::max<int64_t>(n / 2, 1) + kUpdThreads - 1) / kUpdThreads;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sm_count()) * gx)));
   // RKMF_K4_LOAD: 0 streaming (evict-first), 1 default, 2 last-use (default)
-  static const int ldm = [] { const char* e = getenv("RKMF_K4_LOAD"); return e ? atoi(e) : 2; }();
-  static const int order = [] { const char* e = getenv("RKMF_K4_ORDER"); return e ? atoi(e) : 0; }();
+  static const int ldm = [] { const char* e = knob_env("RKMF_K4_LOAD"); return e ? atoi(e) : 2; }();
+  static const int order = [] { const char* e = knob_env("RKMF_K4_ORDER"); return e ? atoi(e) : 0; }();
   const int rev = order == 1 ? (k & 1) : (order == 2 ? 1 : 0);
-  static const int pf = [] { const char* e = getenv("RKMF_K4_PREFETCH"); return e ? atoi(e) : 1; }();
+  static const int pf = [] { const char* e = knob_env("RKMF_K4_PREFETCH"); return e ? atoi(e) : 1; }();
 #define RKMF_K4(U, L)                                                                       \
   launch_maybe_pdl(basis_update_kernel<U, L>, dim3(grid), dim3(kUpdThreads), 0, st, n, k, ldw, \
                    W, z, Rbar, ldr, st_dev, rev, pf)
@@ -566,12 +576,15 @@ void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double*
 
 void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const double* z,
                          const double* Rbar, int64_t ldr, const double* g, double* f_hat,
-                         const double* ref, SolveState* st_dev, cudaStream_t st) {
+                         const double* ref, SolveState* st_dev, const DetRed& red,
+                         cudaStream_t st) {
   if (m_eff > kMaxCoef) param_error("restart: m_r > 1024 is not supported on device");
   const int64_t fneed = (std::max<int64_t>(n, 1) + kUpdThreads - 1) / kUpdThreads;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(fneed, int64_t(sm_count()) * 24)));
+  if (grid > red.max_blocks || red.max_len < 2)
+    param_error("internal: update reduction scratch too small");
   final_update_kernel<<<grid, kUpdThreads, 0, st>>>(n, m_eff, ldw, W, z, Rbar, ldr, g, f_hat, ref,
-                                                    st_dev);
+                                                    st_dev, red);
   RKMF_CUDA(cudaGetLastError());
 }
 

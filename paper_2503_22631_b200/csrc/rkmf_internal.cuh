@@ -4,10 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "detred.cuh"
 #include "rkmf_b200.h"
 
 namespace rkmf_b200 {
@@ -31,6 +33,18 @@ struct Error : std::runtime_error {
                                                       cudaGetErrorString(e_) + " at " + \
                                                       __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
+
+// ---- ablation knobs: environment variables are read only in
+// the experiments build (`make experiments` -> _lib/librkmf_b200_exp.so,
+// -DRKMF_EXPERIMENTS); the product library always runs the defaults. ----
+inline const char* knob_env(const char* name) {
+#ifdef RKMF_EXPERIMENTS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // ---- programmatic dependent launch (PDL) between the per-step kernels ----
 // Each step kernel runs its dependency-free prologue, then waits for the
@@ -122,10 +136,6 @@ void launch_sketch_generate(int64_t d, int64_t n, int64_t j0, int64_t zeta, uint
 void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
                          const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
                          cudaStream_t st);
-// row-major (rbin [n][8] uint8 rows, sbit [n] sign bits) copy for zeta 8,
-// d <= 256, slots edge-coloured per 32-column warp tile (wslow[]: not coloured)
-void launch_sketch_rowbins(int64_t n, int d, const uint16_t* rows, const int8_t* signs,
-                           uint8_t* rbin, uint8_t* sbit, uint8_t* wslow, cudaStream_t st);
 void launch_sketch_export(int64_t count, const uint16_t* rows, const int8_t* signs,
                           int64_t* rows64, cudaStream_t st);
 
@@ -156,9 +166,6 @@ struct SketchView {
   const uint16_t* tile_off;  // [num_tiles][tile_off_stride(d)]: slot offsets, slot bins
   const uint8_t* tile_ent;   // [num_tiles][kTileRows*zeta]: local row | sign<<7
   double scale;
-  const uint8_t* rbin = nullptr;  // row-major copy (zeta 8, d <= 256), or null
-  const uint8_t* sbit = nullptr;
-  const uint8_t* wslow = nullptr;  // per 32-column warp tile: 1 = slots not coloured
 };
 // Per-tile sketch header (uint16): off[d+1] slot offsets, then bin[d] (the
 // sketch row of each slot), padded to 16 bytes.
@@ -193,39 +200,42 @@ __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t*
     acc[bins[s]] += a0 + a1;
   }
 }
-// mode: 0 = z = xscale*A x ; 1 = also sketch z into pacc ; 2 = sketch x into pacc only.
+// mode: 0 = z = xscale*A x ; 1 = also sketch z ; 2 = sketch x only. The
+// sketch comes out as red.groups group partials in red.gpart (detred.cuh:
+// a fixed-order, reproducible reduction); consumers sum them in group order
+// (det_group_sum), launch_det_finish writes the plain d-vector.
 void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const double* x,
-                        const double* xscale_dev, double* z, double* pacc,
-                        const int32_t* stop_flag, int step, int grid, cudaStream_t st);
+                        const double* xscale_dev, double* z, const int32_t* stop_flag,
+                        int step, int grid, DetRed& red, cudaStream_t st);
+void launch_det_finish(const DetRed& red, int64_t L, double* out, cudaStream_t st);
 int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode);
-// K2 with the sketch in the SpMV threads (spmv_rowsketch.cu): diagonal copy
-// (or the identity: A->dval null, ndiag 1) and a sketch with the row-major copy
-bool launch_spmv_rowsketch(const CsrView* A, const SketchView* S, const double* x,
-                           const double* xscale_dev, double* z, double* pacc,
-                           const int32_t* stop_flag, int step, cudaStream_t st);
 // the same pipeline for the sketch of x alone (mode 2)
 bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double* xscale_dev,
-                             double* pacc, cudaStream_t st);
+                             DetRed& red, cudaStream_t st);
 // TMA-pipelined mode-1 kernel (spmv_pipe.cu); returns false when not applicable.
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
-                             const double* xscale_dev, double* z, double* pacc,
-                             const int32_t* stop_flag, int step, cudaStream_t st);
+                             const double* xscale_dev, double* z,
+                             const int32_t* stop_flag, int step, DetRed& red, cudaStream_t st);
 void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st);
 void launch_matrix_check(const CsrView* A, int32_t* flags, bool require_sorted, cudaStream_t st);
 
 // krylov.cu
-void launch_start_init_m(int64_t d, double* sacc, double* U, SolveState* st_dev, bool first,
-                         int m_eff, cudaStream_t st);
+// the start sketch arrives as ng group partials (detred.cuh)
+void launch_start_init_m(int64_t d, const double* sgpart, int ng, double* U, SolveState* st_dev,
+                         bool first, int m_eff, cudaStream_t st);
 // G: (m+1) x (m+1) scratch for the Gram rows of U (row i at i*ldg), or null
 // for the sequential MGS sweep.
-void launch_rgs_step(int64_t d, int k, int64_t m, int64_t n, double tol, double* pacc, double* U,
-                     double* Rbar, double* G, int64_t ldg, SolveState* st_dev, cudaStream_t st);
+// p = S A w_k arrives as ng group partials pgpart[ng][d] (detred.cuh)
+void launch_rgs_step(int64_t d, int k, int64_t m, int64_t n, double tol, const double* pgpart,
+                     int ng, double* U, double* Rbar, double* G, int64_t ldg, SolveState* st_dev,
+                     cudaStream_t st);
 void launch_basis_update(int64_t n, int k, int64_t ldw, double* W, const double* z,
                          const double* Rbar, int64_t ldr, const SolveState* st_dev,
                          cudaStream_t st);
 void launch_final_update(int64_t n, int m_eff, int64_t ldw, double* W, const double* z,
                          const double* Rbar, int64_t ldr, const double* g, double* f_hat,
-                         const double* ref, SolveState* st_dev, cudaStream_t st);
+                         const double* ref, SolveState* st_dev, const DetRed& red,
+                         cudaStream_t st);
 void launch_scale_copy(int64_t n, const double* src, double* dst, const SolveState* st_dev,
                        cudaStream_t st);
 void launch_fill(int64_t n, double v, double* x, cudaStream_t st);

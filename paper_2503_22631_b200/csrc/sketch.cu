@@ -260,188 +260,4 @@ void launch_sketch_export(int64_t count, const uint16_t* rows, const int8_t* /*s
   RKMF_CUDA(cudaGetLastError());
 }
 
-// Row-major layout for the fused K2 with the sketch in the SpMV threads
-// (spmv_rowsketch.cu; zeta == 8, d <= 255): for column j, slot q in 0..7
-// holds one of its 8 (row, sign) entries: rbin[j][q] = row (uint8), bit q of
-// sbit[j] set when the sign is negative. 9 bytes per column.
-//
-// The slot order is an 8-edge-colouring of each warp tile (32 consecutive
-// columns, i.e. the 32 lanes of one SpMV warp): within a warp tile no two
-// columns put the same row in the same slot, so when the 32 lanes add slot q
-// into their warp's accumulator they touch 32 distinct bins, and a plain
-// shared-memory read-add-write is race-free (no fp64 CAS atomics). The
-// bipartite graph columns x rows has column degree 8, so 8 colours suffice
-// whenever no row occurs more than 8 times among the 32 columns (Koenig);
-// colours are assigned greedily with Kempe-chain (alternating path) swaps.
-// A warp tile that cannot be coloured (a row hit > 8 times) keeps the sorted
-// order and is flagged in wslow[], where the kernel falls back to atomics.
-__global__ void sketch_rowbins_kernel(int64_t n, int d, const uint16_t* __restrict__ rows,
-                                      const int8_t* __restrict__ signs, uint8_t* __restrict__ rbin,
-                                      uint8_t* __restrict__ sbit, uint8_t* __restrict__ wslow) {
-  const int64_t nwt = (n + 31) / 32;
-  for (int64_t wt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; wt < nwt;
-       wt += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j0 = wt * 32;
-    const int nc = int(min(int64_t(32), n - j0));
-    uint8_t col[32][8];     // col[c][q] = row (bin) in slot q of column c, 255 = free
-    int8_t sgn[32][8];
-    int8_t binc[256][8];    // binc[b][q] = column using bin b in slot q, -1 = free
-    // hw[h][q][r]: entries of half-warp h in slot q whose bin is r mod 16. A
-    // half-warp's 64-bit shared accesses are conflict-free when its 16 bins
-    // differ mod 16, so among the colours free at both ends the least loaded
-    // residue is taken (fewer bank conflicts in the kernel's read-add-write).
-    uint8_t hw[2][8][16];
-    for (int h = 0; h < 2; ++h)
-      for (int q = 0; q < 8; ++q)
-        for (int r = 0; r < 16; ++r) hw[h][q][r] = 0;
-    for (int b = 0; b < 256; ++b)
-      for (int q = 0; q < 8; ++q) binc[b][q] = -1;
-    for (int c = 0; c < 32; ++c)
-      for (int q = 0; q < 8; ++q) col[c][q] = 255;
-    bool ok = true;
-    for (int c = 0; c < nc && ok; ++c) {
-      for (int k = 0; k < 8 && ok; ++k) {
-        const int b = rows[(j0 + c) * 8 + k];
-        const int8_t sg = signs[(j0 + c) * 8 + k];
-        int a = -1, e = -1;  // a: free at column c, e: free at bin b
-        for (int q = 0; q < 8; ++q) {
-          if (a < 0 && col[c][q] == 255) a = q;
-          if (e < 0 && binc[b][q] < 0) e = q;
-        }
-        if (a < 0 || e < 0) { ok = false; break; }
-        int use = -1, best = 1 << 20;
-        for (int q = 0; q < 8; ++q)
-          if (col[c][q] == 255 && binc[b][q] < 0 && hw[c >> 4][q][b & 15] < best) {
-            best = hw[c >> 4][q][b & 15];
-            use = q;
-          }
-        if (use < 0) {
-          {
-            // swap colours a and e along the alternating path that starts at
-            // bin b with colour a: b -a- c1 -e- b1 -a- c2 ... (it cannot reach
-            // column c, which has a free and e used; bipartite argument)
-            int cur_b = b, cc = binc[b][a];
-            while (cc >= 0) {
-              const int nb = col[cc][e];  // next bin along colour e (255: end)
-              // residue counts: edge (cc, cur_b) moves a -> e, edge (cc, nb) e -> a
-              --hw[cc >> 4][a][cur_b & 15];
-              ++hw[cc >> 4][e][cur_b & 15];
-              if (nb != 255) {
-                --hw[cc >> 4][e][nb & 15];
-                ++hw[cc >> 4][a][nb & 15];
-              }
-              // swap at column cc: its a-edge (to cur_b) becomes e, its e-edge becomes a
-              col[cc][e] = uint8_t(cur_b);
-              const int8_t sa = sgn[cc][a];
-              if (nb != 255) {
-                col[cc][a] = uint8_t(nb);
-                sgn[cc][a] = sgn[cc][e];
-              } else {
-                col[cc][a] = 255;
-              }
-              sgn[cc][e] = sa;
-              binc[cur_b][e] = int8_t(cc);
-              if (binc[cur_b][a] == cc) binc[cur_b][a] = -1;
-              if (nb == 255) break;
-              // bin nb: its e-edge (to cc) becomes a; continue along its old a-edge
-              const int nxt = binc[nb][a];
-              binc[nb][a] = int8_t(cc);
-              if (binc[nb][e] == cc) binc[nb][e] = -1;
-              cur_b = nb;
-              cc = nxt;
-            }
-            use = a;
-          }
-        }
-        col[c][use] = uint8_t(b);
-        sgn[c][use] = sg;
-        binc[b][use] = int8_t(c);
-        ++hw[c >> 4][use][b & 15];
-      }
-    }
-    // local search: swap two slots of one column when both bins stay unique
-    // in their new slots and the half-warp's residue counts get flatter
-    // (sum of squares), i.e. fewer bank conflicts in the kernel
-    for (int pass = 0; pass < 4 && ok; ++pass) {
-      bool moved = false;
-      for (int c = 0; c < nc; ++c) {
-        const int h = c >> 4;
-        for (int q1 = 0; q1 < 8; ++q1)
-          for (int q2 = q1 + 1; q2 < 8; ++q2) {
-            const int b1 = col[c][q1], b2 = col[c][q2];
-            if (binc[b1][q2] >= 0 || binc[b2][q1] >= 0) continue;
-            const int r1 = b1 & 15, r2 = b2 & 15;
-            if (r1 == r2) continue;
-            const int a11 = hw[h][q1][r1], a21 = hw[h][q2][r1];
-            const int a12 = hw[h][q1][r2], a22 = hw[h][q2][r2];
-            // r1 moves q1 -> q2, r2 moves q2 -> q1
-            const int delta = ((a11 - 1) * (a11 - 1) - a11 * a11) + ((a21 + 1) * (a21 + 1) - a21 * a21) +
-                              ((a22 - 1) * (a22 - 1) - a22 * a22) + ((a12 + 1) * (a12 + 1) - a12 * a12);
-            if (delta >= 0) continue;
-            --hw[h][q1][r1]; ++hw[h][q2][r1]; --hw[h][q2][r2]; ++hw[h][q1][r2];
-            binc[b1][q1] = -1; binc[b2][q2] = -1;
-            binc[b1][q2] = int8_t(c); binc[b2][q1] = int8_t(c);
-            col[c][q1] = uint8_t(b2); col[c][q2] = uint8_t(b1);
-            const int8_t t = sgn[c][q1];
-            sgn[c][q1] = sgn[c][q2];
-            sgn[c][q2] = t;
-            moved = true;
-          }
-      }
-      if (!moved) break;
-    }
-    // self-check of the colouring before it is trusted: every slot holds
-    // distinct bins across the warp tile, and every column holds exactly its
-    // own 8 (row, sign) entries
-    for (int q = 0; q < 8 && ok; ++q) {
-      uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int c = 0; c < nc; ++c) {
-        const int b = col[c][q];
-        if (b == 255 && d <= 255) { ok = false; break; }
-        if (seen[b >> 5] & (1u << (b & 31))) { ok = false; break; }
-        seen[b >> 5] |= 1u << (b & 31);
-      }
-    }
-    for (int c = 0; c < nc && ok; ++c) {
-      const int64_t j = j0 + c;
-      for (int k = 0; k < 8 && ok; ++k) {
-        bool found = false;
-        for (int q = 0; q < 8; ++q)
-          found |= col[c][q] == rows[j * 8 + k] && sgn[c][q] == signs[j * 8 + k];
-        ok = found;
-      }
-    }
-    for (int c = 0; c < nc; ++c) {
-      const int64_t j = j0 + c;
-      uint32_t bits = 0;
-      for (int q = 0; q < 8; ++q) {
-        const int b = ok ? col[c][q] : rows[j * 8 + q];
-        const int8_t sg = ok ? sgn[c][q] : signs[j * 8 + q];
-        rbin[j * 8 + q] = uint8_t(b);
-        bits |= (sg < 0 ? 1u : 0u) << q;
-      }
-      sbit[j] = uint8_t(bits);
-    }
-    wslow[wt] = ok ? 0 : 1;
-  }
-}
-
-void launch_sketch_rowbins(int64_t n, int d, const uint16_t* rows, const int8_t* signs,
-                           uint8_t* rbin, uint8_t* sbit, uint8_t* wslow, cudaStream_t st) {
-  if (n <= 0) return;
-  const int64_t nwt = (n + 31) / 32;
-  const int64_t blocks = std::min<int64_t>((nwt + 63) / 64, 148 * 32);
-  sketch_rowbins_kernel<<<int(blocks), 64, 0, st>>>(n, d, rows, signs, rbin, sbit, wslow);
-  RKMF_CUDA(cudaGetLastError());
-  if (getenv("RKMF_PIPE_VERBOSE")) {
-    std::vector<uint8_t> h(static_cast<size_t>(nwt), uint8_t(0));
-    RKMF_CUDA(cudaMemcpyAsync(h.data(), wslow, size_t(nwt), cudaMemcpyDeviceToHost, st));
-    RKMF_CUDA(cudaStreamSynchronize(st));
-    int64_t bad = 0;
-    for (uint8_t v : h) bad += v;
-    fprintf(stderr, "[rkmf] sketch row layout: %lld of %lld warp tiles without a colouring\n",
-            (long long)bad, (long long)nwt);
-  }
-}
-
 }  // namespace rkmf_b200

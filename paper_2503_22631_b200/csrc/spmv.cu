@@ -33,8 +33,8 @@ __global__ void __launch_bounds__(kBlock)
                        const double* __restrict__ val, const double* __restrict__ x,
                        const double* xscale, double* __restrict__ z, int64_t num_tiles, int cap,
                        int d, int zeta, int64_t off_stride, const uint16_t* __restrict__ toff,
-                       const uint8_t* __restrict__ tent, double sscale, double* pacc,
-                       const int32_t* stop, int step) {
+                       const uint8_t* __restrict__ tent, double sscale,
+                       const int32_t* stop, int step, DetRed red) {
   if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool kSpmv = MODE <= 1;
@@ -100,8 +100,11 @@ __global__ void __launch_bounds__(kBlock)
       __syncthreads();
     }
   }
-  if (kSketch)
-    for (int b = t; b < d; b += kBlock) atomicAdd(pacc + b, acc[b]);
+  if (kSketch) {  // block partials -> group partials in a fixed order (detred.cuh)
+    __shared__ int rflag;
+    __syncthreads();
+    det_group_reduce<kBlock, 0>(red, d, acc, t, &rflag);
+  }
 }
 
 size_t smem_bytes(int mode, int cap, int64_t d, int64_t zeta, int64_t off_stride) {
@@ -132,7 +135,7 @@ void* pick(bool rp64, int mode) {
 bool use_pipe() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_SPMV_PIPE");
+    const char* e = knob_env("RKMF_SPMV_PIPE");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -169,8 +172,8 @@ int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode) {
 }
 
 void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const double* x,
-                        const double* xscale_dev, double* z, double* pacc,
-                        const int32_t* stop_flag, int step, int grid, cudaStream_t st) {
+                        const double* xscale_dev, double* z, const int32_t* stop_flag,
+                        int step, int grid, DetRed& red, cudaStream_t st) {
   const int64_t n = A ? A->n_rows : S->n;
   const int64_t tiles = (n + kTileRows - 1) / kTileRows;
   const int cap = A ? A->cap : 0;
@@ -178,12 +181,15 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
   const int64_t off_stride = S ? tile_off_stride(S->d) : 0;
   const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
   if (mode == 1 && A && S && use_pipe() &&
-      launch_spmv_sketch_pipe(A, S, x, xscale_dev, z, pacc, stop_flag, step, st))
+      launch_spmv_sketch_pipe(A, S, x, xscale_dev, z, stop_flag, step, red, st))
     return;
   if (mode == 2 && S && !stop_flag && use_pipe() &&
-      launch_sketch_only_pipe(S, x, xscale_dev, pacc, st))
+      launch_sketch_only_pipe(S, x, xscale_dev, red, st))
     return;
   if (grid <= 0) grid = spmv_sketch_grid(A, S, mode);
+  if (S && (grid > red.max_blocks || S->d > red.max_len))
+    param_error("internal: sketch reduction scratch too small");
+  red.groups = S ? det_groups(grid) : 0;
   const uint16_t* toff = S ? S->tile_off : nullptr;
   const uint8_t* tent = S ? S->tile_ent : nullptr;
   const double sscale = S ? S->scale : 1.0;
@@ -192,7 +198,7 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
   spmv_sketch_kernel<RP, MODE><<<grid, kBlock, smem, st>>>(                                    \
       n, A ? static_cast<const RP*>(A->row_ptr) : nullptr, A ? A->col : nullptr,               \
       A ? A->val : nullptr, x, xscale_dev, z, tiles, cap, d, zeta, off_stride, toff, tent,     \
-      sscale, pacc, stop_flag, step)
+      sscale, stop_flag, step, red)
   if (smem > 48 * 1024)
     RKMF_CUDA(cudaFuncSetAttribute(pick(rp64, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
@@ -206,6 +212,21 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
     else RKMF_LAUNCH_SPMV(int32_t, 2);
   }
 #undef RKMF_LAUNCH_SPMV
+  RKMF_CUDA(cudaGetLastError());
+}
+
+namespace {
+__global__ void det_finish_kernel(const double* __restrict__ gpart, int ng, int64_t L,
+                                  double* out) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < L;
+       j += int64_t(gridDim.x) * blockDim.x)
+    out[j] = det_group_sum(gpart, ng, L, j);
+}
+}  // namespace
+
+void launch_det_finish(const DetRed& red, int64_t L, double* out, cudaStream_t st) {
+  if (L <= 0) return;
+  det_finish_kernel<<<unsigned((L + 127) / 128), 128, 0, st>>>(red.gpart, red.groups, L, out);
   RKMF_CUDA(cudaGetLastError());
 }
 

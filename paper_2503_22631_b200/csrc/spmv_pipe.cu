@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "rkmf_internal.cuh"
+#include "detred.cuh"
 #include "tma.cuh"
 
 namespace rkmf_b200 {
@@ -96,11 +97,12 @@ constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads +
       const double *__restrict__ val, const double *__restrict__ x, const double *xscale,      \
       double *__restrict__ z, int64_t num_tiles, int cap, int d, int zeta, int off_stride,     \
       const uint16_t *__restrict__ toff, const uint8_t *__restrict__ tent, double sscale,      \
-      double *pacc, const int32_t *stop, int step, int nstages, int l2_hints, int debug,        \
-      const int32_t *__restrict__ doff, int ndiag, int64_t ncols, int sync_mode, int dstride
+      const int32_t *stop, int step, int nstages, int l2_hints, int debug,        \
+      const int32_t *__restrict__ doff, int ndiag, int64_t ncols, int sync_mode, int dstride,   \
+      DetRed red
 #define RKMF_PIPE_ARGS                                                                       \
-  n, rp, ci, val, x, xscale, z, num_tiles, cap, d, zeta, off_stride, toff, tent, sscale, pacc, \
-      stop, step, nstages, l2_hints, debug, doff, ndiag, ncols, sync_mode, dstride
+  n, rp, ci, val, x, xscale, z, num_tiles, cap, d, zeta, off_stride, toff, tent, sscale, \
+      stop, step, nstages, l2_hints, debug, doff, ndiag, ncols, sync_mode, dstride, red
 
 template <typename RP, int TPR, int G, int FMT, int ND>
 __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
@@ -125,7 +127,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
   __syncthreads();
   // The matrix and the sketch layout are constant, so the producer fills the
   // first nstages stages before waiting on the previous kernel (PDL: that
-  // overlaps the basis update's tail); x, pacc and the stop flag come from
+  // overlaps the basis update's tail); x and the stop flag come from
   // earlier kernels, so every other thread waits first.
   const bool producer = t == kSpmv + kSketchThreads;
   if (t == 0 && stop) trace_first(step, 10);
@@ -242,8 +244,11 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
         ph ^= 1u;
       }
     }
-    if (!(debug & 8))
-      for (int b = u; b < d; b += kSketchThreads) atomicAdd(pacc + b, acc[b]);
+    // the block's d partials -> its group's partial, summed in a fixed block
+    // order (detred.cuh; K3 sums the groups). The last tile's bar.sync 2
+    // above completed acc.
+    __shared__ int rflag;
+    if (!(debug & 8)) det_group_reduce<kSketchThreads, 2>(red, d, acc, u, &rflag);
     if (u == 0 && stop) trace_max(step, 1);
     return;
   }
@@ -434,17 +439,17 @@ size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages, int fmt) 
 int env_l2_hints() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_L2_HINTS");
+    const char* e = knob_env("RKMF_L2_HINTS");
     v = e ? atoi(e) : 1;
     if (v < 0 || v > 2) v = 1;
   }
   return v;
 }
 
-int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather, 4 no SpMV, 8 no pacc flush, 16 producer waits before filling)
+int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather, 4 no SpMV, 8 no sketch flush, 16 producer waits before filling)
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_PIPE_DEBUG");
+    const char* e = knob_env("RKMF_PIPE_DEBUG");
     v = e ? atoi(e) : 0;
   }
   return v;
@@ -458,7 +463,7 @@ int env_debug() {  // RKMF_PIPE_DEBUG: ablation bits (1 no sketch, 2 no x gather
 int env_sync() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_PIPE_SYNC");
+    const char* e = knob_env("RKMF_PIPE_SYNC");
     v = e ? atoi(e) : 1;
   }
   return v;
@@ -467,7 +472,7 @@ int env_sync() {
 int env_stages() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("RKMF_PIPE_STAGES");
+    const char* e = knob_env("RKMF_PIPE_STAGES");
     v = e ? atoi(e) : 0;
     if (v < 0 || v > kStages) v = 0;
   }
@@ -487,8 +492,8 @@ int sms() {
 
 template <typename RP, int TPR, int G, int FMT = 0, int ND = 1>
 bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
-                   const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
-                   int step, cudaStream_t st) {
+                   const double* xscale_dev, double* z, const int32_t* stop,
+                   int step, DetRed& red, cudaStream_t st) {
   constexpr int kThreads = block_threads<TPR, G>();
   const int off_stride = int(tile_off_stride(S->d));
   auto fn = [] {
@@ -533,7 +538,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
         best_s = s;
       }
     }
-    if (getenv("RKMF_PIPE_VERBOSE"))
+    if (knob_env("RKMF_PIPE_VERBOSE"))
       fprintf(stderr, "[rkmf] K2 pipe RP=%d TPR=%d G=%d FMT=%d ND=%d: stages=%d blocks/SM=%d stride=%lld\n",
               int(sizeof(RP)), TPR, G, FMT, ND, best_s, best_per, (long long)stride);
     slot = next_slot;
@@ -548,11 +553,14 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
+  if (grid > red.max_blocks || S->d > red.max_len)
+    param_error("internal: sketch reduction scratch too small");
+  red.groups = det_groups(grid);
   launch_maybe_pdl(fn, dim3(grid), dim3(kThreads), smem, st, A->n_rows,
                    static_cast<const RP*>(A->row_ptr), A->col, FMT ? A->dval : A->val, x,
                    xscale_dev, z, tiles, cap, int(S->d), int(S->zeta), off_stride, S->tile_off,
-                   S->tile_ent, S->scale, pacc, stop, step, stages, env_l2_hints(), env_debug(),
-                   A->doff, A->ndiag, A->n_cols, env_sync(), A->dstride);
+                   S->tile_ent, S->scale, stop, step, stages, env_l2_hints(), env_debug(),
+                   A->doff, A->ndiag, A->n_cols, env_sync(), A->dstride, red);
   return true;
 }
 
@@ -561,7 +569,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
 int pick_tpr(const CsrView* A) {
   static int env = -1;
   if (env < 0) {
-    const char* e = getenv("RKMF_PIPE_TPR");
+    const char* e = knob_env("RKMF_PIPE_TPR");
     env = e ? atoi(e) : 0;
   }
   if (env == 1 || env == 2 || env == 4) return env;
@@ -575,7 +583,7 @@ int pick_tpr(const CsrView* A) {
 int pick_groups(const CsrView* A) {
   static int env = -1;
   if (env < 0) {
-    const char* e = getenv("RKMF_PIPE_GROUPS");
+    const char* e = knob_env("RKMF_PIPE_GROUPS");
     env = e ? atoi(e) : 0;
   }
   if (env >= 1 && env <= 3) return env;
@@ -585,26 +593,26 @@ int pick_groups(const CsrView* A) {
 
 template <typename RP, int TPR>
 bool launch_pipe_g(const CsrView* A, const SketchView* S, const double* x,
-                   const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
-                   int step, cudaStream_t st) {
+                   const double* xscale_dev, double* z, const int32_t* stop,
+                   int step, DetRed& red, cudaStream_t st) {
   // at most 1024 threads per block: TPR 4 runs one group, TPR 2 up to three
   int g = pick_groups(A);
   while (g > 1 && g * kTileRows * TPR + kSketchThreads + 32 > 1024) --g;
   if (g >= 3 && TPR <= 2)
-    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 3 : 1)>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 3 : 1)>(A, S, x, xscale_dev, z, stop, step, red, st);
   if (g == 2 && TPR <= 2)
-    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 2 : 1)>(A, S, x, xscale_dev, z, pacc, stop, step, st);
-  return launch_pipe_t<RP, TPR, 1>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 2 : 1)>(A, S, x, xscale_dev, z, stop, step, red, st);
+  return launch_pipe_t<RP, TPR, 1>(A, S, x, xscale_dev, z, stop, step, red, st);
 }
 
 template <typename RP>
 bool launch_pipe_rp(const CsrView* A, const SketchView* S, const double* x,
-                    const double* xscale_dev, double* z, double* pacc, const int32_t* stop,
-                    int step, cudaStream_t st) {
+                    const double* xscale_dev, double* z, const int32_t* stop,
+                    int step, DetRed& red, cudaStream_t st) {
   switch (pick_tpr(A)) {
-    case 4: return launch_pipe_g<RP, 4>(A, S, x, xscale_dev, z, pacc, stop, step, st);
-    case 2: return launch_pipe_g<RP, 2>(A, S, x, xscale_dev, z, pacc, stop, step, st);
-    default: return launch_pipe_g<RP, 1>(A, S, x, xscale_dev, z, pacc, stop, step, st);
+    case 4: return launch_pipe_g<RP, 4>(A, S, x, xscale_dev, z, stop, step, red, st);
+    case 2: return launch_pipe_g<RP, 2>(A, S, x, xscale_dev, z, stop, step, red, st);
+    default: return launch_pipe_g<RP, 1>(A, S, x, xscale_dev, z, stop, step, red, st);
   }
 }
 
@@ -615,26 +623,22 @@ void trace_bind_spmv_pipe(unsigned long long* p) { trace_bind_tu(p); }
 // sketch of x alone through the same pipeline (no matrix stream): the start
 // vector's S*start (basis.cpp:103-104), mode 2 of launch_spmv_sketch
 bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double* xscale_dev,
-                             double* pacc, cudaStream_t st) {
+                             DetRed& red, cudaStream_t st) {
   // the diagonal path with one diagonal of ones: x staged by the same
   // prefetching SpMV threads, no matrix stream
   CsrView v{};
   v.n_rows = S->n;
   v.n_cols = S->n;
   v.ndiag = 1;
-  if (launch_spmv_rowsketch(&v, S, x, xscale_dev, nullptr, pacc, nullptr, 0, st)) return true;
-  return launch_pipe_t<int32_t, 1, 1, 2, 1>(&v, S, x, xscale_dev, nullptr, pacc, nullptr, 0, st);
+  return launch_pipe_t<int32_t, 1, 1, 2, 1>(&v, S, x, xscale_dev, nullptr, nullptr, 0, red, st);
 }
 
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
-                             const double* xscale_dev, double* z, double* pacc,
-                             const int32_t* stop_flag, int step, cudaStream_t st) {
-  if (A->ndiag > 0 && A->dval &&
-      launch_spmv_rowsketch(A, S, x, xscale_dev, z, pacc, stop_flag, step, st))
-    return true;
+                             const double* xscale_dev, double* z,
+                             const int32_t* stop_flag, int step, DetRed& red, cudaStream_t st) {
   if (A->ndiag > 0 && A->dval) {  // diagonal copy (at most 8 diagonals), x prefetched
 #define RKMF_DIA(NDV) \
-  case NDV: return launch_pipe_t<int32_t, 1, 1, 2, NDV>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
+  case NDV: return launch_pipe_t<int32_t, 1, 1, 2, NDV>(A, S, x, xscale_dev, z, stop_flag, step, red, st)
     switch (A->ndiag) {
       RKMF_DIA(1); RKMF_DIA(2); RKMF_DIA(3); RKMF_DIA(4);
       RKMF_DIA(5); RKMF_DIA(6); RKMF_DIA(7); RKMF_DIA(8);
@@ -643,8 +647,8 @@ bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double
 #undef RKMF_DIA
   }
   if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
-  return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st)
-                 : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, pacc, stop_flag, step, st);
+  return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, stop_flag, step, red, st)
+                 : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, stop_flag, step, red, st);
 }
 
 }  // namespace rkmf_b200

@@ -40,3 +40,10 @@ def oracle():
 def rk():
     import paper_2503_22631_b200 as rk
     return rk
+
+
+@pytest.fixture(scope="session")
+def torch():
+    import torch as T
+    assert T.cuda.is_available()
+    return T

@@ -41,13 +41,15 @@ def main():
     srows = [None] * world
     dist.all_gather_object(srows, (part.row_begin, rows, signs))
     norm1 = part.A.norm1
+    nd = [None] * world  # diagonal copy on every rank (halo diagonals included)
+    dist.all_gather_object(nd, part.A.ndiag)
     if rank == 0:
         rr = np.concatenate([x[1] for x in sorted(srows, key=lambda t: t[0])])
         ss = np.concatenate([x[2] for x in sorted(srows, key=lambda t: t[0])])
         np.savez(out, f=fg, cycles=r.cycles, converged=r.converged, total_m=r.total_m,
                  updates=np.array([h.update_norm for h in r.history]),
                  matvecs=r.counters["matvecs"], norm1=norm1, row_starts=part.row_starts,
-                 sketch_rows=rr, sketch_signs=ss)
+                 sketch_rows=rr, sketch_signs=ss, ndiag=np.array(nd))
     dist.barrier()
     dist.destroy_process_group()
 

@@ -618,50 +618,3 @@ def test_device_against_golden_fixtures(rk, torch):
         un = np.array([x.update_norm for x in r.history[:c]])
         ug = h[key + "_update_norm"][:c]
         assert np.all(np.abs(un - ug) <= 1e-8 * np.abs(ug) + 1e-12 * np.linalg.norm(P.b))
-
-
-# ---------------- opt-in row-sketch K2 (RKMF_ROWSKETCH=1, spmv_rowsketch.cu) ----------------
-_ROWSKETCH_SCRIPT = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, sys.argv[1])
-import paper_2503_22631_b200 as rk
-from paper_2503_22631_b200 import configs
-from oracle import oracle as O
-def rel(a, b):
-    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
-for name, N in (("cfg2", 33), ("cfg1", 100), ("cfg4", 21)):
-    P = configs.build(name, N)
-    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
-    S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED)
-    OS = O.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED)
-    x = torch.tensor(P.b, device="cuda")
-    # sketch alone (identity path) and fused SpMV + sketch
-    p = rk.sketch_apply(S, x).cpu().numpy()
-    assert rel(p, O.sketch_apply(OS, P.b)) <= 1e-13, (name, "sketch")
-    z, pz = rk.spmv_sketch(A, S, x)
-    zo = O.spmv((P.row_ptr, P.col_idx, P.values), P.b)
-    assert rel(z.cpu().numpy(), zo) <= 1e-14, (name, "spmv")
-    assert rel(pz.cpu().numpy(), O.sketch_apply(OS, zo)) <= 1e-13, (name, "fused sketch")
-    r = rk.restarted_krylov(A, x, rk.FunctionSpec.exp_neg(P.t),
-                            rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max), S)
-    o = O.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, O.KIND_EXP_NEG, P.t,
-                           m_r=P.m, tol=P.tol, k_max=P.k_max, S=OS)
-    assert r.converged and abs(r.cycles - o.cycles) <= 1, (name, r.cycles, o.cycles)
-    assert rel(r.f_hat.cpu().numpy(), o.f_hat) <= 1e-9, (name, "f")
-print("rowsketch ok")
-"""
-
-
-def test_rowsketch_path_matches_oracle(rk):
-    """The opt-in row-sketch K2 (edge-coloured slots, plain shared read-add-write)
-    against the oracle: sketch, fused SpMV + sketch, restarted solve."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, RKMF_ROWSKETCH="1", RKMF_PIPE_VERBOSE="1")
-    r = subprocess.run([sys.executable, "-c", _ROWSKETCH_SCRIPT, root], capture_output=True,
-                       text=True, timeout=600, env=env)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    assert "rowsketch ok" in r.stdout
-    assert "K2 row-sketch" in r.stderr  # the path actually ran

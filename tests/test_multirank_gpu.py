@@ -67,6 +67,10 @@ def test_partitioned_solve_matches_oracle(tmp_path, rk, oracle, name, N, world):
     f1 = r1.f_hat.cpu().numpy()
     assert np.linalg.norm(f - f1) <= 1e-9 * np.linalg.norm(f1)
     assert int(res["matvecs"]) == r1.counters["matvecs"]
+    if name in ("cfg1", "cfg2", "cfg4") and world == 2:
+        # stencils split on a grid plane: every rank streams a diagonal copy
+        # (rank 1's lower halo sits on its own diagonal, columns not monotone)
+        assert np.all(res["ndiag"] > 0), res["ndiag"]
 
 
 @pytest.mark.gpu
