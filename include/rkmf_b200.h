@@ -59,7 +59,9 @@ typedef struct {
   int64_t budget_total_m;
   double divergence_factor;
   int32_t dense_f;        /* RKMF_DENSE_* */
-  int32_t quad_nodes;     /* quadrature nodes (0 = default 512) */
+  int32_t quad_nodes;     /* InvSqrt quadrature nodes: 0 (default) = designed from
+                             the Ritz values of every cycle with node doubling
+                             (branch-cut guard); > 0 = that many fixed nodes */
   int32_t diagnostics;    /* 1: fill CycleRecord kappa_W / leftmost_ritz_re
                              (restart.cpp:101,103; one Gram pass over W_m per
                              cycle, m <= 64); 0 (default): NaN */
@@ -101,6 +103,7 @@ typedef struct {
   int64_t peak_basis_cols;
   int64_t n_records;
   double solve_ms; /* device time of the whole solve (CUDA events) */
+  int64_t quad_nodes; /* restart-quadrature nodes of the last cycle (0: FULL dense f) */
 } rkmf_restart_result;
 
 /* ---- context ---- */
@@ -143,6 +146,11 @@ int rkmf_matrix_info(const rkmf_matrix* A, int64_t* n_rows, int64_t* n_cols, int
  * drops the copy (CSR path only), 1 builds it if the matrix qualifies, 2
  * only queries; *ndiag (optional) receives the diagonal count, 0 = CSR only. */
 int rkmf_matrix_dia(rkmf_matrix* A, int enable, int* ndiag);
+/* Row-pointer width of the device CSR: stored as int32 when nnz < 2^31 - 1,
+ * else int64 (cfg5 on one GPU). enable != 0 widens an int32 matrix to int64
+ * so the int64 instantiations of the SpMV kernels run on small problems
+ * (testing; results are identical); *is64 (optional) receives the width. */
+int rkmf_matrix_rp64(rkmf_matrix* A, int enable, int* is64);
 /* Copies the device CSR to the host: h_row_ptr[n_rows+1] (int64),
  * h_col_idx[nnz], h_values[nnz] (sizes from rkmf_matrix_info; any pointer may
  * be NULL). A partitioned matrix exports its local rows in the local column
@@ -306,6 +314,39 @@ void rkmf_host_free(void* p);
  * matrix written back out (its CSR copied to the host first) */
 int rkmf_matrix_load_mtx(rkmf_context* ctx, const char* path, rkmf_matrix** out);
 int rkmf_matrix_save_mtx(rkmf_context* ctx, const rkmf_matrix* A, const char* path);
+
+/* ---- convergence sweep + CSV: restart::convergence_sweep / MethodSpec /
+ * SweepRecord (restart.hpp:81-129, restart.cpp:124-305) and the CLI's CSV
+ * (rkmf_bench.cpp:172-186). Methods "restart" (classical builder) and
+ * "restart-rand" (d = 16 m unless given) run on the device, one row per
+ * cycle; a failing or unsupported cell (the one-shot approximants "arnoldi",
+ * "incomplete", "rand", "rand-ls", "sfom" are not on the device path) becomes
+ * one NaN row carrying the sanitised message. Rows keep the method order;
+ * without timing the CSV is byte-identical across reruns. ---- */
+typedef struct {
+  char name[32];
+  int64_t m;    /* m_r */
+  int64_t d;    /* sketch rows, 0 = 16 m (restart.cpp:231-232) */
+  int64_t zeta; /* reference default 4 */
+  double tol;   /* absolute, reference default 1e-10 */
+  int64_t k_max;
+  uint64_t seed;
+} rkmf_method_spec;
+typedef struct {
+  char method[32];
+  int64_t n, m_or_totalm, cycle, matvecs;
+  double rel_error, update_norm, kappa_W, leftmost_ritz_re, elapsed_ms;
+  char note[256];
+  double phase_build_ms, phase_eval_ms; /* not CSV columns (the CLI's timing summary) */
+} rkmf_sweep_record;
+/* h_b, h_reference (optional): host vectors; out: cap records, *n_out the count */
+int rkmf_convergence_sweep(rkmf_context* ctx, const rkmf_matrix* A, const double* h_b,
+                           int32_t fn_kind, double fn_t, const double* h_reference,
+                           const rkmf_method_spec* methods, int64_t n_methods, int32_t with_timing,
+                           rkmf_sweep_record* out, int64_t cap, int64_t* n_out);
+/* fixed header, %.17g numbers; path NULL or "" = stdout */
+int rkmf_sweep_write_csv(const rkmf_sweep_record* rows, int64_t n_rows, const char* path,
+                         char* err, int64_t err_cap);
 
 /* R_accum of the last solve on this context (total_m x total_m, column-major,
  * host); n_cap is the caller's capacity in rows. */

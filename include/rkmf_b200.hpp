@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -39,6 +40,10 @@ class DeviceError : public Error {
  public:
   explicit DeviceError(const std::string& m) : Error(m) {}
 };
+class ParseError : public Error {
+ public:
+  explicit ParseError(const std::string& m) : Error(m) {}
+};
 
 inline void check(rkmf_context* ctx, int code) {
   if (code == RKMF_OK) return;
@@ -48,6 +53,16 @@ inline void check(rkmf_context* ctx, int code) {
     case RKMF_SHAPE_ERROR: throw ShapeError(msg);
     case RKMF_NUMERICAL_ERROR: throw NumericalError(msg);
     case RKMF_DEVICE_ERROR: throw DeviceError(msg);
+    case RKMF_PARSE_ERROR: throw ParseError(msg);
+    default: throw Error(msg);
+  }
+}
+inline void check_msg(int code, const char* msg) {  // host-only calls with an err buffer
+  if (code == RKMF_OK) return;
+  switch (code) {
+    case RKMF_PARAMETER_ERROR: throw ParameterError(msg);
+    case RKMF_SHAPE_ERROR: throw ShapeError(msg);
+    case RKMF_PARSE_ERROR: throw ParseError(msg);
     default: throw Error(msg);
   }
 }
@@ -78,6 +93,47 @@ struct SparseMatrix {
   std::vector<double> values;
   int64_t nnz() const { return static_cast<int64_t>(values.size()); }
 };
+
+// ---- sparse.hpp:55-66: Matrix Market / vector interchange (host) ----
+inline SparseMatrix load_matrix_market(const std::string& path) {
+  int64_t nr = 0, nc = 0, nnz = 0;
+  int64_t* rp = nullptr;
+  int32_t* ci = nullptr;
+  double* v = nullptr;
+  char err[1024] = {0};
+  check_msg(rkmf_mtx_load(path.c_str(), &nr, &nc, &nnz, &rp, &ci, &v, err, sizeof(err)), err);
+  SparseMatrix A;
+  A.n_rows = nr;
+  A.n_cols = nc;
+  A.row_ptr.assign(rp, rp + nr + 1);
+  A.col_idx.assign(ci, ci + nnz);
+  A.values.assign(v, v + nnz);
+  rkmf_host_free(rp);
+  rkmf_host_free(ci);
+  rkmf_host_free(v);
+  return A;
+}
+inline void save_matrix_market(const SparseMatrix& A, const std::string& path) {
+  char err[1024] = {0};
+  check_msg(rkmf_mtx_save(path.c_str(), A.n_rows, A.n_cols, A.row_ptr.data(), A.col_idx.data(),
+                          A.values.data(), err, sizeof(err)),
+            err);
+}
+inline std::vector<double> load_vector(const std::string& path) {
+  int64_t n = 0;
+  double* p = nullptr;
+  char err[1024] = {0};
+  check_msg(rkmf_vector_load(path.c_str(), &n, &p, err, sizeof(err)), err);
+  std::vector<double> v(p, p + n);
+  rkmf_host_free(p);
+  return v;
+}
+inline void save_vector(const std::vector<double>& v, const std::string& path) {
+  char err[1024] = {0};
+  check_msg(rkmf_vector_save(path.c_str(), static_cast<int64_t>(v.size()), v.data(), err,
+                             sizeof(err)),
+            err);
+}
 
 // Device-resident copy of a SparseMatrix (validated on upload, sparse.cpp:61-81).
 class DeviceMatrix {
@@ -142,7 +198,22 @@ struct RestartOptions {
   int64_t budget_total_m = 4000;
   double divergence_factor = 1e6;
   int32_t dense_f = RKMF_DENSE_AUTO;
+  int32_t quad_nodes = 0;   // InvSqrt: 0 = adaptive (Ritz-designed, node doubling)
+  bool diagnostics = false;  // kappa_W / leftmost_ritz_re per cycle
 };
+
+// ---- restart.hpp:42-54: test-only observer, fed by device->host copies ----
+struct CycleInfo {
+  int64_t cycle;
+  int64_t n, m_k, w_cols;
+  const double* W;  // n x w_cols column-major
+  int64_t total_m;
+  const double* R_accum;  // total_m x total_m column-major, or nullptr
+  const double* update;
+  const double* f_hat;
+  double alpha;
+};
+using CycleObserver = std::function<void(const CycleInfo&)>;
 
 struct CycleRecord {
   int64_t cycle = 0, total_m = 0;
@@ -168,10 +239,14 @@ struct RestartResult {
   PerfCounters counters;
 };
 
-// restart::restarted_krylov (restart.hpp:74-79) with S != nullptr.
+// restart::restarted_krylov (restart.hpp:74-79): S == nullptr selects the
+// classical builder (restart.cpp:53-55), otherwise the randomized one with the
+// same sketch every cycle; observer is the reference's test-only CycleObserver.
 inline RestartResult restarted_krylov(const Context& ctx, const DeviceMatrix& A,
                                       const std::vector<double>& b, const FunctionSpec& f,
-                                      const RestartOptions& opts, const SketchOperator& S,
+                                      const RestartOptions& opts,
+                                      const SketchOperator* S = nullptr,
+                                      const CycleObserver& observer = nullptr,
                                       const std::vector<double>* reference = nullptr) {
   rkmf_restart_options o;
   rkmf_restart_options_default(&o);
@@ -181,14 +256,28 @@ inline RestartResult restarted_krylov(const Context& ctx, const DeviceMatrix& A,
   o.budget_total_m = opts.budget_total_m;
   o.divergence_factor = opts.divergence_factor;
   o.dense_f = opts.dense_f;
+  o.quad_nodes = opts.quad_nodes;
+  o.diagnostics = opts.diagnostics ? 1 : 0;
   RestartResult res;
   res.f_hat.assign(b.size(), 0.0);
   std::vector<rkmf_cycle_record> recs(static_cast<size_t>(std::max<int64_t>(opts.k_max, 1)) + 1);
   rkmf_restart_result r{};
-  check(ctx.get(), rkmf_restarted_krylov(ctx.get(), A.get(), S.get(), b.data(), 0, f.kind, f.t,
-                                         &o, res.f_hat.data(), 0,
+  struct Tramp {
+    static void call(void* user, const rkmf_cycle_info* i) {
+      const CycleInfo c{i->cycle, i->n,       i->m_k,    i->w_cols, i->W,
+                        i->total_m, i->R_accum, i->update, i->f_hat,  i->alpha};
+      (*static_cast<const CycleObserver*>(user))(c);
+    }
+  };
+  if (observer)
+    check(ctx.get(), rkmf_context_set_observer(ctx.get(), &Tramp::call,
+                                               const_cast<CycleObserver*>(&observer)));
+  const int code = rkmf_restarted_krylov(ctx.get(), A.get(), S ? S->get() : nullptr, b.data(), 0,
+                                         f.kind, f.t, &o, res.f_hat.data(), 0,
                                          reference ? reference->data() : nullptr, &r, recs.data(),
-                                         static_cast<int64_t>(recs.size())));
+                                         static_cast<int64_t>(recs.size()));
+  if (observer) rkmf_context_set_observer(ctx.get(), nullptr, nullptr);
+  check(ctx.get(), code);
   res.converged = r.converged != 0;
   res.alpha = r.alpha;
   res.cycles = r.cycles;
@@ -217,6 +306,14 @@ inline RestartResult restarted_krylov(const Context& ctx, const DeviceMatrix& A,
     check(ctx.get(), rkmf_last_r_accum(ctx.get(), res.R_accum.data(), M, &M));
   }
   return res;
+}
+
+// the randomized builder with S by reference (round-1 signature)
+inline RestartResult restarted_krylov(const Context& ctx, const DeviceMatrix& A,
+                                      const std::vector<double>& b, const FunctionSpec& f,
+                                      const RestartOptions& opts, const SketchOperator& S,
+                                      const std::vector<double>* reference = nullptr) {
+  return restarted_krylov(ctx, A, b, f, opts, &S, nullptr, reference);
 }
 
 }  // namespace rkmf_b200

@@ -90,7 +90,7 @@ class RestartResultC(C.Structure):
                 ("alpha", C.c_double), ("matvecs", C.c_int64), ("dot_n", C.c_int64),
                 ("dot_d", C.c_int64), ("basis_updates", C.c_int64),
                 ("peak_basis_cols", C.c_int64), ("n_records", C.c_int64),
-                ("solve_ms", C.c_double)]
+                ("solve_ms", C.c_double), ("quad_nodes", C.c_int64)]
 
 
 class CycleInfoC(C.Structure):
@@ -149,6 +149,7 @@ SYMBOLS = [
     ("rkmf_matrix_gen_laplacian", C.c_int, [_P, _I32, _I64, _PP]),
     ("rkmf_gen_gaussian_device", C.c_int, [_P, _U64, _I64, _I64, _P]),
     ("rkmf_matrix_export", C.c_int, [_P, _P, _P, _P, _P]),
+    ("rkmf_matrix_rp64", C.c_int, [_P, C.c_int, _P]),
     ("rkmf_matrix_gen_convdiff", C.c_int, [_P, _I64, _D, _D, _D, _D, _PP]),
     ("rkmf_matrix_gen_q1_hex_partitioned", C.c_int, [_P, _I64, _I32, _U64, _I32, _P, _PP]),
     ("rkmf_context_comm_info", C.c_int, [_P, _P, _P, _P]),
@@ -180,6 +181,10 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"rkmf_b200 CUDA library not built: {LIB_PATH} "
                               "(run paper_2503_22631_b200.build() or __graft_entry__.build())")
+        try:  # torch first: the library's libnccl.so.2 then binds to torch's
+            import torch  # noqa: F401  (newer) NCCL instead of the system one
+        except ImportError:
+            pass
         L = C.CDLL(LIB_PATH)
         for name, res, args in SYMBOLS:
             fn = getattr(L, name)
@@ -285,6 +290,19 @@ class SparseMatrix:
         nd = C.c_int()
         self.ctx.check(lib().rkmf_matrix_dia(self.h, int(bool(enable)), C.byref(nd)))
         return nd.value
+
+    def use_rp64(self) -> bool:
+        """Widen the device row pointers to int64 (the storage cfg5's 3.6e9
+        nonzeros need) so the int64 kernel instantiations run; returns the width."""
+        w = C.c_int()
+        self.ctx.check(lib().rkmf_matrix_rp64(self.h, 1, C.byref(w)))
+        return bool(w.value)
+
+    @property
+    def rp64(self) -> bool:
+        w = C.c_int()
+        self.ctx.check(lib().rkmf_matrix_rp64(self.h, 0, C.byref(w)))
+        return bool(w.value)
 
     @property
     def ndiag(self) -> int:
@@ -631,6 +649,7 @@ class RestartResult:
     total_m: int
     counters: dict
     solve_ms: float
+    quad_nodes: int = 0  # restart-quadrature nodes of the last cycle (0: FULL)
     _ctx: Context = field(repr=False, default=None)
     _R: Optional[np.ndarray] = field(repr=False, default=None)
     _solve_id: int = field(repr=False, default=-1)
@@ -715,7 +734,8 @@ def restarted_krylov(A: SparseMatrix, b, f: FunctionSpec, opts: RestartOptions =
                          counters=dict(matvecs=res.matvecs, dot_n=res.dot_n, dot_d=res.dot_d,
                                        basis_updates=res.basis_updates,
                                        peak_basis_cols=res.peak_basis_cols),
-                         solve_ms=res.solve_ms, _ctx=ctx, _solve_id=ctx.solves)
+                         solve_ms=res.solve_ms, quad_nodes=res.quad_nodes, _ctx=ctx,
+                         _solve_id=ctx.solves)
     if keep_R_accum:
         _ = out_res.R_accum
     return out_res

@@ -38,15 +38,24 @@ __device__ __forceinline__ double block_sum_d(double v, double* buf) {
   return s;  // valid in thread 0
 }
 
-// out += ||x||^2 (out zeroed by the caller)
-__global__ void norm2_kernel(int64_t n, const double* __restrict__ x, double* out) {
+// block sum (valid in thread 0) -> *out in a fixed block order (detred.cuh)
+__device__ __forceinline__ void det_scalar(double s, const DetRed& red, double* out) {
+  __shared__ double mine[1];
+  __shared__ int flag;
+  if (threadIdx.x == 0) mine[0] = s;
+  __syncthreads();
+  det_reduce<kThreads, 0>(red, 1, mine, out, int(threadIdx.x), &flag);
+}
+
+// *out = ||x||^2
+__global__ void norm2_kernel(int64_t n, const double* __restrict__ x, double* out, DetRed red) {
   __shared__ double buf[kThreads / 32];
   double s = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * kThreads + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * kThreads)
     s += x[i] * x[i];
   s = block_sum_d(s, buf);
-  if (threadIdx.x == 0) atomicAdd(out, s);
+  det_scalar(s, red, out);
 }
 
 // beta = ||start|| (basis.cpp:38-40); the same state fields as start_init
@@ -64,9 +73,11 @@ __global__ void cl_start_kernel(double* nrm2, SolveState* st, int first, int m_e
   st->err2 = 0.0;
 }
 
-// h[i] += <W[:,i], z> for i <= k; blockIdx.y = column, grid-stride over rows
+// h[i] = <W[:,i], z> for i <= k; blockIdx.y = column (one reduction slice
+// each), grid-stride over rows
 __global__ void multidot_kernel(int64_t n, int k, int64_t ldw, const double* __restrict__ W,
-                                const double* __restrict__ z, double* h, const SolveState* st) {
+                                const double* __restrict__ z, double* h, const SolveState* st,
+                                DetRed red) {
   if (st->stopped <= k) return;
   __shared__ double buf[kThreads / 32];
   const int i = blockIdx.y;
@@ -81,13 +92,13 @@ __global__ void multidot_kernel(int64_t n, int k, int64_t ldw, const double* __r
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) s += w[n - 1] * z[n - 1];
   s = block_sum_d(s, buf);
-  if (threadIdx.x == 0) atomicAdd(h + i, i == 0 ? s * st->sigma : s);
+  det_scalar(i == 0 ? s * st->sigma : s, red, h + i);
 }
 
-// z -= W[:,0..k] h (store != 0), and nrm2 += ||z - W h||^2 when nrm2 != null
+// z -= W[:,0..k] h (store != 0), and *nrm2 = ||z - W h||^2 when nrm2 != null
 __global__ void cgs_update_kernel(int64_t n, int k, int64_t ldw, const double* __restrict__ W,
                                   double* z, const double* __restrict__ h, double* nrm2,
-                                  int store, const SolveState* st) {
+                                  int store, const SolveState* st, DetRed red) {
   if (st->stopped <= k) return;
   __shared__ double coef[kMaxCols];
   __shared__ double buf[kThreads / 32];
@@ -130,7 +141,7 @@ __global__ void cgs_update_kernel(int64_t n, int k, int64_t ldw, const double* _
   }
   if (nrm2) {
     ss = block_sum_d(ss, buf);
-    if (threadIdx.x == 0) atomicAdd(nrm2, ss);
+    det_scalar(ss, red, nrm2);
   }
 }
 
@@ -184,11 +195,18 @@ int grid_rows(int64_t n) {
 
 }  // namespace
 
+void check_red(const DetRed& red, int64_t blocks, int64_t slices) {
+  if (blocks * slices > red.max_blocks || red.max_len < 1 ||
+      (det_groups(int(blocks)) + 1) * slices > red.max_groups)
+    param_error("internal: classical reduction scratch too small");
+}
+
 void launch_cl_start(int64_t n, const double* start, double* nrm2_scratch, SolveState* st_dev,
-                     bool first, int m_eff, bool norm_only, cudaStream_t st) {
+                     bool first, int m_eff, bool norm_only, const DetRed& red, cudaStream_t st) {
   if (norm_only) {
-    RKMF_CUDA(cudaMemsetAsync(nrm2_scratch, 0, sizeof(double), st));
-    norm2_kernel<<<grid_rows(2 * n), kThreads, 0, st>>>(n, start, nrm2_scratch);
+    const int g = grid_rows(2 * n);
+    check_red(red, g, 1);
+    norm2_kernel<<<g, kThreads, 0, st>>>(n, start, nrm2_scratch, red);
   } else {
     cl_start_kernel<<<1, 1, 0, st>>>(nrm2_scratch, st_dev, first ? 1 : 0, m_eff);
   }
@@ -196,18 +214,21 @@ void launch_cl_start(int64_t n, const double* start, double* nrm2_scratch, Solve
 }
 
 void launch_cl_multidot(int64_t n, int k, int64_t ldw, const double* W, const double* z,
-                        double* h, const SolveState* st_dev, cudaStream_t st) {
+                        double* h, const SolveState* st_dev, const DetRed& red, cudaStream_t st) {
   if (k + 1 > kMaxCols) param_error("arnoldi: m > 1024 is not supported on device");
   const int gx = std::max(1, grid_rows(n) / std::max(1, (k + 1) / 4 + 1));
+  check_red(red, gx, k + 1);
   multidot_kernel<<<dim3(unsigned(gx), unsigned(k + 1)), kThreads, 0, st>>>(n, k, ldw, W, z, h,
-                                                                             st_dev);
+                                                                             st_dev, red);
   RKMF_CUDA(cudaGetLastError());
 }
 
 void launch_cl_update(int64_t n, int k, int64_t ldw, const double* W, double* z, const double* h,
-                      double* nrm2, bool store, const SolveState* st_dev, cudaStream_t st) {
-  cgs_update_kernel<<<grid_rows(n), kThreads, 0, st>>>(n, k, ldw, W, z, h, nrm2, store ? 1 : 0,
-                                                       st_dev);
+                      double* nrm2, bool store, const SolveState* st_dev, const DetRed& red,
+                      cudaStream_t st) {
+  const int g = grid_rows(n);
+  if (nrm2) check_red(red, g, 1);
+  cgs_update_kernel<<<g, kThreads, 0, st>>>(n, k, ldw, W, z, h, nrm2, store ? 1 : 0, st_dev, red);
   RKMF_CUDA(cudaGetLastError());
 }
 

@@ -220,15 +220,17 @@ __global__ void __launch_bounds__(32)
     quad_invsqrt_kernel(const double* __restrict__ Rbar, int64_t ldr, int mkmax,
                         const double* __restrict__ shift, const double* __restrict__ weight,
                         double* pi, double* emx, int64_t cycle, const SolveState* st,
-                        double* partial) {
+                        double* partial, int mk_in, double coupling_in) {
+  // mk_in >= 0: replay of a past cycle (its block of R_accum and its coupling
+  // R_accum(M, M-1)) to rebuild the node states of a new node set
   extern __shared__ double Ms[];  // mk x mk, column-major
   __shared__ double rhs[kMaxM];
   const int q = blockIdx.x, lane = threadIdx.x;
-  const int mk = st->stopped;
+  const int mk = mk_in >= 0 ? mk_in : st->stopped;
   const double sg = shift[q];
   // couple to the previous cycle: pi_q *= -c_{k-1} (c = subdiag * alpha_k)
   double piq = pi[q];
-  if (cycle > 1) piq *= -(st->coupling * st->alpha_k) * emx[q];
+  if (cycle > 1) piq *= -(mk_in >= 0 ? coupling_in : st->coupling * st->alpha_k) * emx[q];
   for (int64_t e = lane; e < int64_t(mk) * mk; e += 32) {
     const int i = int(e % mk), j = int(e / mk);
     Ms[e] = Rbar[int64_t(j) * ldr + i] + (i == j ? sg : 0.0);
@@ -259,7 +261,9 @@ __global__ void __launch_bounds__(32)
     __syncwarp();
   }
   const double wq = weight[q] * piq;
-  for (int j = lane; j < mkmax; j += 32) partial[int64_t(q) * mkmax + j] = j < mk ? wq * rhs[j] : 0.0;
+  if (partial)
+    for (int j = lane; j < mkmax; j += 32)
+      partial[int64_t(q) * mkmax + j] = j < mk ? wq * rhs[j] : 0.0;
   if (lane == 0) {
     pi[q] = piq;
     emx[q] = rhs[mk - 1];
@@ -359,6 +363,48 @@ int grid_for(int64_t work) {
 }
 
 }  // namespace
+
+// z^{-1/2} = (2/pi) int_R e^u (z + e^{2u})^{-1} du, midpoint trapezoid on
+// [u0, u1]. For a Ritz value lambda = |lambda| e^{i theta} the
+// integrand's poles sit (pi - theta)/2 from the real u axis, so the
+// discretisation error is ~ exp(-pi (pi - theta) / h): h = pi (pi - theta)/38
+// (capped at 0.25) gives ~1e-16; the tails are below 1e-16 relative once u0 <=
+// ln|lambda|_min / 2 - 38 and u1 >= ln|lambda|_max / 2 + 38. The design takes
+// the extremes over every cycle's Ritz values with a 4x modulus and 0.1 rad
+// angle margin; R_accum is block lower-bidiagonal, so its spectrum is exactly
+// the union of the cycles' Ritz values.
+InvSqrtDesign design_invsqrt(double lmin, double lmax, double thmax) {
+  InvSqrtDesign d;
+  d.lmin = lmin / 4.0;
+  d.lmax = lmax * 4.0;
+  d.thmax = std::min(thmax + 0.1, M_PI - 1e-3);
+  d.h = std::min(0.25, M_PI * (M_PI - d.thmax) / 38.0);
+  d.u0 = 0.5 * std::log(d.lmin) - 38.0;
+  const double u1 = 0.5 * std::log(d.lmax) + 38.0;
+  d.nq = int(std::ceil((u1 - d.u0) / d.h));
+  return d;
+}
+
+bool InvSqrtDesign::covers(double lo, double hi, double th) const {
+  return lo >= lmin && hi <= lmax && th <= thmax;
+}
+
+InvSqrtDesign InvSqrtDesign::doubled() const {
+  InvSqrtDesign d = *this;
+  d.h = h / 2.0;
+  d.nq = 2 * nq;
+  return d;
+}
+
+void invsqrt_nodes(const InvSqrtDesign& d, std::vector<double>& shift, std::vector<double>& weight) {
+  shift.resize(size_t(d.nq));
+  weight.resize(size_t(d.nq));
+  for (int i = 0; i < d.nq; ++i) {
+    const double u = d.u0 + (double(i) + 0.5) * d.h;
+    shift[size_t(i)] = std::exp(2.0 * u);
+    weight[size_t(i)] = (2.0 / M_PI) * d.h * std::exp(u);
+  }
+}
 
 // Contour for exp(-t z) over the t-scaled spectrum (z = t lambda): the parabola
 // zeta(u) = x0 + p u^2 + i q u, u in R, opening to the right where e^{-zeta}
@@ -515,15 +561,18 @@ void launch_make_g(const double* u, int64_t M, int /*mk*/, double* g, const Solv
 
 void launch_quad_invsqrt_cycle(const double* Rbar, int64_t ldr, int mkmax, int64_t cycle,
                                QuadState* q, double* g, const SolveState* st_dev,
-                               double* partial, cudaStream_t st) {
+                               double* partial, cudaStream_t st, int mk_replay,
+                               double coupling_replay) {
   if (mkmax > kMaxM) param_error("quadrature: m_r > 128 is not supported");
   const size_t smem = sizeof(double) * size_t(mkmax) * size_t(mkmax);
   if (smem > 48 * 1024)
     RKMF_CUDA(cudaFuncSetAttribute(quad_invsqrt_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const bool replay = mk_replay >= 0;
   quad_invsqrt_kernel<<<q->nq, 32, smem, st>>>(Rbar, ldr, mkmax, q->shift, q->weight, q->pi,
-                                                q->emx, cycle, st_dev, partial);
-  quad_reduce_kernel<<<1, 128, 0, st>>>(q->nq, mkmax, partial, g, st_dev);
+                                                q->emx, cycle, st_dev, replay ? nullptr : partial,
+                                                mk_replay, coupling_replay);
+  if (!replay) quad_reduce_kernel<<<1, 128, 0, st>>>(q->nq, mkmax, partial, g, st_dev);
   RKMF_CUDA(cudaGetLastError());
 }
 

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -224,15 +225,17 @@ void run_steps_classical(rkmf_context* ctx, const rkmf_matrix* A, const SolveBuf
       launch_spmv_sketch(&A->view, nullptr, 0, x, k == 0 ? &ctx->st_dev->sigma : nullptr, b.z,
                          stop, int(k), grid, none, st);
     });
-    ctx->timed(1, [&] { launch_cl_multidot(b.n, int(k), b.ldw, b.W, b.z, h1, ctx->st_dev, st); });
+    const DetRed& rcl = ctx->red_classical(b.m_eff + 1);
+    const DetRed& rsc = ctx->red_update();
+    ctx->timed(1, [&] { launch_cl_multidot(b.n, int(k), b.ldw, b.W, b.z, h1, ctx->st_dev, rcl, st); });
     comm_allreduce_sum(ctx, h1, size_t(k + 1));
     ctx->timed(2, [&] {
-      launch_cl_update(b.n, int(k), b.ldw, b.W, b.z, h1, nullptr, true, ctx->st_dev, st);
+      launch_cl_update(b.n, int(k), b.ldw, b.W, b.z, h1, nullptr, true, ctx->st_dev, rsc, st);
     });
-    ctx->timed(1, [&] { launch_cl_multidot(b.n, int(k), b.ldw, b.W, b.z, h2, ctx->st_dev, st); });
+    ctx->timed(1, [&] { launch_cl_multidot(b.n, int(k), b.ldw, b.W, b.z, h2, ctx->st_dev, rcl, st); });
     comm_allreduce_sum(ctx, h2, size_t(k + 1));
     ctx->timed(2, [&] {
-      launch_cl_update(b.n, int(k), b.ldw, b.W, b.z, h2, nrm2, !last, ctx->st_dev, st);
+      launch_cl_update(b.n, int(k), b.ldw, b.W, b.z, h2, nrm2, !last, ctx->st_dev, rsc, st);
     });
     comm_allreduce_sum(ctx, nrm2, 1);
     ctx->timed(1, [&] {
@@ -253,14 +256,47 @@ void run_steps_classical(rkmf_context* ctx, const rkmf_matrix* A, const SolveBuf
 void start_classical(rkmf_context* ctx, const SolveBuffers& b, double* cl, bool first) {
   double* nrm2 = cl + 2 * b.ldr;
   ctx->timed(5, [&] {
-    launch_cl_start(b.n, b.W, nrm2, ctx->st_dev, first, int(b.m_eff), true, ctx->stream);
+    launch_cl_start(b.n, b.W, nrm2, ctx->st_dev, first, int(b.m_eff), true, ctx->red_update(),
+                    ctx->stream);
   });
   comm_allreduce_sum(ctx, nrm2, 1);
   ctx->timed(5, [&] {
-    launch_cl_start(b.n, b.W, nrm2, ctx->st_dev, first, int(b.m_eff), false, ctx->stream);
+    launch_cl_start(b.n, b.W, nrm2, ctx->st_dev, first, int(b.m_eff), false, ctx->red_update(),
+                    ctx->stream);
   });
   ctx->launches += 2;
 }
+
+// One node set of the adaptive InvSqrt restart quadrature (densef.cu): the
+// nodes of an InvSqrtDesign, their running states, the partial sums and the
+// g it produces.
+struct QuadSet {
+  rkmf_context::QuadBufs* buf = nullptr;
+  QuadState q{};
+  InvSqrtDesign d;
+  double* partial = nullptr;
+  double* g = nullptr;
+  // stream-ordered (the context stream is non-blocking: a legacy-stream
+  // cudaMemcpy would not wait for its kernels)
+  void load(const InvSqrtDesign& dd, int64_t m_eff, cudaStream_t st) {
+    d = dd;
+    std::vector<double> hs, hw;
+    invsqrt_nodes(d, hs, hw);
+    const std::vector<double> ones(hs.size(), 1.0);
+    const size_t nb = sizeof(double) * hs.size();
+    q.nq = d.nq;
+    q.shift = static_cast<double*>(buf->shift.ensure(nb));
+    q.weight = static_cast<double*>(buf->weight.ensure(nb));
+    q.pi = static_cast<double*>(buf->pi.ensure(nb));
+    q.emx = static_cast<double*>(buf->emx.ensure(nb));
+    partial = static_cast<double*>(buf->partial.ensure(nb * size_t(m_eff)));
+    g = static_cast<double*>(buf->g.ensure(sizeof(double) * size_t(m_eff)));
+    RKMF_CUDA(cudaMemcpyAsync(q.shift, hs.data(), nb, cudaMemcpyHostToDevice, st));
+    RKMF_CUDA(cudaMemcpyAsync(q.weight, hw.data(), nb, cudaMemcpyHostToDevice, st));
+    RKMF_CUDA(cudaMemcpyAsync(q.pi, ones.data(), nb, cudaMemcpyHostToDevice, st));
+    RKMF_CUDA(cudaStreamSynchronize(st));  // the host vectors die here
+  }
+};
 
 // S * start (basis.cpp:103-104) into the start-sketch group partials
 // (ctx->red_st), summed by start_init
@@ -379,7 +415,8 @@ int rkmf_context_destroy(rkmf_context* ctx) {
   if (!ctx) return RKMF_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->redbuf, &ctx->pfin_sk, &ctx->pfin_st, &ctx->z, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
+  for (auto& qb : ctx->isq) qb.release();
+  for (DevBuf* b : {&ctx->redbuf, &ctx->redcl, &ctx->pfin_sk, &ctx->pfin_st, &ctx->z, &ctx->W, &ctx->U, &ctx->Rbar, &ctx->Racc,
                     &ctx->ws, &ctx->u, &ctx->g, &ctx->fhat, &ctx->ref, &ctx->partial,
                     &ctx->qshift, &ctx->qweight, &ctx->qpi, &ctx->qemx, &ctx->scratch, &ctx->gram,
                     &ctx->cl, &ctx->diag})
@@ -624,6 +661,36 @@ int rkmf_matrix_save_mtx(rkmf_context* ctx, const rkmf_matrix* M, const char* pa
     const int c2 = rkmf_mtx_save(path, n, M->view.n_cols, rp.data(), ci.data(), v.data(), err,
                                  sizeof(err));
     if (c2 != RKMF_OK) throw Error(c2, err);
+  });
+}
+
+__global__ void rp_widen_kernel(int64_t n, const int32_t* __restrict__ src, int64_t* dst) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+int rkmf_matrix_rp64(rkmf_matrix* M, int enable, int* is64) {
+  if (!M) return RKMF_PARAMETER_ERROR;
+  return guarded(M->ctx, [&] {
+    set_device(M->ctx);
+    if (enable && !M->view.rp64) {
+      const int64_t n = M->view.n_rows;
+      const size_t elems = size_t(n + 1 + kRpPad);
+      int64_t* rp = nullptr;
+      RKMF_CUDA(cudaMalloc(&rp, sizeof(int64_t) * elems));
+      cudaStream_t st = M->ctx->stream;
+      RKMF_CUDA(cudaMemsetAsync(rp, 0, sizeof(int64_t) * elems, st));
+      rp_widen_kernel<<<256, 256, 0, st>>>(n, static_cast<const int32_t*>(M->rp), rp);
+      RKMF_CUDA(cudaGetLastError());
+      RKMF_CUDA(cudaStreamSynchronize(st));
+      RKMF_CUDA(cudaFree(M->rp));
+      M->rp = rp;
+      M->view.row_ptr = rp;
+      M->view.rp64 = true;
+      M->ctx->launches++;
+    }
+    if (is64) *is64 = M->view.rp64 ? 1 : 0;
   });
 }
 
@@ -979,8 +1046,17 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     };
     QuadState q{};
     double* partial = nullptr;
-    if (dense == RKMF_DENSE_QUADRATURE && fn_kind == RKMF_FN_INV_SQRT) {
-      q.nq = opts.quad_nodes > 0 ? opts.quad_nodes : 512;
+    // InvSqrt: quad_nodes > 0 fixes the node count on the interval
+    // [0.5 ln(||A||_1 1e-14) - 37, 0.5 ln ||A||_1 + 37]; the default (0) designs
+    // the nodes from the Ritz values with node doubling (adaptive below)
+    const bool isq_adaptive = fn_kind == RKMF_FN_INV_SQRT && opts.quad_nodes <= 0;
+    QuadSet qa, qb;
+    qa.buf = &ctx->isq[0];
+    qb.buf = &ctx->isq[1];
+    double s_lmin = std::numeric_limits<double>::infinity(), s_lmax = 0.0, s_th = 0.0;
+    int64_t isq_nodes = 0;
+    if (dense == RKMF_DENSE_QUADRATURE && fn_kind == RKMF_FN_INV_SQRT && !isq_adaptive) {
+      q.nq = opts.quad_nodes;
       q.shift = static_cast<double*>(ctx->qshift.ensure(sizeof(double) * size_t(q.nq)));
       q.weight = static_cast<double*>(ctx->qweight.ensure(sizeof(double) * size_t(q.nq)));
       q.pi = static_cast<double*>(ctx->qpi.ensure(sizeof(double) * size_t(q.nq)));
@@ -1077,12 +1153,98 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       }
       if (dense == RKMF_DENSE_FULL || exp_fallback) {
         full_expneg();
-      } else if (fn_kind == RKMF_FN_INV_SQRT) {
+      } else if (fn_kind == RKMF_FN_INV_SQRT && !isq_adaptive) {
         ctx->timed(3, [&] {
           launch_quad_invsqrt_cycle(bb.Rbar, bb.ldr, int(m_eff), k, &q, g, ctx->st_dev, partial,
                                     st);
         });
         ctx->launches += 2;
+      } else if (fn_kind == RKMF_FN_INV_SQRT) {
+        // Adaptive restart quadrature for z^{-1/2}. The
+        // spectrum of R_accum is the union of the cycles' Ritz values (it is
+        // block lower-bidiagonal): each cycle's are checked against the
+        // branch cut (-inf, 0] and, when they leave the node design, the
+        // nodes are redesigned from all values seen and the earlier cycles are
+        // replayed into the new node states (R_accum kept on device). A new
+        // design is verified by node doubling: the cycle's g from the set and
+        // from the set at half the step must agree to 1e-12, else the finer
+        // set is taken and checked in turn.
+        ctx->sync_state();
+        const int mk = ctx->st_host->stopped;
+        std::vector<double> Rh(size_t(bb.ldr) * size_t(m_eff)), wr, wi;
+        RKMF_CUDA(cudaMemcpy(Rh.data(), bb.Rbar, sizeof(double) * Rh.size(), cudaMemcpyDeviceToHost));
+        ritz_values(Rh, bb.ldr, mk, wr, wi);
+        double clo = std::numeric_limits<double>::infinity(), chi = 0.0, cth = 0.0;
+        for (size_t i = 0; i < wr.size(); ++i) {
+          const double mod = std::hypot(wr[i], wi[i]), th = std::atan2(std::fabs(wi[i]), wr[i]);
+          if (!(mod > 0.0) || !std::isfinite(mod) || th > M_PI - 1e-3) {
+            char v[96];
+            std::snprintf(v, sizeof(v), "%.6g%+.6gi", wr[i], wi[i]);
+            numerical_error("inv_sqrt: a Ritz value of the restart compression lies on the branch "
+                            "cut (-inf, 0] (cycle " + std::to_string(k) + ": " + v +
+                            "): z^{-1/2} is undefined there");
+          }
+          clo = std::min(clo, mod);
+          chi = std::max(chi, mod);
+          cth = std::max(cth, th);
+        }
+        s_lmin = std::min(s_lmin, clo);
+        s_lmax = std::max(s_lmax, chi);
+        s_th = std::max(s_th, cth);
+        if (k > 1 && M + m_eff > Ncap)
+          numerical_error("inv_sqrt: R_accum beyond the budget: the quadrature cannot replay");
+        // the earlier cycles' blocks of R_accum into a set's node states
+        auto replay = [&](QuadSet& s) {
+          for (size_t j = 0; j < cyc_M.size(); ++j) {
+            double coup = 0.0;
+            if (j > 0) {  // R_accum(M_j, M_j - 1) = coupling * alpha (restart.cpp:67)
+              RKMF_CUDA(cudaMemcpyAsync(&coup, Racc + (cyc_M[j] - 1) * ldR + cyc_M[j],
+                                        sizeof(double), cudaMemcpyDeviceToHost, st));
+              RKMF_CUDA(cudaStreamSynchronize(st));
+            }
+            launch_quad_invsqrt_cycle(Racc + cyc_M[j] * ldR + cyc_M[j], ldR, int(m_eff),
+                                      int64_t(j) + 1, &s.q, nullptr, ctx->st_dev, nullptr, st,
+                                      int(cyc_mk[j]), coup);
+            ctx->launches++;
+          }
+        };
+        auto current = [&](QuadSet& s) {
+          launch_quad_invsqrt_cycle(bb.Rbar, bb.ldr, int(m_eff), k, &s.q, s.g, ctx->st_dev,
+                                    s.partial, st);
+          ctx->launches += 2;
+        };
+        ctx->timed(3, [&] {
+          if (k == 1 || !qa.d.covers(clo, chi, cth)) {
+            qa.load(design_invsqrt(s_lmin, s_lmax, s_th), m_eff, st);
+            replay(qa);
+            current(qa);
+            std::vector<double> ga(static_cast<size_t>(mk)), gb(static_cast<size_t>(mk));
+            for (;;) {
+              qb.load(qa.d.doubled(), m_eff, st);
+              replay(qb);
+              current(qb);
+              RKMF_CUDA(cudaMemcpyAsync(ga.data(), qa.g, sizeof(double) * size_t(mk),
+                                        cudaMemcpyDeviceToHost, st));
+              RKMF_CUDA(cudaMemcpyAsync(gb.data(), qb.g, sizeof(double) * size_t(mk),
+                                        cudaMemcpyDeviceToHost, st));
+              RKMF_CUDA(cudaStreamSynchronize(st));
+              double dn = 0.0, bn = 0.0;
+              for (int i = 0; i < mk; ++i) {
+                dn += (ga[size_t(i)] - gb[size_t(i)]) * (ga[size_t(i)] - gb[size_t(i)]);
+                bn += gb[size_t(i)] * gb[size_t(i)];
+              }
+              if (std::sqrt(dn) <= 1e-12 * std::sqrt(bn)) break;  // qa is accurate
+              std::swap(qa, qb);  // the finer set, its states advanced through this cycle
+              if (qa.d.nq > (1 << 16))
+                numerical_error("inv_sqrt: the restart quadrature does not converge under node "
+                                "doubling (cycle " + std::to_string(k) + ")");
+            }
+          } else {
+            current(qa);
+          }
+          RKMF_CUDA(cudaMemcpyAsync(g, qa.g, sizeof(double) * size_t(m_eff), cudaMemcpyDeviceToDevice, st));
+        });
+        isq_nodes = qa.d.nq;
       } else {
         // ExpNeg restart quadrature. The contour is designed from the Ritz
         // values seen so far; when a cycle's Ritz values leave it, it is
@@ -1123,9 +1285,11 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
           RKMF_CUDA(cudaMemcpyAsync(q.pi, ones.data(), sizeof(double) * ones.size(), cudaMemcpyHostToDevice, st));
           for (size_t j = 0; j < cyc_M.size(); ++j) {  // replay cycles 1..k-1
             double coup = 0.0;
-            if (j > 0)  // R_accum(M_j, M_j - 1) = coupling * alpha (restart.cpp:67)
-              RKMF_CUDA(cudaMemcpy(&coup, Racc + (cyc_M[j] - 1) * ldR + cyc_M[j], sizeof(double),
-                                   cudaMemcpyDeviceToHost));
+            if (j > 0) {  // R_accum(M_j, M_j - 1) = coupling * alpha (restart.cpp:67)
+              RKMF_CUDA(cudaMemcpyAsync(&coup, Racc + (cyc_M[j] - 1) * ldR + cyc_M[j],
+                                        sizeof(double), cudaMemcpyDeviceToHost, st));
+              RKMF_CUDA(cudaStreamSynchronize(st));
+            }
             launch_quad_expneg_cycle(Racc + cyc_M[j] * ldR + cyc_M[j], ldR, int(m_eff),
                                      int64_t(j) + 1, &q, g, ctx->st_dev, partial, st,
                                      int(cyc_mk[j]), coup);
@@ -1274,6 +1438,7 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
     res->basis_updates = updates;
     res->peak_basis_cols = peak;
     res->n_records = int64_t(recs.size());
+    res->quad_nodes = isq_adaptive ? isq_nodes : (q.nq > 0 ? q.nq : 0);
     if (records)
       for (int64_t i = 0; i < std::min<int64_t>(records_cap, res->n_records); ++i) records[i] = recs[size_t(i)];
     ctx->racc_ld = ldR;

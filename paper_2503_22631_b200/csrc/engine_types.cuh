@@ -76,6 +76,13 @@ struct rkmf_context {
   SolveState* st_host = nullptr;  // pinned
   DevBuf z, W, U, Rbar, Racc, ws, u, g, fhat, ref, partial, qshift, qweight, qpi,
       qemx, scratch, gram, cl, diag;
+  // the adaptive InvSqrt quadrature's two node sets (engine.cu QuadSet)
+  struct QuadBufs {
+    DevBuf shift, weight, pi, emx, partial, g;
+    void release() {
+      for (DevBuf* b : {&shift, &weight, &pi, &emx, &partial, &g}) b->release();
+    }
+  } isq[2];
   rkmf_cycle_observer observer = nullptr;  // test-only CycleObserver (restart.hpp:53)
   void* observer_user = nullptr;
   int64_t racc_ld = 0;   // leading dimension of the last solve's R_accum
@@ -112,9 +119,35 @@ struct rkmf_context {
       rs[i]->tick = tk + i * (gk + 1);
       rs[i]->max_blocks = kb;
       rs[i]->max_len = int(i < 2 ? d : 2);
+      rs[i]->max_groups = gk;
       rs[i]->groups = 0;
     }
     red_cap_d = d;
+  }
+  // the classical builder's k+1 dots: one reduction slice per column, up to
+  // 8 blocks per SM each (classical.cu grid_rows)
+  DevBuf redcl;
+  int64_t red_cl_slices = 0;
+  DetRed red_cl;
+  const DetRed& red_classical(int64_t slices) {
+    if (slices > red_cl_slices || !redcl.p) {
+      int sms = 0;
+      RKMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      const int64_t nb = 8 * std::max(sms, 1), ng = det_groups(int(nb)) + 1;
+      const size_t nd = size_t(slices) * size_t(nb + ng);
+      const size_t bytes = sizeof(double) * nd + sizeof(unsigned) * size_t(slices * (ng + 1));
+      redcl.ensure(bytes);
+      RKMF_CUDA(cudaMemsetAsync(redcl.p, 0, bytes, stream));
+      double* p = redcl.as<double>();
+      red_cl.part = p;
+      red_cl.gpart = p + size_t(slices) * size_t(nb);
+      red_cl.tick = reinterpret_cast<unsigned*>(p + nd);
+      red_cl.max_blocks = int(slices * nb);
+      red_cl.max_len = 1;
+      red_cl.max_groups = int(slices * (ng + 1));
+      red_cl_slices = slices;
+    }
+    return red_cl;
   }
   DetRed& red_sketch(int64_t d) {
     ensure_red(d);

@@ -94,7 +94,7 @@ __global__ void q1_fill_kernel(int64_t N, const double* __restrict__ kappa, int 
     auto bnd = [&](int64_t X, int64_t Y, int64_t Z) {
       return X == 0 || Y == 0 || Z == 0 || X == N - 1 || Y == N - 1 || Z == N - 1;
     };
-    const bool rb = dirichlet && bnd(x, y, z);
+    const bool brow = dirichlet && bnd(x, y, z);
     int64_t k = rp[i];
     for (int dx = -1; dx <= 1; ++dx) {
       const int64_t X = x + dx;
@@ -107,7 +107,7 @@ __global__ void q1_fill_kernel(int64_t N, const double* __restrict__ kappa, int 
           if (Z < 0 || Z >= N) continue;
           const int64_t c = (X * N + Y) * N + Z;
           double val;
-          if (dirichlet && (rb || bnd(X, Y, Z))) {
+          if (dirichlet && (brow || bnd(X, Y, Z))) {
             val = (c == r) ? 1.0 : 0.0;
           } else {
             const int D = (dx != 0) + (dy != 0) + (dz != 0);

@@ -241,12 +241,15 @@ void launch_scale_copy(int64_t n, const double* src, double* dst, const SolveSta
 void launch_fill(int64_t n, double v, double* x, cudaStream_t st);
 
 // classical.cu: the classical builder (S == nullptr) via CGS2
+// the grid reductions (norms, the k+1 dots as reduction slices) are the
+// fixed-order ones of detred.cuh
 void launch_cl_start(int64_t n, const double* start, double* nrm2_scratch, SolveState* st_dev,
-                     bool first, int m_eff, bool norm_only, cudaStream_t st);
+                     bool first, int m_eff, bool norm_only, const DetRed& red, cudaStream_t st);
 void launch_cl_multidot(int64_t n, int k, int64_t ldw, const double* W, const double* z,
-                        double* h, const SolveState* st_dev, cudaStream_t st);
+                        double* h, const SolveState* st_dev, const DetRed& red, cudaStream_t st);
 void launch_cl_update(int64_t n, int k, int64_t ldw, const double* W, double* z, const double* h,
-                      double* nrm2, bool store, const SolveState* st_dev, cudaStream_t st);
+                      double* nrm2, bool store, const SolveState* st_dev, const DetRed& red,
+                      cudaStream_t st);
 void launch_cl_decide(int k, int64_t ldr, int64_t n_global, double tol, double* h1, double* h2,
                       double* nrm2, double* Rbar, double* rlast, SolveState* st_dev,
                       cudaStream_t st);
@@ -281,9 +284,21 @@ struct QuadState {
   double* shift;   // sigma_q, size nq
   double* weight;  // w_q, size nq
 };
+// mk_replay >= 0: replay a past cycle (its R_accum block and coupling) into
+// the node states of a new node set; no output
 void launch_quad_invsqrt_cycle(const double* Rbar, int64_t ldr, int mk, int64_t cycle,
                                QuadState* q, double* g, const SolveState* st_dev,
-                               double* partial, cudaStream_t st);
+                               double* partial, cudaStream_t st, int mk_replay = -1,
+                               double coupling_replay = 0.0);
+// the InvSqrt node set from the extremes of the Ritz values seen (densef.cu)
+struct InvSqrtDesign {
+  double u0 = 0, h = 0.25, lmin = 0, lmax = 0, thmax = 0;
+  int nq = 0;
+  bool covers(double lmin_seen, double lmax_seen, double thmax_seen) const;
+  InvSqrtDesign doubled() const;  // same interval, half the step
+};
+InvSqrtDesign design_invsqrt(double lmin, double lmax, double thmax);
+void invsqrt_nodes(const InvSqrtDesign& d, std::vector<double>& shift, std::vector<double>& weight);
 // ExpNeg quadrature (complex nodes, see densef.cu): shift/weight/pi/emx hold
 // nq complex values (interleaved re, im)
 // mk_replay >= 0: replay a past cycle (its R_accum block, its coupling) to

@@ -248,7 +248,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
     // order (detred.cuh; K3 sums the groups). The last tile's bar.sync 2
     // above completed acc.
     __shared__ int rflag;
-    if (!(debug & 8)) det_group_reduce<kSketchThreads, 2>(red, d, acc, u, &rflag);
+    if (!(debug & 8)) det_group_reduce<kSketchThreads, 2, 16>(red, d, acc, u, &rflag);
     if (u == 0 && stop) trace_max(step, 1);
     return;
   }

@@ -4,6 +4,7 @@
 // semigroup identity exp(-tA)b = exp(-tA/2)(exp(-tA/2)b). Exit code 0 = pass.
 #include <cmath>
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "rkmf_b200.hpp"
@@ -45,6 +46,33 @@ int main() {
     std::printf("cpp_api_smoke: n=%lld cycles=%lld converged=%d semigroup_rel=%.3e R_accum=%zux\n",
                 (long long)n, (long long)full.cycles, int(full.converged), rel,
                 full.R_accum.size());
+    // classical builder (S == nullptr, restart.cpp:53-55) and the observer
+    int seen = 0;
+    double last_f = 0.0;
+    CycleObserver obs = [&](const CycleInfo& ci) {
+      ++seen;
+      last_f = ci.f_hat[0];
+    };
+    RestartResult cl = restarted_krylov(ctx, dA, b, FunctionSpec::exp_neg(t), o, nullptr, obs);
+    double ec = 0;
+    for (size_t i = 0; i < b.size(); ++i)
+      ec += (cl.f_hat[i] - full.f_hat[i]) * (cl.f_hat[i] - full.f_hat[i]);
+    const double rel_cl = std::sqrt(ec / nf);
+    const bool obs_ok = seen == int(cl.cycles) && last_f == cl.f_hat[0];
+    // Matrix Market round trip (sparse.cpp:140-211)
+    const std::string path = "/tmp/rkmf_cpp_api_smoke.mtx";
+    save_matrix_market(A, path);
+    const SparseMatrix B = load_matrix_market(path);
+    std::remove(path.c_str());
+    const bool mtx_ok = B.row_ptr == A.row_ptr && B.col_idx == A.col_idx && B.values == A.values;
+    std::printf("cpp_api_smoke: classical_rel=%.3e observer_calls=%d mtx_round_trip=%d\n", rel_cl,
+                seen, int(mtx_ok));
+    bool parse_threw = false;
+    try {
+      load_matrix_market("/nonexistent/rkmf.mtx");
+    } catch (const ParseError&) {
+      parse_threw = true;
+    }
     bool threw = false;
     try {
       RestartOptions bad;
@@ -53,8 +81,10 @@ int main() {
     } catch (const ParameterError& ex) {
       threw = std::string(ex.what()).find("restart: m_r must be >= 1") == 0;
     }
-    return (full.converged && rel < 1e-9 && threw &&
-            full.R_accum.size() == size_t(full.total_m * full.total_m)) ? 0 : 1;
+    return (full.converged && rel < 1e-9 && threw && cl.converged && rel_cl < 1e-9 && obs_ok &&
+            mtx_ok && parse_threw && full.R_accum.size() == size_t(full.total_m * full.total_m))
+               ? 0
+               : 1;
   } catch (const std::exception& ex) {
     std::printf("cpp_api_smoke: exception: %s\n", ex.what());
     return 2;

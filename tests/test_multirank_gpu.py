@@ -98,3 +98,29 @@ def test_partitioned_classical_matches_oracle(tmp_path, oracle, name, N, world):
                                 m_r=P.m, tol=P.tol, k_max=P.k_max, S=None)
     assert bool(res["converged"]) and abs(int(res["cycles"]) - o.cycles) <= 1
     assert np.linalg.norm(res["f"] - o.f_hat) <= 1e-9 * np.linalg.norm(o.f_hat)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,world", [(24, 2), (24, 3)])
+def test_q1_rows_generated_in_hbm(tmp_path, oracle, N, world):
+    """cfg5's partitioned input path: every rank's Q1 rows generated in HBM
+    (whole x-planes + the x-plane halo plan) equal the host-built rows
+    uploaded through rkmf_matrix_create_partitioned bit-for-bit (CSR in local
+    numbering, norm1, b slice, f_hat), and the assembled f_hat matches the
+    oracle at the north-star bar."""
+    from paper_2503_22631_b200 import configs
+    out = str(tmp_path / f"q1_{N}_{world}.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(ROOT, "tests", "mr_q1_worker.py"), out, str(N)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = np.load(out)
+    assert res["flags"].all(), res["flags"]
+    assert f"'nranks': {world}" in str(res["comm"])
+    P = configs.build("cfg5", N)
+    S = oracle.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED)
+    o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, oracle.KIND_EXP_NEG, P.t,
+                                m_r=P.m, tol=P.tol, k_max=P.k_max, S=S)
+    assert bool(res["converged"]) and abs(int(res["cycles"]) - o.cycles) <= 1
+    assert np.linalg.norm(res["f"] - o.f_hat) <= 1e-9 * np.linalg.norm(o.f_hat)
