@@ -102,6 +102,20 @@ class CycleInfoC(C.Structure):
 
 _OBSERVER_CB = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(CycleInfoC))
 
+
+class MethodSpecC(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("m", C.c_int64), ("d", C.c_int64), ("zeta", C.c_int64),
+                ("tol", C.c_double), ("k_max", C.c_int64), ("seed", C.c_uint64)]
+
+
+class SweepRecordC(C.Structure):
+    _fields_ = [("method", C.c_char * 32), ("n", C.c_int64), ("m_or_totalm", C.c_int64),
+                ("cycle", C.c_int64), ("matvecs", C.c_int64), ("rel_error", C.c_double),
+                ("update_norm", C.c_double), ("kappa_W", C.c_double),
+                ("leftmost_ritz_re", C.c_double), ("elapsed_ms", C.c_double),
+                ("note", C.c_char * 256), ("phase_build_ms", C.c_double),
+                ("phase_eval_ms", C.c_double)]
+
 # Every symbol declared in include/rkmf_b200.h: (name, restype, argtypes)
 _P, _I64, _U64, _D, _I32 = C.c_void_p, C.c_int64, C.c_uint64, C.c_double, C.c_int32
 _PP = C.POINTER(C.c_void_p)
@@ -160,6 +174,9 @@ SYMBOLS = [
     ("rkmf_host_free", None, [_P]),
     ("rkmf_matrix_load_mtx", C.c_int, [_P, C.c_char_p, _PP]),
     ("rkmf_matrix_save_mtx", C.c_int, [_P, _P, C.c_char_p]),
+    ("rkmf_convergence_sweep", C.c_int,
+     [_P, _P, _P, _I32, _D, _P, _P, _I64, _I32, _P, _I64, _P]),
+    ("rkmf_sweep_write_csv", C.c_int, [_P, _I64, C.c_char_p, C.c_char_p, _I64]),
 ]
 
 _lib = None
@@ -856,6 +873,55 @@ def partitioned_sketch(ctx: Context, d: int, n_global: int, zeta: int, seed: int
     ctx.check(lib().rkmf_sketch_create_partitioned(ctx.h, d, n_global, zeta, C.c_uint64(seed),
                                                    col_begin, n_local, C.byref(h)))
     return SketchOperator(ctx, h, d, n_local, zeta, seed)
+
+
+# ---- convergence sweep (restart.cpp:124-305) and its CSV (rkmf_bench.cpp:172-186) ----
+@dataclass
+class MethodSpec:
+    """restart::MethodSpec (restart.hpp:81-97) for the device sweep."""
+    name: str
+    m: int = 100
+    d: int = 0
+    zeta: int = 4
+    tol: float = 1e-10
+    k_max: int = 100
+    seed: int = 0
+
+
+def convergence_sweep(A: SparseMatrix, b, f: FunctionSpec, methods, reference=None,
+                      with_timing: bool = False) -> list:
+    """Rows (dicts with the SweepRecord fields) of every method in order."""
+    bb = np.ascontiguousarray(b, np.float64)
+    ref = None if reference is None else np.ascontiguousarray(reference, np.float64)
+    ms = (MethodSpecC * max(len(methods), 1))()
+    for i, m in enumerate(methods):
+        ms[i] = MethodSpecC(m.name.encode()[:31], m.m, m.d, m.zeta, m.tol, m.k_max, m.seed)
+    n = C.c_int64()
+    A.ctx.check(lib().rkmf_convergence_sweep(A.ctx.h, A.h, _ptr(bb), f.kind, f.t, _ptr(ref), ms,
+                                             len(methods), int(with_timing), None, 0,
+                                             C.byref(n)))
+    recs = (SweepRecordC * max(n.value, 1))()
+    A.ctx.check(lib().rkmf_convergence_sweep(A.ctx.h, A.h, _ptr(bb), f.kind, f.t, _ptr(ref), ms,
+                                             len(methods), int(with_timing), recs, n.value,
+                                             C.byref(n)))
+    rows = []
+    for i in range(n.value):
+        r = recs[i]
+        rows.append({k: (getattr(r, k).decode() if t in (C.c_char * 32, C.c_char * 256)
+                         else getattr(r, k)) for k, t in SweepRecordC._fields_})
+    return rows
+
+
+def write_sweep_csv(rows, path: str = "") -> None:
+    """The CLI's CSV (fixed header, %.17g numbers); "" writes to stdout."""
+    recs = (SweepRecordC * max(len(rows), 1))()
+    for i, r in enumerate(rows):
+        vals = dict(r)
+        vals["method"] = vals["method"].encode()
+        vals["note"] = vals["note"].encode()
+        recs[i] = SweepRecordC(**vals)
+    err = C.create_string_buffer(512)
+    _io_check(lib().rkmf_sweep_write_csv(recs, len(rows), os.fsencode(path), err, 512), err)
 
 
 # ---- Matrix Market / vector interchange: sparse.cpp:140-242 (host only) ----
