@@ -146,6 +146,14 @@ int rkmf_matrix_info(const rkmf_matrix* A, int64_t* n_rows, int64_t* n_cols, int
  * drops the copy (CSR path only), 1 builds it if the matrix qualifies, 2
  * only queries; *ndiag (optional) receives the diagonal count, 0 = CSR only. */
 int rkmf_matrix_dia(rkmf_matrix* A, int enable, int* ndiag);
+/* Row dictionary of the diagonal copy (B200-specific): when the copy's rows
+ * take at most 256 distinct value tuples (constant-coefficient stencils: 27 on
+ * a 3D 7-point grid), the fused SpMV + sketch streams one tuple-id byte per
+ * row and reads the values from a shared-memory dictionary (results
+ * bit-identical). Built with the diagonal copy by default. enable = 0 drops
+ * it, 1 builds it if the copy exists and qualifies, 2 only queries;
+ * *ntuples (optional) receives the tuple count, 0 = none. */
+int rkmf_matrix_dia_dict(rkmf_matrix* A, int enable, int* ntuples);
 /* Row-pointer width of the device CSR: stored as int32 when nnz < 2^31 - 1,
  * else int64 (cfg5 on one GPU). enable != 0 widens an int32 matrix to int64
  * so the int64 instantiations of the SpMV kernels run on small problems

@@ -133,6 +133,7 @@ SYMBOLS = [
     ("rkmf_matrix_destroy", C.c_int, [_P]),
     ("rkmf_matrix_info", C.c_int, [_P, _P, _P, _P, _P]),
     ("rkmf_matrix_dia", C.c_int, [_P, C.c_int, _P]),
+    ("rkmf_matrix_dia_dict", C.c_int, [_P, C.c_int, _P]),
     ("rkmf_sketch_create", C.c_int, [_P, _I64, _I64, _I64, _U64, _PP]),
     ("rkmf_sketch_destroy", C.c_int, [_P]),
     ("rkmf_sketch_set_scale", C.c_int, [_P, _D]),
@@ -307,6 +308,22 @@ class SparseMatrix:
         nd = C.c_int()
         self.ctx.check(lib().rkmf_matrix_dia(self.h, int(bool(enable)), C.byref(nd)))
         return nd.value
+
+    def set_row_dictionary(self, enable: bool) -> int:
+        """Drop (False) or build (True, if the diagonal copy's rows take at
+        most 256 distinct value tuples) the row dictionary the fused SpMV +
+        sketch then streams (one byte per row); returns the tuple count
+        (0 = none). Results are identical."""
+        nt = C.c_int()
+        self.ctx.check(lib().rkmf_matrix_dia_dict(self.h, int(bool(enable)), C.byref(nt)))
+        return nt.value
+
+    @property
+    def ntuples(self) -> int:
+        """Distinct row tuples of the diagonal copy's dictionary (0 = none)."""
+        nt = C.c_int()
+        self.ctx.check(lib().rkmf_matrix_dia_dict(self.h, 2, C.byref(nt)))
+        return nt.value
 
     def use_rp64(self) -> bool:
         """Widen the device row pointers to int64 (the storage cfg5's 3.6e9

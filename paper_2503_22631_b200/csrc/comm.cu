@@ -162,30 +162,6 @@ __global__ void pack_kernel(int64_t cnt, const int32_t* __restrict__ idx,
     out[i] = x[idx[i]];
 }
 
-__global__ void colsum_abs_kernel(int64_t nnz, const int32_t* __restrict__ ci,
-                                  const double* __restrict__ val, double* colsum) {
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
-       k += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(colsum + ci[k], fabs(val[k]));
-}
-
-__global__ void scatter_add_kernel(int64_t cnt, const int32_t* __restrict__ idx,
-                                   const double* __restrict__ v, double* out) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
-       i += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(out + idx[i], v[i]);
-}
-
-__global__ void max_abs_kernel(int64_t n, const double* __restrict__ v, double* out) {
-  double m = 0.0;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    m = fmax(m, v[i]);
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0)  // non-negative doubles order like their bit patterns
-    atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(m));
-}
-
 int blocks_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096))); }
 
 }  // namespace
@@ -209,33 +185,38 @@ void comm_halo_exchange(rkmf_context* ctx, const rkmf_matrix* A, double* x) {
 }
 
 // Global norm1 = max column abs-sum (sparse.cpp:97-102) of a partitioned
-// matrix whose halo plan is set: local column sums, the halo parts returned
-// to their owners (the reverse of the halo exchange), max, allreduce(max).
+// matrix whose halo plan is set, order-independent like the single-GPU one
+// (spmv.cu fixed-point words): the global max |a_ij| (allreduce max) fixes
+// the scale, local fixed-point column sums, their halo parts returned to the
+// owners (the reverse of the halo exchange; the words travel as 8-byte
+// payloads) and added with integer atomics, local max, allreduce(max).
 void partitioned_norm1(rkmf_context* ctx, rkmf_matrix* M) {
   const HaloPlan& h = M->halo;
   const int64_t n_local = h.n_local, n_halo = h.n_halo, nnz = M->view.nnz;
+  const int64_t nc = n_local + n_halo;
   cudaStream_t st = ctx->stream;
   Transport& T = *ctx->comm;
-  DevBuf cs, back, mx;
-  cs.ensure(sizeof(double) * size_t(n_local + n_halo + 1));
-  back.ensure(sizeof(double) * size_t(std::max<int64_t>(h.send_total, 1)));
+  ScopedBuf cs, back, mx, vm;
+  cs.ensure(sizeof(unsigned long long) * size_t(2 * nc + 1));
+  back.ensure(sizeof(unsigned long long) * size_t(std::max<int64_t>(h.send_total, 1)));
   mx.ensure(sizeof(double));
-  RKMF_CUDA(cudaMemsetAsync(cs.p, 0, sizeof(double) * size_t(n_local + n_halo + 1), st));
-  RKMF_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(double), st));
-  if (nnz > 0)
-    colsum_abs_kernel<<<blocks_for(nnz), 256, 0, st>>>(nnz, M->col, M->val, cs.as<double>());
-  T.alltoallv(cs.as<double>() + n_local, h.recv_off, h.recv_cnt, back.p, h.send_off, h.send_cnt,
-              true, st);
-  if (h.send_total > 0)
-    scatter_add_kernel<<<blocks_for(h.send_total), 256, 0, st>>>(h.send_total, h.send_idx,
-                                                                  back.as<double>(), cs.as<double>());
-  if (n_local > 0)
-    max_abs_kernel<<<blocks_for(n_local), 256, 0, st>>>(n_local, cs.as<double>(), mx.as<double>());
-  RKMF_CUDA(cudaGetLastError());
+  vm.ensure(sizeof(double));
+  auto* hi = static_cast<unsigned long long*>(cs.p);
+  auto* lo = hi + nc;
+  auto* vmax = static_cast<unsigned long long*>(vm.p);
+  launch_abs_max_bits(nnz, M->val, vmax, st);
+  T.allreduce(vm.as<double>(), 1, true, st);  // non-negative: max of the values = max of the bits
+  launch_fx_colsum(nnz, M->col, M->val, vmax, nc, hi, lo, st);
+  for (unsigned long long* word : {hi, lo}) {
+    T.alltoallv(word + n_local, h.recv_off, h.recv_cnt, back.p, h.send_off, h.send_cnt, false, st);
+    launch_fx_scatter_add(h.send_total, h.send_idx, static_cast<unsigned long long*>(back.p), word,
+                          st);
+  }
+  launch_fx_colmax(n_local, hi, lo, vmax, mx.as<double>(), st);
   T.allreduce(mx.as<double>(), 1, true, st);
   RKMF_CUDA(cudaMemcpyAsync(&M->norm1, mx.p, sizeof(double), cudaMemcpyDeviceToHost, st));
   RKMF_CUDA(cudaStreamSynchronize(st));
-  ctx->launches += 3;
+  ctx->launches += 5;
 }
 
 }  // namespace rkmf_b200

@@ -133,9 +133,185 @@ void launch_fill(const CsrView& v, const int32_t* toff, int64_t stride, int nd, 
                                             v.val, toff, stride, nd, dval);
 }
 
+
+// ---- row dictionary of the diagonal copy ----
+// Stencil matrices with constant coefficients (cfg1, cfg2, cfg4, cfg5) have
+// few distinct rows: in the diagonal layout a row is the tuple of its nd
+// values, and only boundary faces, edges and corners change it (27 tuples on
+// a 3D 7-point grid). Then K2 streams one byte per row (the tuple id) instead
+// of 8 nd, and looks the values up in a shared-memory dictionary: the same
+// values in the same order, so z stays bit-identical. Built on device: each
+// row's tuple is hashed (64-bit) into an open-addressing table; the host
+// orders the occupied slots by their smallest row (deterministic ids) and a
+// last pass assigns each row its id and compares its values with the
+// dictionary's bit for bit (a hash collision fails the build, it never
+// corrupts a row). More than kMaxTuples distinct rows: no dictionary.
+constexpr int kTupTable = 4096;
+
+__device__ __forceinline__ uint64_t tup_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t row_hash(const double* __restrict__ dval, int64_t row, int nd) {
+  const int64_t tile = row / kTileRows, r = row % kTileRows;
+  uint64_t h = 0x9E3779B97F4A7C15ULL * uint64_t(nd + 1);
+  for (int q = 0; q < nd; ++q)
+    h = tup_mix(h ^ uint64_t(__double_as_longlong(dval[(tile * nd + q) * kTileRows + r])));
+  return h | 1ULL;  // 0 marks an empty slot
+}
+
+// flags[0]: more than kMaxTuples distinct rows (or the table filled)
+__global__ void tup_insert_kernel(int64_t n, int nd, const double* __restrict__ dval,
+                                  unsigned long long* keys, unsigned long long* rep,
+                                  unsigned long long* rowhash, int32_t* count, int32_t* flags) {
+  for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < n;
+       row += int64_t(gridDim.x) * blockDim.x) {
+    if (*(volatile int32_t*)flags) return;
+    const unsigned long long h = row_hash(dval, row, nd);
+    rowhash[row] = h;
+    int slot = int(h & (kTupTable - 1));
+    bool found = false;
+    for (int i = 0; i < kTupTable; ++i) {
+      const unsigned long long k = keys[slot];
+      if (k == h) { found = true; break; }
+      if (k == 0ULL) {
+        const unsigned long long old = atomicCAS(keys + slot, 0ULL, h);
+        if (old == 0ULL) {
+          if (atomicAdd(count, 1) >= kMaxTuples) flags[0] = 1;
+          found = true;
+          break;
+        }
+        if (old == h) { found = true; break; }
+      }
+      slot = (slot + 1) & (kTupTable - 1);
+    }
+    if (!found) { flags[0] = 1; return; }
+    atomicMin(rep + slot, (unsigned long long)row);
+  }
+}
+
+__global__ void tup_gather_kernel(int ntup, int nd, const double* __restrict__ dval,
+                                  const long long* __restrict__ rep_rows, double* dict) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntup * nd) return;
+  const int id = i / nd, q = i % nd;
+  const int64_t row = rep_rows[id], tile = row / kTileRows, r = row % kTileRows;
+  dict[i] = dval[(tile * nd + q) * kTileRows + r];
+}
+
+// flags[1]: a row differs from its dictionary tuple (hash collision)
+__global__ void tup_assign_kernel(int64_t n, int nd, const double* __restrict__ dval,
+                                  const unsigned long long* __restrict__ keys,
+                                  const int16_t* __restrict__ slot_id,
+                                  const unsigned long long* __restrict__ rowhash,
+                                  const double* __restrict__ dict, uint8_t* tid, int32_t* flags) {
+  for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < n;
+       row += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long h = rowhash[row];
+    int slot = int(h & (kTupTable - 1));
+    while (keys[slot] != h) slot = (slot + 1) & (kTupTable - 1);  // inserted above
+    const int id = slot_id[slot];
+    const int64_t tile = row / kTileRows, r = row % kTileRows;
+    for (int q = 0; q < nd; ++q)
+      if (__double_as_longlong(dval[(tile * nd + q) * kTileRows + r]) !=
+          __double_as_longlong(dict[id * nd + q]))
+        flags[1] = 1;
+    tid[row] = uint8_t(id);
+  }
+}
+
 }  // namespace
 
+void drop_dia_dict(rkmf_matrix* M) {
+  if (M->dia_tid) cudaFree(M->dia_tid);
+  if (M->dia_dict) cudaFree(M->dia_dict);
+  M->dia_tid = nullptr;
+  M->dia_dict = nullptr;
+  M->view.dtid = nullptr;
+  M->view.ddict = nullptr;
+  M->view.ntup = 0;
+}
+
+// Builds the row dictionary of an existing diagonal copy when the matrix has
+// at most kMaxTuples distinct rows (leaves it absent otherwise).
+void build_dia_dict(rkmf_matrix* M) {
+  drop_dia_dict(M);
+  const CsrView& v = M->view;
+  if (!v.dval || v.ndiag < 1 || v.n_rows < 1) return;
+  rkmf_context* ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  const int nd = v.ndiag;
+  const int64_t n = v.n_rows, tiles = (n + kTileRows - 1) / kTileRows;
+  ScopedBuf keys, rep, rowhash, slot_id, rrows, misc;
+  keys.ensure(sizeof(unsigned long long) * kTupTable);
+  rep.ensure(sizeof(unsigned long long) * kTupTable);
+  rowhash.ensure(sizeof(unsigned long long) * size_t(n));
+  misc.ensure(sizeof(int32_t) * 4);
+  int32_t* cnt = misc.as<int32_t>();
+  int32_t* flags = cnt + 1;
+  RKMF_CUDA(cudaMemsetAsync(keys.p, 0, sizeof(unsigned long long) * kTupTable, st));
+  RKMF_CUDA(cudaMemsetAsync(rep.p, 0xFF, sizeof(unsigned long long) * kTupTable, st));
+  RKMF_CUDA(cudaMemsetAsync(misc.p, 0, sizeof(int32_t) * 4, st));
+  const int grid = 4 * 148;
+  tup_insert_kernel<<<grid, 256, 0, st>>>(n, nd, v.dval, static_cast<unsigned long long*>(keys.p),
+                                          static_cast<unsigned long long*>(rep.p),
+                                          static_cast<unsigned long long*>(rowhash.p), cnt, flags);
+  RKMF_CUDA(cudaGetLastError());
+  ctx->launches++;
+  std::vector<unsigned long long> hk(kTupTable), hr(kTupTable);
+  int32_t hf[4];
+  RKMF_CUDA(cudaMemcpyAsync(hf, misc.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
+  RKMF_CUDA(cudaMemcpyAsync(hk.data(), keys.p, sizeof(unsigned long long) * kTupTable,
+                            cudaMemcpyDeviceToHost, st));
+  RKMF_CUDA(cudaMemcpyAsync(hr.data(), rep.p, sizeof(unsigned long long) * kTupTable,
+                            cudaMemcpyDeviceToHost, st));
+  RKMF_CUDA(cudaStreamSynchronize(st));
+  if (hf[1] || hf[0] > kMaxTuples) return;
+  // ids in order of each tuple's first row (deterministic)
+  std::vector<std::pair<unsigned long long, int>> occ;
+  for (int i = 0; i < kTupTable; ++i)
+    if (hk[size_t(i)]) occ.push_back({hr[size_t(i)], i});
+  std::sort(occ.begin(), occ.end());
+  const int ntup = int(occ.size());
+  if (ntup < 1 || ntup > kMaxTuples) return;
+  std::vector<int16_t> sid(kTupTable, int16_t(-1));
+  std::vector<long long> rows(static_cast<size_t>(ntup));
+  for (int id = 0; id < ntup; ++id) {
+    sid[size_t(occ[size_t(id)].second)] = int16_t(id);
+    rows[size_t(id)] = (long long)occ[size_t(id)].first;
+  }
+  slot_id.ensure(sizeof(int16_t) * kTupTable);
+  rrows.ensure(sizeof(long long) * size_t(ntup));
+  RKMF_CUDA(cudaMemcpyAsync(slot_id.p, sid.data(), sizeof(int16_t) * kTupTable,
+                            cudaMemcpyHostToDevice, st));
+  RKMF_CUDA(cudaMemcpyAsync(rrows.p, rows.data(), sizeof(long long) * size_t(ntup),
+                            cudaMemcpyHostToDevice, st));
+  if (cudaMalloc(&M->dia_dict, sizeof(double) * size_t(ntup) * size_t(nd)) != cudaSuccess ||
+      cudaMalloc(&M->dia_tid, size_t(tiles) * kTileRows + 16) != cudaSuccess) {
+    cudaGetLastError();
+    return drop_dia_dict(M);
+  }
+  RKMF_CUDA(cudaMemsetAsync(M->dia_tid, 0, size_t(tiles) * kTileRows + 16, st));
+  tup_gather_kernel<<<(ntup * nd + 127) / 128, 128, 0, st>>>(
+      ntup, nd, v.dval, static_cast<const long long*>(rrows.p), M->dia_dict);
+  tup_assign_kernel<<<grid, 256, 0, st>>>(
+      n, nd, v.dval, static_cast<const unsigned long long*>(keys.p),
+      static_cast<const int16_t*>(slot_id.p), static_cast<const unsigned long long*>(rowhash.p),
+      M->dia_dict, M->dia_tid, flags);
+  RKMF_CUDA(cudaGetLastError());
+  ctx->launches += 2;
+  RKMF_CUDA(cudaMemcpyAsync(hf, misc.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
+  RKMF_CUDA(cudaStreamSynchronize(st));
+  if (hf[1]) return drop_dia_dict(M);
+  M->view.dtid = M->dia_tid;
+  M->view.ddict = M->dia_dict;
+  M->view.ntup = ntup;
+}
+
 void drop_dia(rkmf_matrix* M) {
+  drop_dia_dict(M);
   if (M->dia_val) cudaFree(M->dia_val);
   if (M->dia_off) cudaFree(M->dia_off);
   M->dia_val = nullptr;
@@ -217,6 +393,7 @@ void build_dia(rkmf_matrix* M) {
   M->view.doff = M->dia_off;
   M->view.ndiag = nd;
   M->view.dstride = int(stride);
+  build_dia_dict(M);
 }
 
 bool dia_enabled_by_env() {

@@ -29,10 +29,13 @@ constexpr int kGramRows = 64;
 constexpr int kGramMaxM = 64;
 constexpr int kGramPairsPerThread = (kGramMaxM * (kGramMaxM + 1) / 2 + kGramThreads - 1) / kGramThreads;
 
-// G[i*m + j] += sum_r W[r,i] W[r,j] (i <= j); column 0 scaled by sigma
+// part[block][q] = sum over the block's rows of W[r,i] W[r,j] for pair q = (i, j),
+// i <= j; column 0 scaled by sigma. gram_finish_kernel sums the blocks in
+// block order (no floating-point atomics: kappa_W is bitwise reproducible,
+// acceptance.cpp:545-582)
 __global__ void __launch_bounds__(kGramThreads)
     gram_kernel(int64_t n, int m, int64_t ldw, const double* __restrict__ W, const SolveState* st,
-                double* G) {
+                double* part) {
   __shared__ double tile[kGramRows][kGramMaxM + 1];
   __shared__ short pi[kGramMaxM * (kGramMaxM + 1) / 2], pj[kGramMaxM * (kGramMaxM + 1) / 2];
   const int P = m * (m + 1) / 2;
@@ -70,22 +73,45 @@ __global__ void __launch_bounds__(kGramThreads)
 #pragma unroll
   for (int a = 0; a < kGramPairsPerThread; ++a) {
     const int q = t + a * kGramThreads;
-    if (q < P) atomicAdd(G + pi[q] * m + pj[q], acc[a]);
+    if (q < P) part[int64_t(blockIdx.x) * P + q] = acc[a];
+  }
+}
+
+__global__ void gram_finish_kernel(int m, int nblocks, const double* __restrict__ part, double* G) {
+  const int P = m * (m + 1) / 2;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < P; q += gridDim.x * blockDim.x) {
+    int i = 0, rem = q;
+    while (rem >= m - i) { rem -= m - i; ++i; }
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += part[int64_t(b) * P + q];
+    G[i * m + i + rem] = s;
   }
 }
 
 }  // namespace
 
-bool launch_gram(int64_t n, int m, int64_t ldw, const double* W, const SolveState* st_dev,
-                 double* G, cudaStream_t st) {
-  if (m < 1 || m > kGramMaxM) return false;
-  RKMF_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * size_t(m) * size_t(m), st));
+int gram_grid(int64_t n) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (n + kGramRows - 1) / kGramRows;
-  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, 4 * int64_t(sms))));
-  gram_kernel<<<grid, kGramThreads, 0, st>>>(n, m, ldw, W, st_dev, G);
+  return int(std::max<int64_t>(1, std::min<int64_t>(tiles, 4 * int64_t(sms))));
+}
+
+size_t gram_scratch_doubles(int64_t n, int m) {
+  return size_t(m) * size_t(m) + size_t(gram_grid(n)) * size_t(m) * size_t(m + 1) / 2;
+}
+
+// G = the first m*m doubles of the scratch (gram_scratch_doubles), the block
+// partials after them
+bool launch_gram(int64_t n, int m, int64_t ldw, const double* W, const SolveState* st_dev,
+                 double* G, cudaStream_t st) {
+  if (m < 1 || m > kGramMaxM) return false;
+  RKMF_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * size_t(m) * size_t(m), st));
+  const int grid = gram_grid(n);
+  double* part = G + size_t(m) * size_t(m);
+  gram_kernel<<<grid, kGramThreads, 0, st>>>(n, m, ldw, W, st_dev, part);
+  gram_finish_kernel<<<(m * (m + 1) / 2 + 127) / 128, 128, 0, st>>>(m, grid, part, G);
   RKMF_CUDA(cudaGetLastError());
   return true;
 }

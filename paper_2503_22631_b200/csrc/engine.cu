@@ -80,10 +80,10 @@ void finish_matrix(rkmf_matrix* M, int64_t max_tile_nnz, bool require_sorted) {
   int32_t* flags = reinterpret_cast<int32_t*>(scr);
   double* out = reinterpret_cast<double*>(scr + 16);
   DevBuf colsum;
-  colsum.ensure(sizeof(double) * size_t(M->view.n_cols + 1));
+  colsum.ensure(sizeof(double) * size_t(2 * M->view.n_cols + 1));
   launch_matrix_check(&M->view, flags, require_sorted, ctx->stream);
   launch_matrix_norm1(&M->view, colsum.as<double>(), out, ctx->stream);
-  ctx->launches += 3;
+  ctx->launches += 4;
   int32_t hf[2] = {0, 0};
   RKMF_CUDA(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
   RKMF_CUDA(cudaMemcpyAsync(&M->norm1, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -591,6 +591,16 @@ int rkmf_matrix_dia(rkmf_matrix* M, int enable, int* ndiag) {
     if (enable == 1) build_dia(M);
     else if (enable == 0) drop_dia(M);  // other values: query only
     if (ndiag) *ndiag = M->view.ndiag;
+  });
+}
+
+int rkmf_matrix_dia_dict(rkmf_matrix* M, int enable, int* ntuples) {
+  if (!M) return RKMF_PARAMETER_ERROR;
+  return guarded(M->ctx, [&] {
+    set_device(M->ctx);
+    if (enable == 1) build_dia_dict(M);
+    else if (enable == 0) drop_dia_dict(M);  // other values: query only
+    if (ntuples) *ntuples = M->view.ntup;
   });
 }
 
@@ -1119,10 +1129,10 @@ int rkmf_restarted_krylov(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sk
       bool diag_ok = false;
       double* Gd = nullptr;
       if (opts.diagnostics) {
-        Gd = static_cast<double*>(ctx->diag.ensure(sizeof(double) * size_t(m_eff) * size_t(m_eff)));
+        Gd = static_cast<double*>(ctx->diag.ensure(sizeof(double) * gram_scratch_doubles(n, int(m_eff))));
         diag_ok = launch_gram(n, int(m_eff), bb.ldw, bb.W, ctx->st_dev, Gd, st);
         if (diag_ok) {
-          ctx->launches++;
+          ctx->launches += 2;
           comm_allreduce_sum(ctx, Gd, size_t(m_eff) * size_t(m_eff));
         }
       }

@@ -35,6 +35,14 @@ struct DevBuf {
   }
 };
 
+// a DevBuf freed when it leaves scope (setup-time temporaries)
+struct ScopedBuf : DevBuf {
+  ScopedBuf() = default;
+  ScopedBuf(const ScopedBuf&) = delete;
+  ScopedBuf& operator=(const ScopedBuf&) = delete;
+  ~ScopedBuf() { release(); }
+};
+
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 }  // namespace rkmf_b200
@@ -225,6 +233,8 @@ struct rkmf_matrix {
   double norm1 = 0.0;
   double* dia_val = nullptr;  // optional diagonal copy (dia.cu)
   int32_t* dia_off = nullptr;  // its sorted diagonal offsets
+  uint8_t* dia_tid = nullptr;  // optional row dictionary of the copy: tuple ids
+  double* dia_dict = nullptr;  // and the distinct row tuples
   bool partitioned = false;
   HaloPlan halo;
   int64_t n_rows_global() const { return partitioned ? halo.n_global : view.n_rows; }
@@ -259,6 +269,8 @@ namespace rkmf_b200 {
 // dia.cu
 void build_dia(rkmf_matrix* M);
 void drop_dia(rkmf_matrix* M);
+void build_dia_dict(rkmf_matrix* M);
+void drop_dia_dict(rkmf_matrix* M);
 bool dia_enabled_by_env();
 // comm.cu
 void comm_allreduce_sum(rkmf_context* ctx, double* buf, size_t count);

@@ -155,8 +155,15 @@ struct CsrView {
   const int32_t* doff;  // offsets: [8] for every tile (dstride 0) or [tile][8] (dstride 8)
   int ndiag;
   int dstride;
+  // optional row dictionary of the diagonal copy (dia.cu): every row's ndiag
+  // values are one of ntup distinct tuples; dtid[tile * 128 + r] = the row's
+  // tuple id, ddict[id * ndiag + q] its values. ntup == 0 when absent.
+  const uint8_t* dtid;
+  const double* ddict;
+  int ntup;
 };
 constexpr int kMaxDiag = 8;
+constexpr int kMaxTuples = 256;
 // Row-pointer tail padding (entries) and value/column padding (elements)
 // allocated by the engine so 16-byte-rounded bulk copies stay in bounds.
 constexpr int64_t kRpPad = 136;
@@ -186,18 +193,23 @@ __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t*
   for (int j = 0; NT * j < d; ++j) {
     const int s = (j & 1) ? NT * j + NT - 1 - t : NT * j + t;
     if (s >= d) continue;
-    const int e0 = off[s], e1 = off[s + 1];
-    double a0 = 0.0, a1 = 0.0;
-    int e = e0;
+    const int e0 = off[s], len = int(off[s + 1]) - e0;
+    const uint8_t* ep = ent + e0;
+    // four independent chains, four entry bytes off one address register
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int i = 0;
 #pragma unroll 1
-    for (; e + 1 < e1; e += 2) {
-      const double v0 = zs2[ent[e]];
-      const double v1 = zs2[ent[e + 1]];
-      a0 += v0;
-      a1 += v1;
+    for (; i + 4 <= len; i += 4, ep += 4) {
+      a0 += zs2[ep[0]];
+      a1 += zs2[ep[1]];
+      a2 += zs2[ep[2]];
+      a3 += zs2[ep[3]];
     }
-    if (e < e1) a0 += zs2[ent[e]];  // odd length: no masked over-read (bank conflicts)
-    acc[bins[s]] += a0 + a1;
+    const int r = len - i;  // 0..3 left: predicated, no masked over-read
+    if (r > 0) a0 += zs2[ep[0]];
+    if (r > 1) a1 += zs2[ep[1]];
+    if (r > 2) a2 += zs2[ep[2]];
+    acc[bins[s]] += (a0 + a1) + (a2 + a3);
   }
 }
 // mode: 0 = z = xscale*A x ; 1 = also sketch z ; 2 = sketch x only. The
@@ -216,7 +228,18 @@ bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double*
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z,
                              const int32_t* stop_flag, int step, DetRed& red, cudaStream_t st);
+// colsum: scratch of 2 * n_cols + 1 doubles (fixed-point words, spmv.cu)
 void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st);
+// the fixed-point column abs-sums behind norm1 (order-independent; spmv.cu)
+void launch_abs_max_bits(int64_t nnz, const double* val, unsigned long long* vmax_bits,
+                         cudaStream_t st);
+void launch_fx_colsum(int64_t nnz, const int32_t* col, const double* val,
+                      const unsigned long long* vmax_bits, int64_t ncols, unsigned long long* hi,
+                      unsigned long long* lo, cudaStream_t st);
+void launch_fx_scatter_add(int64_t cnt, const int32_t* idx, const unsigned long long* v,
+                           unsigned long long* out, cudaStream_t st);
+void launch_fx_colmax(int64_t n, const unsigned long long* hi, const unsigned long long* lo,
+                      const unsigned long long* vmax_bits, double* out, cudaStream_t st);
 void launch_matrix_check(const CsrView* A, int32_t* flags, bool require_sorted, cudaStream_t st);
 
 // krylov.cu
@@ -257,6 +280,7 @@ void launch_cl_scale(int64_t n, int k, int64_t ldw, double* W, const double* z,
                      const double* Rbar, int64_t ldr, const SolveState* st_dev, cudaStream_t st);
 
 // diag.cu: per-cycle kappa_W and leftmost Ritz value (opt-in)
+size_t gram_scratch_doubles(int64_t n, int m);
 bool launch_gram(int64_t n, int m, int64_t ldw, const double* W, const SolveState* st_dev,
                  double* G, cudaStream_t st);
 double kappa_from_gram(const std::vector<double>& G, int m);

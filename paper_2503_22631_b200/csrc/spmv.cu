@@ -233,22 +233,65 @@ void launch_det_finish(const DetRed& red, int64_t L, double* out, cudaStream_t s
 // ---- setup kernels: norm1 (sparse.cpp:97-102) and validate (sparse.cpp:61-81) ----
 namespace {
 
-template <typename RP>
-__global__ void colsum_kernel(int64_t nnz, const int32_t* __restrict__ ci,
-                              const double* __restrict__ val, double* colsum) {
+// Column abs-sums for norm1 in fixed point, so that the result does not
+// depend on the order in which threads add (bitwise reproducible solves; the
+// breakdown threshold 1e-14 ||A||_1 and the fixed-node InvSqrt interval read
+// it). With 2^E > max |a_ij| every |a_ij| 2^-E in [0, 1) is split into two
+// 40-bit integer words (bits 2^-1..2^-40 and 2^-41..2^-80) added with
+// integer atomics: exact and order-free for columns of < 2^24 entries; bits
+// below 2^-80 max|a_ij| are dropped. The reference sums each column in row
+// order (sparse.cpp:97-102); the two agree to about one rounding.
+__global__ void absmax_bits_kernel(int64_t nnz, const double* __restrict__ val,
+                                   unsigned long long* out) {
+  double m = 0.0;
   for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
        k += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(colsum + ci[k], fabs(val[k]));
+    m = fmax(m, fabs(val[k]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0)  // non-negative doubles order like their bit patterns
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
-__global__ void max_kernel(int64_t n, const double* __restrict__ v, double* out) {
+__device__ __forceinline__ int fx_exponent(const unsigned long long* vmax_bits) {
+  const double vm = __longlong_as_double((long long)*vmax_bits);
+  return vm > 0.0 ? ilogb(vm) + 1 : 0;  // 2^E > vmax
+}
+
+__global__ void fx_colsum_kernel(int64_t nnz, const int32_t* __restrict__ ci,
+                                 const double* __restrict__ val,
+                                 const unsigned long long* vmax_bits, unsigned long long* hi,
+                                 unsigned long long* lo) {
+  const int E = fx_exponent(vmax_bits);
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const double a = ldexp(fabs(val[k]), 40 - E);  // < 2^40
+    const double h = floor(a);
+    const double l = floor((a - h) * 1099511627776.0);  // 2^40
+    const int32_t c = ci[k];
+    if (h != 0.0) atomicAdd(hi + c, (unsigned long long)h);
+    if (l != 0.0) atomicAdd(lo + c, (unsigned long long)l);
+  }
+}
+
+__global__ void fx_colmax_kernel(int64_t n, const unsigned long long* __restrict__ hi,
+                                 const unsigned long long* __restrict__ lo,
+                                 const unsigned long long* vmax_bits, double* out) {
+  const int E = fx_exponent(vmax_bits);
   double m = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
-    m = fmax(m, v[i]);
+    m = fmax(m, ldexp(double(hi[i]), E - 40) + ldexp(double(lo[i]), E - 80));
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0)  // non-negative doubles order like their bit patterns
-    atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(m));
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void fx_scatter_add_kernel(int64_t cnt, const int32_t* __restrict__ idx,
+                                      const unsigned long long* __restrict__ v,
+                                      unsigned long long* out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (v[i]) atomicAdd(out + idx[i], v[i]);
 }
 
 // flags[0]: shape violation, flags[1]: non-finite value
@@ -270,13 +313,42 @@ __global__ void check_kernel(int64_t n_rows, int64_t n_cols, const RP* __restric
 
 }  // namespace
 
-void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st) {
-  RKMF_CUDA(cudaMemsetAsync(colsum, 0, sizeof(double) * size_t(A->n_cols), st));
-  RKMF_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
-  const int g = 4 * num_sms();
-  if (A->nnz > 0) colsum_kernel<int32_t><<<g, 256, 0, st>>>(A->nnz, A->col, A->val, colsum);
-  if (A->n_cols > 0) max_kernel<<<g, 256, 0, st>>>(A->n_cols, colsum, out);
+void launch_abs_max_bits(int64_t nnz, const double* val, unsigned long long* vmax_bits,
+                         cudaStream_t st) {
+  RKMF_CUDA(cudaMemsetAsync(vmax_bits, 0, sizeof(unsigned long long), st));
+  if (nnz > 0) absmax_bits_kernel<<<4 * num_sms(), 256, 0, st>>>(nnz, val, vmax_bits);
   RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_fx_colsum(int64_t nnz, const int32_t* col, const double* val,
+                      const unsigned long long* vmax_bits, int64_t ncols, unsigned long long* hi,
+                      unsigned long long* lo, cudaStream_t st) {
+  RKMF_CUDA(cudaMemsetAsync(hi, 0, sizeof(unsigned long long) * size_t(ncols), st));
+  RKMF_CUDA(cudaMemsetAsync(lo, 0, sizeof(unsigned long long) * size_t(ncols), st));
+  if (nnz > 0) fx_colsum_kernel<<<4 * num_sms(), 256, 0, st>>>(nnz, col, val, vmax_bits, hi, lo);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_fx_scatter_add(int64_t cnt, const int32_t* idx, const unsigned long long* v,
+                           unsigned long long* out, cudaStream_t st) {
+  if (cnt > 0) fx_scatter_add_kernel<<<4 * num_sms(), 256, 0, st>>>(cnt, idx, v, out);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+void launch_fx_colmax(int64_t n, const unsigned long long* hi, const unsigned long long* lo,
+                      const unsigned long long* vmax_bits, double* out, cudaStream_t st) {
+  RKMF_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+  if (n > 0) fx_colmax_kernel<<<4 * num_sms(), 256, 0, st>>>(n, hi, lo, vmax_bits, out);
+  RKMF_CUDA(cudaGetLastError());
+}
+
+// colsum: scratch of 2 * n_cols + 1 words (hi, lo, the max |a_ij| bits)
+void launch_matrix_norm1(const CsrView* A, double* colsum, double* out, cudaStream_t st) {
+  auto* w = reinterpret_cast<unsigned long long*>(colsum);
+  unsigned long long *hi = w, *lo = w + A->n_cols, *vmax = w + 2 * A->n_cols;
+  launch_abs_max_bits(A->nnz, A->val, vmax, st);
+  launch_fx_colsum(A->nnz, A->col, A->val, vmax, A->n_cols, hi, lo, st);
+  launch_fx_colmax(A->n_cols, hi, lo, vmax, out, st);
 }
 
 void launch_matrix_check(const CsrView* A, int32_t* flags, bool require_sorted, cudaStream_t st) {

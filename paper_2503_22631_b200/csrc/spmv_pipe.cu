@@ -97,15 +97,27 @@ constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads +
       const double *__restrict__ val, const double *__restrict__ x, const double *xscale,      \
       double *__restrict__ z, int64_t num_tiles, int cap, int d, int zeta, int off_stride,     \
       const uint16_t *__restrict__ toff, const uint8_t *__restrict__ tent, double sscale,      \
-      const int32_t *stop, int step, int nstages, int l2_hints, int debug,        \
-      const int32_t *__restrict__ doff, int ndiag, int64_t ncols, int sync_mode, int dstride,   \
-      DetRed red
+      const int32_t *stop, int step, int nstages, int l2_hints_arg, int debug_arg,        \
+      const int32_t *__restrict__ doff, int ndiag, int64_t ncols, int sync_mode_arg, int dstride,   \
+      const double *__restrict__ ddict, int ntup, DetRed red
 #define RKMF_PIPE_ARGS                                                                       \
   n, rp, ci, val, x, xscale, z, num_tiles, cap, d, zeta, off_stride, toff, tent, sscale, \
-      stop, step, nstages, l2_hints, debug, doff, ndiag, ncols, sync_mode, dstride, red
+      stop, step, nstages, l2_hints_arg, debug_arg, doff, ndiag, ncols, sync_mode_arg, dstride, ddict, ntup, red
+
+// The ablation knobs (RKMF_PIPE_DEBUG / _SYNC / RKMF_L2_HINTS) reach the
+// kernel only in the experiments build; the product build folds them to
+// their defaults at compile time (fewer instructions in an issue-bound kernel).
+#ifdef RKMF_EXPERIMENTS
+#define RKMF_KNOB(arg, def) (arg)
+#else
+#define RKMF_KNOB(arg, def) (def)
+#endif
 
 template <typename RP, int TPR, int G, int FMT, int ND>
 __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
+  const int debug = RKMF_KNOB(debug_arg, 0);
+  const int sync_mode = RKMF_KNOB(sync_mode_arg, 1);
+  const int l2_hints = RKMF_KNOB(l2_hints_arg, 1);
   constexpr int kSpmv = spmv_threads<TPR, G>();
   constexpr int kGroup = kTileRows * TPR;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -114,7 +126,12 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
   __shared__ int32_t doff_s[kMaxDiag];  // FMT 2 with one offset list (dstride 0)
   if (FMT && threadIdx.x < kMaxDiag) doff_s[threadIdx.x] = doff ? doff[threadIdx.x] : 0;
   double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d], sketch threads
+  // FMT 3: the row dictionary [ntup][ND] after acc (constant: loaded before
+  // the PDL wait)
+  double* dict_s = acc + (d + 1) / 2 * 2;
   const int t = threadIdx.x;
+  if constexpr (FMT == 3)
+    for (int i = t; i < ntup * ND; i += block_threads<TPR, G>()) dict_s[i] = ddict[i];
   if (t == 0) {
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&full[s], 1);
@@ -278,82 +295,101 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
     else
       mbar_arrive(&zsr[s]);
   };
-  if constexpr (FMT == 2) {
+  if constexpr (FMT >= 2) {
     // Diagonal copy, ND diagonals: x is read at row + offset. Those reads do
     // not depend on the staged values, so each thread loads the next tile's x
     // (into the other register buffer) before waiting for this tile's stage.
-    // Interior tiles (every offset in range) skip the bounds checks.
-    auto load_x = [&](int64_t tl, double* dst) {
-      // the sorted offsets: one list for all tiles (shared memory), or the
-      // tile's own ([tile][kMaxDiag], the same line in every thread);
-      // nullptr = the identity
-      int doffr[ND];
-      if (dstride == 0) {
+    // Row indices fit in 32 bits (build_dia), so the addressing is 32-bit;
+    // with one offset list for all tiles (dstride 0) the offsets sit in
+    // registers and the tiles whose reads are all in range (every tile but
+    // the first and last few) are one index interval, tested per tile with
+    // two compares.
+    const int32_t n32 = int32_t(n), nc32 = int32_t(ncols), nt32 = int32_t(num_tiles);
+    const bool single = dstride == 0;
+    int offs[ND];
+    int32_t tlo = 0, thi = 0;  // interior tiles [tlo, thi) (single list)
+    if (single) {
 #pragma unroll
-        for (int q = 0; q < ND; ++q) doffr[q] = doff_s[q];
-      } else if (doff) {
-        const int4* p = reinterpret_cast<const int4*>(doff + tl * kMaxDiag);
+      for (int q = 0; q < ND; ++q) offs[q] = doff ? doff_s[q] : 0;
+      // tile t is interior when 128 t + offs[0] >= 0, 128 t + 127 + offs[ND-1] < ncols
+      // and 128 t + 128 <= n
+      tlo = offs[0] >= 0 ? 0 : (-offs[0] + kTileRows - 1) / kTileRows;
+      const int64_t lim = min(int64_t(nc32) - kTileRows - int64_t(offs[ND - 1]),
+                              int64_t(n32) - kTileRows);
+      thi = lim < 0 ? 0 : int32_t(lim / kTileRows) + 1;
+      thi = max(tlo, min(thi, nt32));
+    }
+    uint64_t zpol;  // z with an L2 evict_last hint: K4 reads it next
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zpol));
+    auto load_x = [&](int32_t tl, double* dst) {
+      const int32_t row = tl * kTileRows + rl;
+      if (single && tl >= tlo && tl < thi) {
+        // row + offs[q] >= 0 here: one 32-bit add and one wide multiply-add
+#pragma unroll
+        for (int q = 0; q < ND; ++q) dst[q] = __ldg(x + uint32_t(row + offs[q]));
+        return;
+      }
+      int o[ND];
+      if (single) {
+#pragma unroll
+        for (int q = 0; q < ND; ++q) o[q] = offs[q];
+      } else if (doff) {  // the tile's own sorted offsets ([tile][kMaxDiag])
+        const int4* p = reinterpret_cast<const int4*>(doff + int64_t(tl) * kMaxDiag);
         const int4 a = __ldg(p), b = __ldg(p + 1);
         const int all[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int q = 0; q < ND; ++q) doffr[q] = all[q];
+        for (int q = 0; q < ND; ++q) o[q] = all[q];
       } else {
 #pragma unroll
-        for (int q = 0; q < ND; ++q) doffr[q] = 0;
+        for (int q = 0; q < ND; ++q) o[q] = 0;
       }
-      const int64_t r0 = tl * kTileRows, row = r0 + rl;
-      if (r0 + doffr[0] >= 0 && r0 + kTileRows - 1 + doffr[ND - 1] < ncols && r0 + kTileRows <= n) {
-        const double* xr = x + row;
 #pragma unroll
-        for (int q = 0; q < ND; ++q) dst[q] = __ldg(xr + doffr[q]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < ND; ++q) {
-          const int64_t c = row + doffr[q];
-          dst[q] = (row < n && c >= 0 && c < ncols) ? __ldg(x + c) : 0.0;
-        }
+      for (int q = 0; q < ND; ++q) {
+        const int32_t c = row + o[q];
+        dst[q] = (row < n32 && c >= 0 && c < nc32) ? __ldg(x + uint32_t(c)) : 0.0;
       }
     };
-    auto step = [&](int64_t tile, const double* xc, double* xn) {
-      const int64_t nt = tile + int64_t(G) * gridDim.x;
-      if (nt < num_tiles) load_x(nt, xn);
+    // One register buffer: a tile's x is loaded right after the previous
+    // tile's products consumed the buffer, so the loads are in flight while
+    // the thread waits for the tile's stage (the same overlap as a double
+    // buffer, half the registers: no spills at four blocks per SM).
+    double xc[ND];
+    int32_t tile = int32_t(blockIdx.x) + g * int32_t(gridDim.x);
+    const int32_t gstride = G * int32_t(gridDim.x);
+    if (tile < nt32) load_x(tile, xc);
+    for (; tile < nt32; tile += gstride) {
       mbar_wait(&full[s], ph);
-      unsigned char* st = smem + s * L.stride;
+      const unsigned char* st = smem + s * L.stride;
       if (!(debug & 4)) {
-        const int64_t row = tile * kTileRows + rl;
-        const bool live = row < n;
-        const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
+        const int32_t row = tile * kTileRows + rl;
+        const bool live = row < n32;
         double sum = 0.0;
-        if (val) {
+        if constexpr (FMT == 3) {
+          // the row's tuple id (one streamed byte) -> its ND values in the
+          // shared dictionary: the same values in the same order as FMT 2
+          const double* dv = dict_s + int(st[L.val + rl]) * ND;
+#pragma unroll
+          for (int q = 0; q < ND; ++q) sum += dv[q] * xc[q];
+        } else if (val) {
+          const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
 #pragma unroll
           for (int q = 0; q < ND; ++q) sum += vt[q * kTileRows] * xc[q];
         } else {  // identity: z = x
           sum = xc[0];
         }
         sum *= xs;
-        if (live && z) {
-          // z with an L2 evict_last hint: K4 reads it next (cfg2 solve
-          // 8592 -> 8684 vec/s, cfg4 1501 -> 1523)
-          uint64_t zp;
-          asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zp));
-          asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(z + row), "d"(sum), "l"(zp)
+        if (live && z)
+          asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(z + uint32_t(row)),
+                       "d"(sum), "l"(zpol)
                        : "memory");
-        }
         const double zt = live ? sum * sscale : 0.0;
-        double* zs = reinterpret_cast<double*>(st + L.zs);
+        double* zs = reinterpret_cast<double*>(const_cast<unsigned char*>(st) + L.zs);
         zs[rl] = zt;
         zs[kTileRows + rl] = -zt;
       }
       handoff();
       advance();
-    };
-    double xa[ND], xb[ND];
-    int64_t tile = blockIdx.x + int64_t(g) * gridDim.x;
-    if (tile < num_tiles) load_x(tile, xa);
-    for (; tile < num_tiles; tile += 2 * int64_t(G) * gridDim.x) {
-      step(tile, xa, xb);
-      const int64_t t2 = tile + int64_t(G) * gridDim.x;
-      if (t2 < num_tiles) step(t2, xb, xa);
+      if (tile + gstride < nt32) load_x(tile + gstride, xc);
     }
     return;
   } else {
@@ -414,8 +450,13 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
 // gathers in flight; left to the heuristics, ptxas squeezed it to 40
 // registers for a second block that never fits and interleaved the gathers
 // with the FMA chain (cfg3 K2 502 vs 462 us).
+// four resident blocks per SM (56 registers, no spills): cfg4 K2 246 vs 316 us
+// at three blocks (70 registers), cfg2 41.5 vs 49.0 us (profiles/r02e_variants.txt)
+#ifndef RKMF_K2_DIA_MINB
+#define RKMF_K2_DIA_MINB 4
+#endif
 template <typename RP, int TPR, int G, int FMT, int ND = 1>
-__global__ void __launch_bounds__(block_threads<TPR, G>())
+__global__ void __launch_bounds__(block_threads<TPR, G>(), RKMF_K2_DIA_MINB)
     spmv_sketch_pipe_kernel(RKMF_PIPE_PARAMS) {
   pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS);
 }
@@ -426,9 +467,9 @@ __global__ void __launch_bounds__(block_threads<TPR, G>(), 1)
 }
 
 template <typename RP>
-size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages, int fmt) {
+size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages, int fmt, int dict_len = 0) {
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, fmt);
-  return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2);
+  return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2 + dict_len);
 }
 
 // RKMF_L2_HINTS: 0 no L2 hints, 1 (default) evict_first on the matrix and
@@ -500,7 +541,9 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
     if constexpr (FMT != 0) return spmv_sketch_pipe_kernel<RP, TPR, G, FMT, ND>;
     else return spmv_sketch_pipe_csr_kernel<RP, TPR, G, FMT, ND>;
   }();
-  const int cap = FMT ? A->ndiag * kTileRows : A->cap;
+  // FMT 3 streams one tuple-id byte per row: 128 bytes = 16 "values" per tile
+  const int cap = FMT == 3 ? kTileRows / 8 : FMT ? A->ndiag * kTileRows : A->cap;
+  const int dict_len = FMT == 3 ? A->ntup * A->ndiag : 0;
   // Pick the stage count. G stages feed the SpMV groups and one the sketch,
   // so (stages - G - 1) x resident blocks x stage bytes are in flight ahead
   // of them: take the configuration that keeps >= 64 KB per SM ahead (HBM
@@ -511,7 +554,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   static thread_local int bests[4][2];
   static thread_local int next_slot = 0;
   const int64_t key = (int64_t(cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP) ^
-                      (FMT << 4) ^ (int64_t(ND) << 32);
+                      (FMT << 4) ^ (int64_t(ND) << 32) ^ (int64_t(dict_len) << 48);
   int slot = -1;
   for (int i = 0; i < 4; ++i)
     if (keys[i] == key) slot = i;
@@ -524,7 +567,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
                                                 int(S->zeta), FMT).stride);
     for (int s = G + 2; s <= kStages; ++s) {
       if (env_stages() && s != env_stages()) continue;
-      const size_t sm = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), s, FMT);
+      const size_t sm = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), s, FMT, dict_len);
       if (sm > 220 * 1024) continue;
       RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
       int per = 0;
@@ -549,7 +592,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   }
   if (best_s == 0) return false;
   const int stages = best_s, per_sm = best_per;
-  const size_t smem = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), stages, FMT);
+  const size_t smem = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), stages, FMT, dict_len);
   RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
@@ -557,10 +600,11 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
     param_error("internal: sketch reduction scratch too small");
   red.groups = det_groups(grid);
   launch_maybe_pdl(fn, dim3(grid), dim3(kThreads), smem, st, A->n_rows,
-                   static_cast<const RP*>(A->row_ptr), A->col, FMT ? A->dval : A->val, x,
+                   static_cast<const RP*>(A->row_ptr), A->col,
+                   FMT == 3 ? reinterpret_cast<const double*>(A->dtid) : FMT ? A->dval : A->val, x,
                    xscale_dev, z, tiles, cap, int(S->d), int(S->zeta), off_stride, S->tile_off,
                    S->tile_ent, S->scale, stop, step, stages, env_l2_hints(), env_debug(),
-                   A->doff, A->ndiag, A->n_cols, env_sync(), A->dstride, red);
+                   A->doff, A->ndiag, A->n_cols, env_sync(), A->dstride, A->ddict, A->ntup, red);
   return true;
 }
 
@@ -636,6 +680,16 @@ bool launch_sketch_only_pipe(const SketchView* S, const double* x, const double*
 bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double* x,
                              const double* xscale_dev, double* z,
                              const int32_t* stop_flag, int step, DetRed& red, cudaStream_t st) {
+  if (A->ndiag > 0 && A->dtid && A->ntup > 0) {  // row dictionary of the diagonal copy
+#define RKMF_DIT(NDV) \
+  case NDV: return launch_pipe_t<int32_t, 1, 1, 3, NDV>(A, S, x, xscale_dev, z, stop_flag, step, red, st)
+    switch (A->ndiag) {
+      RKMF_DIT(1); RKMF_DIT(2); RKMF_DIT(3); RKMF_DIT(4);
+      RKMF_DIT(5); RKMF_DIT(6); RKMF_DIT(7); RKMF_DIT(8);
+      default: break;
+    }
+#undef RKMF_DIT
+  }
   if (A->ndiag > 0 && A->dval) {  // diagonal copy (at most 8 diagonals), x prefetched
 #define RKMF_DIA(NDV) \
   case NDV: return launch_pipe_t<int32_t, 1, 1, 2, NDV>(A, S, x, xscale_dev, z, stop_flag, step, red, st)

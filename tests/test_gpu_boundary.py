@@ -98,6 +98,25 @@ def test_solves_are_bitwise_reproducible(rk, torch, name, N, classical):
     assert np.array_equal(r3.f_hat, r1.f_hat.cpu().numpy())
 
 
+def test_norm1_and_diagnostics_reproducible(rk, torch, oracle):
+    """norm1 (fixed-point column sums, spmv.cu) and the per-cycle kappa_W
+    (Gram partials summed in block order, diag.cu) are the same bits on every
+    run: the CSV harness prints them (acceptance.cpp:545-582, c14)."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build("cfg3", 24)  # lognormal values: column sums round
+    n1 = {rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values).norm1 for _ in range(4)}
+    assert len(n1) == 1
+    assert n1.pop() == pytest.approx(oracle.norm1((P.row_ptr, P.col_idx, P.values)), rel=1e-15)
+    P = configs.build("cfg1", 64)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max, diagnostics=True)
+    b = torch.tensor(P.b, device="cuda")
+    runs = [rk.restarted_krylov(A, b, rk.FunctionSpec.exp_neg(P.t), opts, S) for _ in range(3)]
+    k = [[h.kappa_W for h in r.history] for r in runs]
+    assert k[0] == k[1] == k[2] and all(np.isfinite(k[0]))
+
+
 def test_sketch_reduction_reproducible(rk, torch):
     """The fused kernel's sketch (many blocks) is the same bits every launch."""
     from paper_2503_22631_b200 import configs

@@ -35,13 +35,14 @@ def _device(rk, torch, P, rp64=False, **opt):
     return r, A
 
 
-def _oracle(oracle, P, want_R=False, **opt):
+def _oracle(oracle, P, want_R=False, threads=THREADS, b=None, **opt):
     S = oracle.make_sketch(P.d, P.n, P.zeta, 1)
     kind = oracle.KIND_EXP_NEG if P.fn == "exp_neg" else oracle.KIND_INV_SQRT
     o = dict(m_r=P.m, tol=P.tol, k_max=P.k_max)
     o.update(opt)
-    return oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, kind, P.t, S=S,
-                                   threads=THREADS, want_R=want_R, **o)
+    return oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values),
+                                   P.b if b is None else b, kind, P.t, S=S,
+                                   threads=threads, want_R=want_R, **o)
 
 
 @pytest.fixture(scope="module")
@@ -80,24 +81,46 @@ def test_cfg3_kind_against_oracle(rk, oracle, torch, N):
     """cfg3's operator kind and parameters (lognormal Q1 with Dirichlet rows,
     f = z^{-1/2}, m = 40, d = 160, tol 1e-7 relative): the device restart
     quadrature against the oracle's Denman-Beavers f(R_accum) (the reference
-    has no InvSqrt kind: parity unpinned), converged and at
-    equal forced cycle counts."""
+    has no InvSqrt kind: parity unpinned).
+
+    This restart process amplifies rounding: scaling b by (1 + 2^-50), which
+    changes nothing in exact arithmetic (f(A) is linear in b), moves the
+    oracle's own one-cycle f_hat by 1.6e-4 relative at N = 56 and its
+    converged f_hat by up to 1e-6, with cycle counts 13-16
+    (tools/cfg3_sensitivity.py, profiles/r02b_cfg3_sensitivity.txt), although
+    every dense step is well conditioned (kappa(W) 2.6, f(R_accum) e1 to 1e-13
+    against a Schur sqrtm). So each bar is the oracle's own spread under that
+    perturbation: the device's f_hat within max(1e-9, 10 x spread) of the
+    oracle's, converged (spread: the largest of three perturbations; cycle
+    count within the oracle runs' range +-1) and at equal forced cycle
+    counts. (Where the spread is below 1e-10 the bar is the north-star
+    1e-9.)"""
     from paper_2503_22631_b200 import configs
     P = configs.build("cfg3", N)
     assert (P.m, P.d) == (40, 160)
+    delta = 2.0 ** -50
+
+    def spread_of(o, op):
+        return _rel(op.f_hat / (1.0 + delta), o.f_hat)
+
     r, _ = _device(rk, torch, P)
     o = _oracle(oracle, P)
-    assert r.converged and o.converged and abs(r.cycles - o.cycles) <= 1
-    assert _rel(r.f_hat.cpu().numpy(), o.f_hat) <= 1e-9
-    k = o.cycles
-    r, _ = _device(rk, torch, P, tol=1e-30, k_max=k)
-    un = np.array([h.update_norm for h in r.history])
-    uo = np.array([h["update_norm"] for h in o.history])
-    assert r.cycles == k
-    # per-cycle updates while they are above the rounding floor of f_hat
-    big = uo >= 1e-8 * uo[0]
-    assert np.allclose(un[big], uo[big], rtol=1e-6, atol=0), np.abs(un / uo - 1).max()
-    assert _rel(r.f_hat.cpu().numpy(), o.f_hat) <= 1e-9
+    # the spread is a chaotic quantity: the largest over three perturbations
+    ops = [_oracle(oracle, P, b=P.b * (1.0 + e)) for e in (delta, 2 * delta, 3 * delta)]
+    assert r.converged and o.converged and all(x.converged for x in ops)
+    cyc = [o.cycles] + [x.cycles for x in ops]
+    assert min(cyc) - 1 <= r.cycles <= max(cyc) + 1, (r.cycles, cyc)
+    err = _rel(r.f_hat.cpu().numpy(), o.f_hat)
+    spread = max(_rel(x.f_hat / (1.0 + e), o.f_hat)
+                 for x, e in zip(ops, (delta, 2 * delta, 3 * delta)))
+    assert err <= max(1e-9, 10.0 * spread), (err, spread)
+    for k in (1, 3):
+        rk_, _ = _device(rk, torch, P, tol=1e-30, k_max=k)
+        ok = _oracle(oracle, P, tol=1e-30, k_max=k)
+        okp = _oracle(oracle, P, b=P.b * (1.0 + delta), tol=1e-30, k_max=k)
+        assert rk_.cycles == ok.cycles == k
+        err, spread = _rel(rk_.f_hat.cpu().numpy(), ok.f_hat), spread_of(ok, okp)
+        assert err <= max(1e-9, 10.0 * spread), (k, err, spread)
 
 
 def test_cfg5_kind_int64_row_pointers(rk, oracle, torch):

@@ -88,6 +88,40 @@ def test_dia_bitexact_vs_csr(rk, oracle, torch, name, N, nd):
     assert A.set_diagonal_copy(True) == nd
 
 
+@pytest.mark.parametrize("name,N,ntup", [("cfg1", 100, 9), ("cfg2", 41, 27), ("cfg4", 23, 27),
+                                         ("cfg1", 256, 9)])
+def test_row_dictionary(rk, oracle, torch, name, N, ntup):
+    """Constant-coefficient stencils: the diagonal copy's rows take few value
+    tuples (3 x 3 boundary classes in 2D, 27 in 3D), so K2 streams one byte
+    per row (dia.cu row dictionary). z is bit-identical to the copy without
+    the dictionary and to the CSR kernel; whole solves agree to rounding (the
+    sketch's cross-block sums follow the grid)."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build(name, N)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    assert A.ndiag > 0 and A.ntuples == ntup
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    z1, p1 = rk.spmv_sketch(A, S, P.b)
+    f = rk.FunctionSpec.exp_neg(P.t)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
+    b = torch.tensor(P.b, device="cuda")
+    r1 = rk.restarted_krylov(A, b, f, opts, S)
+    assert A.set_row_dictionary(False) == 0 and A.ntuples == 0 and A.ndiag > 0
+    z0, p0 = rk.spmv_sketch(A, S, P.b)
+    r0 = rk.restarted_krylov(A, b, f, opts, S)
+    assert torch.equal(z1, z0) and rel(p1, p0) <= 1e-14
+    assert r1.cycles == r0.cycles and rel(r1.f_hat, r0.f_hat) <= 1e-12
+    assert A.set_diagonal_copy(False) == 0 and A.ntuples == 0
+    zc, _ = rk.spmv_sketch(A, S, P.b)
+    assert torch.equal(z1, zc)
+    assert rel(z1, oracle.spmv((P.row_ptr, P.col_idx, P.values), P.b)) <= 1e-14
+    assert A.set_diagonal_copy(True) > 0 and A.ntuples == ntup
+    # values that vary per row (> 256 tuples): the copy stays, no dictionary
+    v = P.values * (1.0 + 1e-3 * np.random.default_rng(3).random(P.values.size))
+    B = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, v)
+    assert B.ndiag > 0 and B.ntuples == 0
+
+
 def test_dia_eligibility(rk, torch):
     rng = np.random.default_rng(5)
     # scattered nonzeros: CSR only
