@@ -142,15 +142,27 @@ def class_bytes(n, nnz, m, total_m, cycles):
             "start_sketch_init": start}
 
 
-def k2_streamed_bytes(n, nnz, ndiag, d, zeta):
+def k2_streamed_bytes(n, nnz, ndiag, ntuples, d, zeta):
     """Bytes K2 streams by design per launch: the matrix stream it actually
-    reads (the diagonal copy: 8 ndiag per row; else CSR 12 nnz + 4 (n+1)), the
-    sketch tile layout (per 128-row tile a uint16 header of 2 off_stride and
-    128 zeta entry bytes), x read and z written."""
+    reads (the diagonal copy's row dictionary: one tuple-id byte per row; the
+    diagonal copy: 8 ndiag per row; else CSR 12 nnz + 4 (n+1)), the sketch
+    tile layout (per 128-row tile a uint16 header of 2 off_stride and 128 zeta
+    entry bytes), x read and z written."""
     tiles = (n + 127) // 128
     off_stride = (2 * d + 1 + 7) // 8 * 8
-    mat = 8 * ndiag * tiles * 128 if ndiag else 12 * nnz + 4 * (n + 1)
+    if ndiag and ntuples:
+        mat = tiles * 128
+    elif ndiag:
+        mat = 8 * ndiag * tiles * 128
+    else:
+        mat = 12 * nnz + 4 * (n + 1)
     return mat + tiles * (2 * off_stride + 128 * zeta) + 16 * n
+
+
+def matrix_stream(A):
+    if A.ndiag and A.ntuples:
+        return f"diagonal copy ({A.ndiag} diagonals) as a row dictionary ({A.ntuples} tuples)"
+    return f"diagonal copy ({A.ndiag} diagonals)" if A.ndiag else "CSR"
 
 
 # ------------------------------ reference arm ------------------------------
@@ -435,12 +447,11 @@ def run_ours(args):
             kernels[cls] = ent
         k2 = kernels["spmv_sketch"]
         if k2["launches"]:
-            sb = k2_streamed_bytes(w.n, w.nnz, A.ndiag, w.d, w.zeta)
+            sb = k2_streamed_bytes(w.n, w.nnz, A.ndiag, A.ntuples, w.d, w.zeta)
             gbs = sb * k2["launches"] / (k2["ms"] / 1e3) / 1e9
             k2.update({"streamed_bytes_per_launch": sb, "streamed_gbs": gbs,
                        "streamed_frac": gbs / peak,
-                       "stream": (f"diagonal copy ({A.ndiag} diagonals)" if A.ndiag else "CSR")
-                       + " + sketch tile layout + x + z"})
+                       "stream": matrix_stream(A) + " + sketch tile layout + x + z"})
         dom = max((c for c in cb if kernels[c]["ms"] > 0), key=lambda c: kernels[c]["ms"])
         dk = kernels[dom]
         traffic, capture = (load_traffic(name, dom) if world == 1 else (None, None))
@@ -464,8 +475,7 @@ def run_ours(args):
                "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generators, BASELINE.json shapes)",
                "config": workload_config(name, w.meta, world),
-               "device_config": {"matrix_stream": (f"diagonal copy, {A.ndiag} diagonals"
-                                                   if A.ndiag else "CSR"),
+               "device_config": {"matrix_stream": matrix_stream(A),
                                  "rows_per_gpu": w.n, "nnz_per_gpu": w.nnz},
                "comm": comm,
                "solve": {"cycles": res.cycles, "total_m": res.total_m,

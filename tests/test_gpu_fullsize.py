@@ -91,7 +91,7 @@ def test_cfg3_kind_against_oracle(rk, oracle, torch, N):
     every dense step is well conditioned (kappa(W) 2.6, f(R_accum) e1 to 1e-13
     against a Schur sqrtm). So each bar is the oracle's own spread under that
     perturbation: the device's f_hat within max(1e-9, 10 x spread) of the
-    oracle's, converged (spread: the largest of three perturbations; cycle
+    oracle's, converged (spread: the larger of two perturbations; cycle
     count within the oracle runs' range +-1) and at equal forced cycle
     counts. (Where the spread is below 1e-10 the bar is the north-star
     1e-9.)"""
@@ -105,14 +105,14 @@ def test_cfg3_kind_against_oracle(rk, oracle, torch, N):
 
     r, _ = _device(rk, torch, P)
     o = _oracle(oracle, P)
-    # the spread is a chaotic quantity: the largest over three perturbations
-    ops = [_oracle(oracle, P, b=P.b * (1.0 + e)) for e in (delta, 2 * delta, 3 * delta)]
+    # the spread is a chaotic quantity: the larger over two perturbations
+    ops = [_oracle(oracle, P, b=P.b * (1.0 + e)) for e in (delta, 3 * delta)]
     assert r.converged and o.converged and all(x.converged for x in ops)
     cyc = [o.cycles] + [x.cycles for x in ops]
     assert min(cyc) - 1 <= r.cycles <= max(cyc) + 1, (r.cycles, cyc)
     err = _rel(r.f_hat.cpu().numpy(), o.f_hat)
     spread = max(_rel(x.f_hat / (1.0 + e), o.f_hat)
-                 for x, e in zip(ops, (delta, 2 * delta, 3 * delta)))
+                 for x, e in zip(ops, (delta, 3 * delta)))
     assert err <= max(1e-9, 10.0 * spread), (err, spread)
     for k in (1, 3):
         rk_, _ = _device(rk, torch, P, tol=1e-30, k_max=k)
