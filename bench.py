@@ -142,21 +142,20 @@ def class_bytes(n, nnz, m, total_m, cycles):
             "start_sketch_init": start}
 
 
-def k2_streamed_bytes(n, nnz, ndiag, ntuples, d, zeta):
+def k2_streamed_bytes(n, nnz, ndiag, ntuples, layout):
     """Bytes K2 streams by design per launch: the matrix stream it actually
     reads (the diagonal copy's row dictionary: one tuple-id byte per row; the
     diagonal copy: 8 ndiag per row; else CSR 12 nnz + 4 (n+1)), the sketch
-    tile layout (per 128-row tile a uint16 header of 2 off_stride and 128 zeta
-    entry bytes), x read and z written."""
+    tile layout (per 128-row tile its header and entry block,
+    S.layout_bytes_per_tile()), x read and z written."""
     tiles = (n + 127) // 128
-    off_stride = (2 * d + 1 + 7) // 8 * 8
     if ndiag and ntuples:
         mat = tiles * 128
     elif ndiag:
         mat = 8 * ndiag * tiles * 128
     else:
         mat = 12 * nnz + 4 * (n + 1)
-    return mat + tiles * (2 * off_stride + 128 * zeta) + 16 * n
+    return mat + tiles * sum(layout) + 16 * n
 
 
 def matrix_stream(A):
@@ -447,7 +446,7 @@ def run_ours(args):
             kernels[cls] = ent
         k2 = kernels["spmv_sketch"]
         if k2["launches"]:
-            sb = k2_streamed_bytes(w.n, w.nnz, A.ndiag, A.ntuples, w.d, w.zeta)
+            sb = k2_streamed_bytes(w.n, w.nnz, A.ndiag, A.ntuples, w.S.layout_bytes_per_tile())
             gbs = sb * k2["launches"] / (k2["ms"] / 1e3) / 1e9
             k2.update({"streamed_bytes_per_launch": sb, "streamed_gbs": gbs,
                        "streamed_frac": gbs / peak,

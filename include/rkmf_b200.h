@@ -174,6 +174,10 @@ int rkmf_sketch_destroy(rkmf_sketch* S);
 /* SketchOperator::scale (default 1/sqrt(zeta)); settable as the reference's
  * tests do (test_sketch.cpp:162-173). */
 int rkmf_sketch_set_scale(rkmf_sketch* S, double scale);
+/* Bytes per 128-column tile of the device tile layout the fused kernel
+ * streams: the header and the entry block (no reference counterpart; for
+ * bandwidth accounting). */
+int rkmf_sketch_layout_info(const rkmf_sketch* S, int64_t* header_bytes, int64_t* entry_bytes);
 /* Copies rows (n*zeta int64) and signs (n*zeta int8) to the host. */
 int rkmf_sketch_export(rkmf_context* ctx, const rkmf_sketch* S, int64_t* h_rows, int8_t* h_signs,
                        double* h_scale);

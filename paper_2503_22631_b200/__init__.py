@@ -137,6 +137,7 @@ SYMBOLS = [
     ("rkmf_sketch_create", C.c_int, [_P, _I64, _I64, _I64, _U64, _PP]),
     ("rkmf_sketch_destroy", C.c_int, [_P]),
     ("rkmf_sketch_set_scale", C.c_int, [_P, _D]),
+    ("rkmf_sketch_layout_info", C.c_int, [_P, _P, _P]),
     ("rkmf_sketch_export", C.c_int, [_P, _P, _P, _P, _P]),
     ("rkmf_spmv", C.c_int, [_P, _P, _P, _P]),
     ("rkmf_sketch_apply", C.c_int, [_P, _P, _P, _P]),
@@ -449,6 +450,12 @@ class SketchOperator:
     def __init__(self, ctx: Context, handle, d, n, zeta, seed):
         self.ctx, self.h, self.d, self.n, self.zeta, self.seed = ctx, handle, d, n, zeta, seed
         self._scale = 1.0 / math.sqrt(zeta)
+
+    def layout_bytes_per_tile(self):
+        """(header, entry) bytes per 128-column tile of the layout K2 streams."""
+        h, e = C.c_int64(), C.c_int64()
+        lib().rkmf_sketch_layout_info(self.h, C.byref(h), C.byref(e))
+        return h.value, e.value
 
     @property
     def scale(self) -> float:

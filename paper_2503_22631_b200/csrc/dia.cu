@@ -229,8 +229,10 @@ void drop_dia_dict(rkmf_matrix* M) {
   if (M->dia_dict) cudaFree(M->dia_dict);
   M->dia_tid = nullptr;
   M->dia_dict = nullptr;
+  M->dia_dict_host.clear();
   M->view.dtid = nullptr;
   M->view.ddict = nullptr;
+  M->view.ddict_host = nullptr;
   M->view.ntup = 0;
 }
 
@@ -305,8 +307,12 @@ void build_dia_dict(rkmf_matrix* M) {
   RKMF_CUDA(cudaMemcpyAsync(hf, misc.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
   RKMF_CUDA(cudaStreamSynchronize(st));
   if (hf[1]) return drop_dia_dict(M);
+  M->dia_dict_host.assign(size_t(ntup) * size_t(nd), 0.0);
+  RKMF_CUDA(cudaMemcpy(M->dia_dict_host.data(), M->dia_dict, sizeof(double) * size_t(ntup) * size_t(nd),
+                       cudaMemcpyDeviceToHost));
   M->view.dtid = M->dia_tid;
   M->view.ddict = M->dia_dict;
+  M->view.ddict_host = M->dia_dict_host.data();
   M->view.ntup = ntup;
 }
 

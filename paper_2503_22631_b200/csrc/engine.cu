@@ -744,17 +744,20 @@ int rkmf_sketch_create_partitioned(rkmf_context* ctx, int64_t d, int64_t n_globa
       const int64_t off_stride = tile_off_stride(d);
       RKMF_CUDA(cudaMalloc(&S->rows, sizeof(uint16_t) * size_t(std::max<int64_t>(n * zeta, 1))));
       RKMF_CUDA(cudaMalloc(&S->signs, size_t(std::max<int64_t>(n * zeta, 1))));
+      launch_sketch_generate(d, n, col_begin, zeta, seed, S->rows, S->signs, ctx->stream);
       // one allocation for the tile layout (header | entries), so a single L2
       // access-policy window can keep it resident across steps
+      S->ent_stride = sketch_tiles_stride(d, n, zeta, S->rows, ctx->stream);
       const size_t ob = round_up(int64_t(sizeof(uint16_t)) * std::max<int64_t>(tiles * off_stride, 1), 256);
-      const size_t eb = size_t(std::max<int64_t>(tiles * kTileRows * zeta, 16)) + 16;
+      const size_t eb = size_t(std::max<int64_t>(tiles * S->ent_stride, 16)) + 16;
       void* tl = nullptr;
       RKMF_CUDA(cudaMalloc(&tl, ob + eb));
       S->tile_off = static_cast<uint16_t*>(tl);
       S->tile_ent = static_cast<uint8_t*>(tl) + ob;
       S->layout_bytes = ob + eb;
-      launch_sketch_generate(d, n, col_begin, zeta, seed, S->rows, S->signs, ctx->stream);
-      launch_sketch_tiles(d, n, zeta, S->rows, S->signs, S->tile_off, S->tile_ent, ctx->stream);
+      launch_sketch_tiles(d, n, zeta, S->rows, S->signs, S->tile_off, S->tile_ent, S->ent_stride,
+                          ctx->stream);
+      ctx->launches += 1;
       ctx->launches += 2;
       RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
@@ -781,6 +784,13 @@ int rkmf_sketch_destroy(rkmf_sketch* S) {
 int rkmf_sketch_set_scale(rkmf_sketch* S, double scale) {
   if (!S) return RKMF_PARAMETER_ERROR;
   S->scale = scale;
+  return RKMF_OK;
+}
+
+int rkmf_sketch_layout_info(const rkmf_sketch* S, int64_t* header_bytes, int64_t* entry_bytes) {
+  if (!S) return RKMF_PARAMETER_ERROR;
+  if (header_bytes) *header_bytes = int64_t(sizeof(uint16_t)) * tile_off_stride(S->d);
+  if (entry_bytes) *entry_bytes = S->ent_stride;
   return RKMF_OK;
 }
 

@@ -235,6 +235,7 @@ struct rkmf_matrix {
   int32_t* dia_off = nullptr;  // its sorted diagonal offsets
   uint8_t* dia_tid = nullptr;  // optional row dictionary of the copy: tuple ids
   double* dia_dict = nullptr;  // and the distinct row tuples
+  std::vector<double> dia_dict_host;  // host copy (K2 passes small ones as kernel parameters)
   bool partitioned = false;
   HaloPlan halo;
   int64_t n_rows_global() const { return partitioned ? halo.n_global : view.n_rows; }
@@ -251,6 +252,7 @@ struct rkmf_sketch {
   int8_t* signs = nullptr;
   uint16_t* tile_off = nullptr;  // one allocation: header, then entries
   uint8_t* tile_ent = nullptr;
+  int64_t ent_stride = 0;  // entry bytes per tile (sketch_tiles_stride)
   size_t layout_bytes = 0;
   SketchView view() const {
     SketchView v;
@@ -259,6 +261,7 @@ struct rkmf_sketch {
     v.zeta = zeta;
     v.tile_off = tile_off;
     v.tile_ent = tile_ent;
+    v.ent_stride = ent_stride;
     v.scale = scale;
     return v;
   }

@@ -133,9 +133,12 @@ struct SolveState {
 // columns [j0, j0 + n) of the global operator (j0 = 0 for a whole sketch)
 void launch_sketch_generate(int64_t d, int64_t n, int64_t j0, int64_t zeta, uint64_t seed,
                             uint16_t* rows, int8_t* signs, cudaStream_t st);
+// bytes per tile the entry layout needs (the largest tile's), then the layout
+int64_t sketch_tiles_stride(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
+                            cudaStream_t st);
 void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
                          const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
-                         cudaStream_t st);
+                         int64_t ent_stride, cudaStream_t st);
 void launch_sketch_export(int64_t count, const uint16_t* rows, const int8_t* signs,
                           int64_t* rows64, cudaStream_t st);
 
@@ -160,6 +163,7 @@ struct CsrView {
   // tuple id, ddict[id * ndiag + q] its values. ntup == 0 when absent.
   const uint8_t* dtid;
   const double* ddict;
+  const double* ddict_host;  // host copy of ddict
   int ntup;
 };
 constexpr int kMaxDiag = 8;
@@ -170,48 +174,82 @@ constexpr int64_t kRpPad = 136;
 constexpr int64_t kNnzPad = 8;
 struct SketchView {
   int64_t d, n, zeta;
-  const uint16_t* tile_off;  // [num_tiles][tile_off_stride(d)]: slot offsets, slot bins
-  const uint8_t* tile_ent;   // [num_tiles][kTileRows*zeta]: local row | sign<<7
+  const uint16_t* tile_off;  // [num_tiles][tile_off_stride(d)]: the tile header (below)
+  const uint8_t* tile_ent;   // [num_tiles][ent_stride]: entries, local row | sign<<7
+  int64_t ent_stride;        // bytes per tile of tile_ent (a multiple of 128)
   double scale;
 };
-// Per-tile sketch header (uint16): off[d+1] slot offsets, then bin[d] (the
-// sketch row of each slot), padded to 16 bytes.
-__host__ __device__ inline int64_t tile_off_stride(int64_t d) { return (2 * d + 1 + 7) / 8 * 8; }
+// Sketch tile layout (built by sketch_tiles_kernel, read by sketch_tile_gather).
+// The d sketch rows ("bins") of a 128-column tile are renumbered into slots by
+// entry count, descending; the 128 sketch threads walk the slots in snake
+// order, warp w of pass j taking slots [128 j + 32 w, +32) (j even) or
+// [128 j + 96 - 32 w, +32) (j odd, lane order reversed): a "group" of 32
+// slots of near-equal length per warp. Header (uint16 units):
+//   len[d]  uint8  slot lengths                 (bytes 0 .. d-1)
+//   bin[d]  uint16 the sketch row of each slot  (from tile_hdr_bin(d))
+//   gb[ng]  uint16 byte offset of group g's entries (from tile_hdr_gbase(d))
+// Entries of a group: ceil(L/4) rounds of one 32-bit word per lane, L the
+// group's longest slot (word k of lane l at gb + 4 (32 k + l)); byte c of the
+// word is the lane's entry 4k + c, which feeds its chain c (the sums are those
+// of a slot-contiguous layout with the same entry order). Each round is one
+// conflict-free shared load per warp; bytes past a lane's length are padding.
+// A tile's groups take sum over groups of 128 ceil(L/4) bytes; every tile has
+// the sketch's largest such size (ent_stride, measured when it is built).
+constexpr int kSketchNT = 128;  // sketch threads per tile (fixed by the layout)
+__host__ __device__ inline int64_t tile_groups(int64_t d) {
+  return 4 * ((d + kSketchNT - 1) / kSketchNT);
+}
+__host__ __device__ inline int64_t tile_hdr_bin(int64_t d) { return (d + 1) / 2; }
+__host__ __device__ inline int64_t tile_hdr_gbase(int64_t d) { return (d + 1) / 2 + d; }
+__host__ __device__ inline int64_t tile_off_stride(int64_t d) {
+  return (tile_hdr_gbase(d) + tile_groups(d) + 7) / 8 * 8;
+}
 
 // Sketch epilogue of one 128-row tile (sketch.cpp:51-63 as a gather): thread t
-// of NT sums the tile's contributions to the slots it owns and adds them to
-// acc[bin]. Slots are sorted by length, and thread t takes slots t,
-// 2NT-1-t, 2NT+t, 4NT-1-t, ... (snake), so each warp walks 32 slots of
-// near-equal length and every thread gets about the same number of entries. zs2 holds the scaled
-// z of the tile's rows twice, zs2[r] = +z_r and zs2[128 + r] = -z_r, so an
-// entry byte (local row | sign << 7) indexes its signed value directly.
-template <int NT = 128>
-__device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t* off,
+// sums the tile's contributions to the slots it owns and adds them to
+// acc[bin]. zs2 holds the scaled z of the tile's rows twice, zs2[r] = +z_r and
+// zs2[128 + r] = -z_r, so an entry byte (local row | sign << 7) indexes its
+// signed value directly. The warp runs the group's rounds in lockstep (trip
+// count = the group's longest slot), a lane's padding bytes predicated off.
+// Every lane of the warp executes this (slots past d have length 0).
+__device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t* hdr,
                                                    const uint8_t* ent, const double* zs2,
                                                    double* acc) {
-  const uint16_t* bins = off + d + 1;
+  constexpr int NT = kSketchNT;
+  const uint8_t* lens = reinterpret_cast<const uint8_t*>(hdr);
+  const uint16_t* bins = hdr + tile_hdr_bin(d);
+  const uint16_t* gbase = hdr + tile_hdr_gbase(d);
+  const int lane = t & 31, w = t >> 5;
   for (int j = 0; NT * j < d; ++j) {
     const int s = (j & 1) ? NT * j + NT - 1 - t : NT * j + t;
-    if (s >= d) continue;
-    const int e0 = off[s], len = int(off[s + 1]) - e0;
-    const uint8_t* ep = ent + e0;
-    // four independent chains, four entry bytes off one address register
+    const int len = s < d ? int(lens[s]) : 0;
+    const int mx = int(__reduce_max_sync(0xffffffffu, unsigned(len)));
+    const uint32_t* gw = reinterpret_cast<const uint32_t*>(ent + gbase[4 * j + w]) + lane;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int i = 0;
+    int p = 0;
 #pragma unroll 1
-    for (; i + 4 <= len; i += 4, ep += 4) {
-      a0 += zs2[ep[0]];
-      a1 += zs2[ep[1]];
-      a2 += zs2[ep[2]];
-      a3 += zs2[ep[3]];
+    for (; p + 4 < mx; p += 8, gw += 64) {  // two rounds per iteration
+      const uint32_t e = gw[0], f = gw[32];
+      if (p < len) a0 += zs2[e & 0xffu];
+      if (p + 1 < len) a1 += zs2[(e >> 8) & 0xffu];
+      if (p + 2 < len) a2 += zs2[(e >> 16) & 0xffu];
+      if (p + 3 < len) a3 += zs2[e >> 24];
+      if (p + 4 < len) a0 += zs2[f & 0xffu];
+      if (p + 5 < len) a1 += zs2[(f >> 8) & 0xffu];
+      if (p + 6 < len) a2 += zs2[(f >> 16) & 0xffu];
+      if (p + 7 < len) a3 += zs2[f >> 24];
     }
-    const int r = len - i;  // 0..3 left: predicated, no masked over-read
-    if (r > 0) a0 += zs2[ep[0]];
-    if (r > 1) a1 += zs2[ep[1]];
-    if (r > 2) a2 += zs2[ep[2]];
-    acc[bins[s]] += (a0 + a1) + (a2 + a3);
+    if (p < mx) {
+      const uint32_t e = gw[0];
+      if (p < len) a0 += zs2[e & 0xffu];
+      if (p + 1 < len) a1 += zs2[(e >> 8) & 0xffu];
+      if (p + 2 < len) a2 += zs2[(e >> 16) & 0xffu];
+      if (p + 3 < len) a3 += zs2[e >> 24];
+    }
+    if (s < d) acc[bins[s]] += (a0 + a1) + (a2 + a3);
   }
 }
+
 // mode: 0 = z = xscale*A x ; 1 = also sketch z ; 2 = sketch x only. The
 // sketch comes out as red.groups group partials in red.gpart (detred.cuh:
 // a fixed-order, reproducible reduction); consumers sum them in group order

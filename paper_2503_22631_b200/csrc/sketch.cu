@@ -90,7 +90,8 @@ __global__ void sketch_tiles_kernel(int64_t d, int64_t n, int zeta, int64_t off_
                                     const uint16_t* __restrict__ rows,
                                     const int8_t* __restrict__ signs,
                                     uint16_t* __restrict__ tile_off,
-                                    uint8_t* __restrict__ tile_ent) {
+                                    uint8_t* __restrict__ tile_ent, int64_t ent_stride,
+                                    unsigned long long* __restrict__ size_max) {
   extern __shared__ int sh[];
   int* cnt = sh;                   // d + 1: bin offsets
   int* cur = sh + (d + 1);         // d: insertion cursors, then slot of each bin
@@ -126,7 +127,7 @@ __global__ void sketch_tiles_kernel(int64_t d, int64_t n, int zeta, int64_t off_
     for (int k = 0; k < zeta; ++k) {
       const int r = rows[col * zeta + k];
       const int pos = atomicAdd(&cur[r], 1);
-      ent[pos] = uint8_t(t | (signs[col * zeta + k] < 0 ? 0x80 : 0));
+      ent[pos] = uint8_t(t | (signs && signs[col * zeta + k] < 0 ? 0x80 : 0));
     }
   __syncthreads();
   for (int64_t b = t; b < d; b += blockDim.x) {  // deterministic order inside a bin
@@ -149,63 +150,88 @@ __global__ void sketch_tiles_kernel(int64_t d, int64_t n, int zeta, int64_t off_
     cur[b] = rank;
   }
   __syncthreads();
+  // slot -> bin
+  for (int64_t b = t; b < d; b += blockDim.x) soff[cur[b]] = b;
+  __syncthreads();
+  // group g = 4 j + w holds the slots of warp w in pass j (sketch_tile_gather)
+  auto slot_of = [&](int64_t g, int l) -> int64_t {
+    const int64_t j = g / 4, u = 32 * (g % 4) + l;
+    return (j & 1) ? kSketchNT * j + kSketchNT - 1 - u : kSketchNT * j + u;
+  };
+  auto slot_len = [&](int64_t sl) { return sl < d ? cnt[soff[sl] + 1] - cnt[soff[sl]] : 0; };
+  const int64_t ng = tile_groups(d);
+  if (size_max) {  // sizing pass: this tile's entry bytes
+    if (t == 0) {
+      unsigned long long tot = 0;
+      for (int64_t g = 0; g < ng; ++g) {
+        int mx = 0;
+        for (int l = 0; l < 32; ++l) mx = max(mx, slot_len(slot_of(g, l)));
+        tot += 128ull * unsigned((mx + 3) / 4);
+      }
+      atomicMax(size_max, tot);
+    }
+    return;
+  }
+  // header: slot lengths (uint8), slot bins, group entry offsets
   uint16_t* toff = tile_off + tile * off_stride;
-  for (int64_t b = t; b < d; b += blockDim.x) {
-    soff[cur[b] + 1] = cnt[b + 1] - cnt[b];
-    toff[d + 1 + cur[b]] = uint16_t(b);
+  uint8_t* hlen = reinterpret_cast<uint8_t*>(toff);
+  uint16_t* hbin = toff + tile_hdr_bin(d);
+  uint16_t* hgb = toff + tile_hdr_gbase(d);
+  for (int64_t sl = t; sl < d; sl += blockDim.x) {
+    hlen[sl] = uint8_t(slot_len(sl));
+    hbin[sl] = uint16_t(soff[sl]);
   }
-  __syncthreads();
+  for (int64_t q = d + t; q < 2 * tile_hdr_bin(d); q += blockDim.x) hlen[q] = 0;
   if (t == 0) {
-    soff[0] = 0;
-    for (int64_t q = 1; q <= d; ++q) soff[q] += soff[q - 1];
+    int base = 0;
+    for (int64_t g = 0; g < ng; ++g) {
+      hgb[g] = uint16_t(base);
+      int mx = 0;
+      for (int l = 0; l < 32; ++l) mx = max(mx, slot_len(slot_of(g, l)));
+      base += 128 * ((mx + 3) / 4);
+    }
+    for (int64_t q = tile_hdr_gbase(d) + ng; q < off_stride; ++q) toff[q] = 0;
   }
+  uint8_t* tent = tile_ent + tile * ent_stride;
+  for (int64_t e = t; e < ent_stride; e += blockDim.x) tent[e] = 0;
   __syncthreads();
-  for (int64_t q = t; q <= d; q += blockDim.x) toff[q] = uint16_t(soff[q]);
-  for (int64_t q = 2 * d + 1 + t; q < off_stride; q += blockDim.x) toff[q] = 0;
-  uint8_t* tent = tile_ent + tile * int64_t(kTileRows) * zeta;
-  const int total = cnt[d];
-  __syncthreads();  // slot bins (toff) visible to the whole block
-  // Entry order inside each slot, bank-aware: the 32 slots of a group are
-  // walked by one warp in lockstep (sketch_tile_gather: group = slot / 32), and
-  // at position q every lane loads zs2[entry]; the double at index u sits in
-  // bank pair (u mod 16) = (row mod 16). Greedily give each lane, position by
-  // position, its remaining entry in the least-used bank pair, so the warp's
-  // loads spread over the 16 pairs (~2 wavefronts instead of ~4-5). Only the
-  // summation order inside a bin changes; the layout stays deterministic.
-  const int ngroups = int((d + 31) / 32);
-  for (int g = t; g < ngroups; g += blockDim.x) {
-    const int s0 = 32 * g, s1 = int(min(d, int64_t(s0) + 32));
-    int maxc = 0;
-    for (int sl = s0; sl < s1; ++sl) maxc = max(maxc, soff[sl + 1] - soff[sl]);
-    if (maxc > 64) {  // unusually long bins: keep the column order
-      for (int sl = s0; sl < s1; ++sl) {
-        const int b = toff[d + 1 + sl], src = cnt[b], c = soff[sl + 1] - soff[sl];
-        for (int e = 0; e < c; ++e) tent[soff[sl] + e] = ent[src + e];
-      }
-      continue;
+  // Entry order inside each slot, bank-aware. Round p of a group is one
+  // shared load of zs2 per lane with len > p; a 64-bit load is served per
+  // half-warp, and the double at index u sits in bank pair u mod 16 = row mod
+  // 16. Round by round, every active lane takes its remaining entry whose
+  // bank pair is least used so far in its half-warp. Only the summation order
+  // inside a bin changes; the layout stays deterministic.
+  for (int64_t g = t; g < ng; g += blockDim.x) {
+    int len[32], src[32];
+    uint32_t taken[32][4];
+    int mx = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int64_t sl = slot_of(g, l);
+      len[l] = slot_len(sl);
+      src[l] = sl < d ? cnt[soff[sl]] : 0;
+      mx = max(mx, len[l]);
+      for (int w = 0; w < 4; ++w) taken[l][w] = 0u;
     }
-    uint64_t used[32];
-    for (int l = 0; l < 32; ++l) used[l] = 0;
-    for (int q = 0; q < maxc; ++q) {
-      int load[16];
-      for (int k = 0; k < 16; ++k) load[k] = 0;
-      for (int sl = s0; sl < s1; ++sl) {
-        const int c = soff[sl + 1] - soff[sl];
-        if (q >= c) continue;
-        const int src = cnt[toff[d + 1 + sl]];
+    uint8_t* ge = tent + hgb[g];
+    for (int p = 0; p < mx; ++p) {
+      int load[2][16];
+      for (int h = 0; h < 2; ++h)
+        for (int q = 0; q < 16; ++q) load[h][q] = 0;
+      for (int l = 0; l < 32; ++l) {
+        if (p >= len[l]) continue;
+        int* ld = load[l >> 4];
         int best = -1, bl = 1 << 30;
-        for (int e = 0; e < c; ++e) {
-          if ((used[sl - s0] >> e) & 1ull) continue;
-          const int bank = ent[src + e] & 15;
-          if (load[bank] < bl) { bl = load[bank]; best = e; }
+        for (int e = 0; e < len[l]; ++e) {
+          if ((taken[l][e >> 5] >> (e & 31)) & 1u) continue;
+          const int bank = ent[src[l] + e] & 15;
+          if (ld[bank] < bl) { bl = ld[bank]; best = e; }
         }
-        used[sl - s0] |= 1ull << best;
-        load[ent[src + best] & 15]++;
-        tent[soff[sl] + q] = ent[src + best];
+        taken[l][best >> 5] |= 1u << (best & 31);
+        ld[ent[src[l] + best] & 15]++;
+        ge[4 * (32 * (p >> 2) + l) + (p & 3)] = ent[src[l] + best];
       }
     }
   }
-  for (int e = total + t; e < kTileRows * zeta; e += blockDim.x) tent[e] = 0;
 }
 
 __global__ void sketch_export_kernel(int64_t count, const uint16_t* __restrict__ rows,
@@ -238,18 +264,46 @@ void launch_sketch_generate(int64_t d, int64_t n, int64_t j0, int64_t zeta, uint
   RKMF_CUDA(cudaFreeAsync(dl, st));
 }
 
-void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
-                         const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
-                         cudaStream_t st) {
-  const int64_t tiles = (n + kTileRows - 1) / kTileRows;
-  const int64_t off_stride = tile_off_stride(d);
+namespace {
+size_t tiles_smem(int64_t d, int64_t zeta) {
   const size_t smem = sizeof(int) * size_t(3 * d + 2) + size_t(kTileRows * zeta) + 16;
   if (smem > 200 * 1024) param_error("sketch: d too large for the device tile layout");
   if (smem > 48 * 1024)
     RKMF_CUDA(cudaFuncSetAttribute(sketch_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
-  sketch_tiles_kernel<<<unsigned(tiles), kBlock, smem, st>>>(d, n, int(zeta), off_stride, rows,
-                                                              signs, tile_off, tile_ent);
+  return smem;
+}
+}  // namespace
+
+int64_t sketch_tiles_stride(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
+                            cudaStream_t st) {
+  const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+  if (tiles == 0) return 128;
+  const size_t smem = tiles_smem(d, zeta);
+  unsigned long long* dm = nullptr;
+  RKMF_CUDA(cudaMallocAsync(&dm, sizeof(unsigned long long), st));
+  RKMF_CUDA(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
+  sketch_tiles_kernel<<<unsigned(tiles), kBlock, smem, st>>>(d, n, int(zeta), tile_off_stride(d),
+                                                              rows, nullptr, nullptr, nullptr, 0,
+                                                              dm);
+  RKMF_CUDA(cudaGetLastError());
+  unsigned long long hm = 0;
+  RKMF_CUDA(cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st));
+  RKMF_CUDA(cudaStreamSynchronize(st));
+  RKMF_CUDA(cudaFree(dm));
+  if (hm > 65535) param_error("sketch: a tile's entry layout exceeds 64 KB (zeta too large)");
+  return std::max<int64_t>(128, int64_t(hm));
+}
+
+void launch_sketch_tiles(int64_t d, int64_t n, int64_t zeta, const uint16_t* rows,
+                         const int8_t* signs, uint16_t* tile_off, uint8_t* tile_ent,
+                         int64_t ent_stride, cudaStream_t st) {
+  const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+  if (tiles == 0) return;
+  const size_t smem = tiles_smem(d, zeta);
+  sketch_tiles_kernel<<<unsigned(tiles), kBlock, smem, st>>>(d, n, int(zeta), tile_off_stride(d),
+                                                              rows, signs, tile_off, tile_ent,
+                                                              ent_stride, nullptr);
   RKMF_CUDA(cudaGetLastError());
 }
 

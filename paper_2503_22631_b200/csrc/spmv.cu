@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kBlock)
     spmv_sketch_kernel(int64_t n, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
                        const double* __restrict__ val, const double* __restrict__ x,
                        const double* xscale, double* __restrict__ z, int64_t num_tiles, int cap,
-                       int d, int zeta, int64_t off_stride, const uint16_t* __restrict__ toff,
+                       int d, int ent_stride, int64_t off_stride, const uint16_t* __restrict__ toff,
                        const uint8_t* __restrict__ tent, double sscale,
                        const int32_t* stop, int step, DetRed red) {
   if (stop != nullptr && *stop <= step) return;  // breakdown earlier in this cycle
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kBlock)
   double* zs = acc + (kSketch ? (d + 1) / 2 * 2 : 0);      // [2*128] (+z, -z), 16-byte aligned
   double* prod = zs + (kSketch ? 2 * kTileRows : 0);       // [cap]
   uint16_t* off = reinterpret_cast<uint16_t*>(prod + (kSpmv ? cap : 0));  // [off_stride]
-  uint8_t* ent = reinterpret_cast<uint8_t*>(off + (kSketch ? off_stride : 0));  // [128*zeta]
+  uint8_t* ent = reinterpret_cast<uint8_t*>(off + (kSketch ? off_stride : 0));  // [tile_ent_stride]
 
   const int t = threadIdx.x;
   const double xs = xscale ? *xscale : 1.0;
@@ -92,9 +92,10 @@ __global__ void __launch_bounds__(kBlock)
       zs[kTileRows + t] = -zs[t];
       const uint16_t* go = toff + tile * off_stride;
       for (int q = t; q < off_stride; q += kBlock) off[q] = go[q];
-      const uint4* ge = reinterpret_cast<const uint4*>(tent + tile * int64_t(kTileRows) * zeta);
+      const int64_t es = ent_stride;
+      const uint4* ge = reinterpret_cast<const uint4*>(tent + tile * es);
       uint4* se = reinterpret_cast<uint4*>(ent);
-      for (int q = t; q < 8 * zeta; q += kBlock) se[q] = __ldcs(ge + q);
+      for (int q = t; q < es / 16; q += kBlock) se[q] = __ldcs(ge + q);
       __syncthreads();
       sketch_tile_gather(t, d, off, ent, zs, acc);
       __syncthreads();
@@ -107,11 +108,11 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-size_t smem_bytes(int mode, int cap, int64_t d, int64_t zeta, int64_t off_stride) {
+size_t smem_bytes(int mode, int cap, int64_t d, int64_t ent_stride, int64_t off_stride) {
   size_t s = 0;
   if (mode >= 1) s += sizeof(double) * size_t((d + 1) / 2 * 2 + 2 * kTileRows);
   if (mode <= 1) s += sizeof(double) * size_t(cap);
-  if (mode >= 1) s += sizeof(uint16_t) * size_t(off_stride) + size_t(kTileRows * zeta) + 16;
+  if (mode >= 1) s += sizeof(uint16_t) * size_t(off_stride) + size_t(ent_stride) + 16;
   return (s + 15) / 16 * 16;
 }
 
@@ -158,9 +159,9 @@ int spmv_sketch_grid(const CsrView* A, const SketchView* S, int mode) {
   const int64_t n = A ? A->n_rows : S->n;
   const int64_t tiles = (n + kTileRows - 1) / kTileRows;
   const int cap = A ? A->cap : 0;
-  const int64_t d = S ? S->d : 0, zeta = S ? S->zeta : 0;
+  const int64_t d = S ? S->d : 0, es = S ? S->ent_stride : 0;
   const int64_t off_stride = S ? tile_off_stride(d) : 0;
-  const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
+  const size_t smem = smem_bytes(mode, cap, d, es, off_stride);
   void* fn = pick(A ? A->rp64 : false, mode);
   if (smem > 48 * 1024)
     RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -177,9 +178,9 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
   const int64_t n = A ? A->n_rows : S->n;
   const int64_t tiles = (n + kTileRows - 1) / kTileRows;
   const int cap = A ? A->cap : 0;
-  const int d = S ? int(S->d) : 0, zeta = S ? int(S->zeta) : 0;
+  const int d = S ? int(S->d) : 0, es = S ? int(S->ent_stride) : 0;
   const int64_t off_stride = S ? tile_off_stride(S->d) : 0;
-  const size_t smem = smem_bytes(mode, cap, d, zeta, off_stride);
+  const size_t smem = smem_bytes(mode, cap, d, es, off_stride);
   if (mode == 1 && A && S && use_pipe() &&
       launch_spmv_sketch_pipe(A, S, x, xscale_dev, z, stop_flag, step, red, st))
     return;
@@ -197,7 +198,7 @@ void launch_spmv_sketch(const CsrView* A, const SketchView* S, int mode, const d
 #define RKMF_LAUNCH_SPMV(RP, MODE)                                                             \
   spmv_sketch_kernel<RP, MODE><<<grid, kBlock, smem, st>>>(                                    \
       n, A ? static_cast<const RP*>(A->row_ptr) : nullptr, A ? A->col : nullptr,               \
-      A ? A->val : nullptr, x, xscale_dev, z, tiles, cap, d, zeta, off_stride, toff, tent,     \
+      A ? A->val : nullptr, x, xscale_dev, z, tiles, cap, d, es, off_stride, toff, tent,     \
       sscale, stop_flag, step, red)
   if (smem > 48 * 1024)
     RKMF_CUDA(cudaFuncSetAttribute(pick(rp64, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,

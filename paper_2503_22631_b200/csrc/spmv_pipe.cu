@@ -32,6 +32,17 @@ namespace {
 
 
 constexpr int kStages = 8;
+// doubles per row-dictionary tuple in shared memory (ND rounded up to even)
+template <int ND>
+constexpr int kDictStride = (ND + 1) / 2 * 2;
+// A row dictionary of at most kDictParam doubles travels in the kernel's
+// parameter space (__grid_constant__: read through the constant cache, one
+// access per warp when its rows share a tuple) instead of shared memory,
+// whose 16-byte loads cost the load/store pipe about 13% of its wavefronts.
+constexpr int kDictParam = 224;
+struct DictParam {
+  double v[kDictParam];
+};
 
 
 struct StageLayout {
@@ -41,7 +52,7 @@ struct StageLayout {
 // FMT 0 (CSR): row pointers, up to cap values and columns (+ alignment slack);
 // FMT 2 (DIA): cap = ndiag * 128 values, no row pointers or columns.
 __host__ __device__ inline StageLayout stage_layout(int rp_bytes, int cap, int off_stride,
-                                                    int zeta, int fmt) {
+                                                    int ent_bytes, int fmt) {
   auto r16 = [](uint32_t x) { return (x + 15u) & ~15u; };
   StageLayout L;
   uint32_t o = 0;
@@ -54,7 +65,7 @@ __host__ __device__ inline StageLayout stage_layout(int rp_bytes, int cap, int o
   L.off = o;
   o += r16(uint32_t(off_stride) * 2u);
   L.ent = o;
-  o += r16(uint32_t(kTileRows * zeta));
+  o += r16(uint32_t(ent_bytes));
   L.zs = o;  // zs2: +z then -z of the tile's rows (sketch_tile_gather)
   o += 2 * kTileRows * 8u;
   L.meta = o;
@@ -95,13 +106,13 @@ constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads +
 #define RKMF_PIPE_PARAMS                                                                       \
   int64_t n, const RP *__restrict__ rp, const int32_t *__restrict__ ci,                        \
       const double *__restrict__ val, const double *__restrict__ x, const double *xscale,      \
-      double *__restrict__ z, int64_t num_tiles, int cap, int d, int zeta, int off_stride,     \
+      double *__restrict__ z, int64_t num_tiles, int cap, int d, int ent_stride, int off_stride,     \
       const uint16_t *__restrict__ toff, const uint8_t *__restrict__ tent, double sscale,      \
       const int32_t *stop, int step, int nstages, int l2_hints_arg, int debug_arg,        \
       const int32_t *__restrict__ doff, int ndiag, int64_t ncols, int sync_mode_arg, int dstride,   \
       const double *__restrict__ ddict, int ntup, DetRed red
 #define RKMF_PIPE_ARGS                                                                       \
-  n, rp, ci, val, x, xscale, z, num_tiles, cap, d, zeta, off_stride, toff, tent, sscale, \
+  n, rp, ci, val, x, xscale, z, num_tiles, cap, d, ent_stride, off_stride, toff, tent, sscale, \
       stop, step, nstages, l2_hints_arg, debug_arg, doff, ndiag, ncols, sync_mode_arg, dstride, ddict, ntup, red
 
 // The ablation knobs (RKMF_PIPE_DEBUG / _SYNC / RKMF_L2_HINTS) reach the
@@ -114,14 +125,15 @@ constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads +
 #endif
 
 template <typename RP, int TPR, int G, int FMT, int ND>
-__device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
+__device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpar) {
   const int debug = RKMF_KNOB(debug_arg, 0);
   const int sync_mode = RKMF_KNOB(sync_mode_arg, 1);
   const int l2_hints = RKMF_KNOB(l2_hints_arg, 1);
   constexpr int kSpmv = spmv_threads<TPR, G>();
   constexpr int kGroup = kTileRows * TPR;
   extern __shared__ __align__(128) unsigned char smem[];
-  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, FMT);
+  const int ent_bytes = ent_stride;
+  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, ent_bytes, FMT);
   __shared__ __align__(8) uint64_t full[kStages], zsr[kStages], empty[kStages];
   __shared__ int32_t doff_s[kMaxDiag];  // FMT 2 with one offset list (dstride 0)
   if (FMT && threadIdx.x < kMaxDiag) doff_s[threadIdx.x] = doff ? doff[threadIdx.x] : 0;
@@ -130,8 +142,13 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
   // the PDL wait)
   double* dict_s = acc + (d + 1) / 2 * 2;
   const int t = threadIdx.x;
+  const bool dict_par = ntup * ND <= kDictParam;
   if constexpr (FMT == 3)
-    for (int i = t; i < ntup * ND; i += block_threads<TPR, G>()) dict_s[i] = ddict[i];
+    if (!dict_par)
+    for (int i = t; i < ntup * kDictStride<ND>; i += block_threads<TPR, G>()) {
+      const int tup = i / kDictStride<ND>, q = i % kDictStride<ND>;
+      dict_s[i] = q < ND ? ddict[tup * ND + q] : 0.0;
+    }
   if (t == 0) {
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&full[s], 1);
@@ -199,13 +216,13 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
       const uint32_t cbytes = uint32_t(((re - cs0) * 4 + 15) & ~15LL);
       const uint32_t rbytes = sizeof(RP) == 4 ? 528u : 1040u;
       const uint32_t obytes = uint32_t(off_stride) * 2u;
-      const uint32_t ebytes = uint32_t(kTileRows * zeta);
+      const uint32_t ebytes = uint32_t(ent_bytes);
       if (FMT) {  // one contiguous block of ndiag x 128 values
         const uint32_t dbytes = val ? uint32_t(cap) * 8u : 0u;
         mbar_expect_tx(&full[s], dbytes + obytes + ebytes);
         if (val) bulk_g2s(st + L.val, val + tile * int64_t(cap), dbytes, &full[s], pol);
         bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], mpol);
-        bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], mpol);
+        bulk_g2s(st + L.ent, tent + tile * int64_t(ent_bytes), ebytes, &full[s], mpol);
         if (++s == nstages) {
           s = 0;
           if (it >= nstages) eph ^= 1u;
@@ -224,7 +241,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
         bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s], pol);
       }
       bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], mpol);
-      bulk_g2s(st + L.ent, tent + tile * int64_t(kTileRows) * zeta, ebytes, &full[s], mpol);
+      bulk_g2s(st + L.ent, tent + tile * int64_t(ent_bytes), ebytes, &full[s], mpol);
       if (++s == nstages) {
         s = 0;
         if (it >= nstages) eph ^= 1u;  // rounds 1, 2, ... of each stage
@@ -249,7 +266,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
       }
       unsigned char* st = smem + s * L.stride;
       if (!(debug & 1))
-        sketch_tile_gather<kSketchThreads>(u, d, reinterpret_cast<const uint16_t*>(st + L.off),
+        sketch_tile_gather(u, d, reinterpret_cast<const uint16_t*>(st + L.off),
                                            st + L.ent,
                                            reinterpret_cast<const double*>(st + L.zs), acc);
       // orders this tile's acc updates before the next tile's (slot -> bin
@@ -367,9 +384,21 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
         if constexpr (FMT == 3) {
           // the row's tuple id (one streamed byte) -> its ND values in the
           // shared dictionary: the same values in the same order as FMT 2
-          const double* dv = dict_s + int(st[L.val + rl]) * ND;
+          const int tid = int(st[L.val + rl]);
+          if (dict_par) {
+            const double* dv = dpar.v + tid * ND;
 #pragma unroll
-          for (int q = 0; q < ND; ++q) sum += dv[q] * xc[q];
+            for (int q = 0; q < ND; ++q) sum += dv[q] * xc[q];
+          } else {
+            // (tuples padded to an even count of doubles: 16-byte loads)
+            const double2* dv = reinterpret_cast<const double2*>(dict_s + tid * kDictStride<ND>);
+#pragma unroll
+            for (int q = 0; q < ND; q += 2) {
+              const double2 v = dv[q / 2];
+              sum += v.x * xc[q];
+              if (q + 1 < ND) sum += v.y * xc[q + 1];
+            }
+          }
         } else if (val) {
           const double* vt = reinterpret_cast<const double*>(st + L.val) + rl;
 #pragma unroll
@@ -457,18 +486,18 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS) {
 #endif
 template <typename RP, int TPR, int G, int FMT, int ND = 1>
 __global__ void __launch_bounds__(block_threads<TPR, G>(), RKMF_K2_DIA_MINB)
-    spmv_sketch_pipe_kernel(RKMF_PIPE_PARAMS) {
-  pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS);
+    spmv_sketch_pipe_kernel(RKMF_PIPE_PARAMS, const __grid_constant__ DictParam dpar) {
+  pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS, dpar);
 }
 template <typename RP, int TPR, int G, int FMT, int ND = 1>
 __global__ void __launch_bounds__(block_threads<TPR, G>(), 1)
     spmv_sketch_pipe_csr_kernel(RKMF_PIPE_PARAMS) {
-  pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS);
+  pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS, DictParam{});
 }
 
 template <typename RP>
-size_t pipe_smem(int cap, int d, int off_stride, int zeta, int stages, int fmt, int dict_len = 0) {
-  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, zeta, fmt);
+size_t pipe_smem(int cap, int d, int off_stride, int ent_bytes, int stages, int fmt, int dict_len = 0) {
+  const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, ent_bytes, fmt);
   return size_t(stages) * L.stride + sizeof(double) * size_t((d + 1) / 2 * 2 + dict_len);
 }
 
@@ -543,7 +572,8 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   }();
   // FMT 3 streams one tuple-id byte per row: 128 bytes = 16 "values" per tile
   const int cap = FMT == 3 ? kTileRows / 8 : FMT ? A->ndiag * kTileRows : A->cap;
-  const int dict_len = FMT == 3 ? A->ntup * A->ndiag : 0;
+  const bool dict_par = FMT == 3 && A->ntup * ND <= kDictParam;
+  const int dict_len = FMT == 3 && !dict_par ? A->ntup * kDictStride<ND> : 0;
   // Pick the stage count. G stages feed the SpMV groups and one the sketch,
   // so (stages - G - 1) x resident blocks x stage bytes are in flight ahead
   // of them: take the configuration that keeps >= 64 KB per SM ahead (HBM
@@ -553,7 +583,7 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   static thread_local int64_t keys[4] = {-1, -1, -1, -1};
   static thread_local int bests[4][2];
   static thread_local int next_slot = 0;
-  const int64_t key = (int64_t(cap) << 40) ^ (S->d << 20) ^ (S->zeta << 8) ^ sizeof(RP) ^
+  const int64_t key = (int64_t(cap) << 40) ^ (S->d << 20) ^ (S->ent_stride << 8) ^ sizeof(RP) ^
                       (FMT << 4) ^ (int64_t(ND) << 32) ^ (int64_t(dict_len) << 48);
   int slot = -1;
   for (int i = 0; i < 4; ++i)
@@ -564,10 +594,10 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
     best_per = 0;
     int64_t best_ahead = -1;
     const int64_t stride = int64_t(stage_layout(int(sizeof(RP)), cap, off_stride,
-                                                int(S->zeta), FMT).stride);
+                                                int(S->ent_stride), FMT).stride);
     for (int s = G + 2; s <= kStages; ++s) {
       if (env_stages() && s != env_stages()) continue;
-      const size_t sm = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), s, FMT, dict_len);
+      const size_t sm = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->ent_stride), s, FMT, dict_len);
       if (sm > 220 * 1024) continue;
       RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
       int per = 0;
@@ -592,19 +622,28 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   }
   if (best_s == 0) return false;
   const int stages = best_s, per_sm = best_per;
-  const size_t smem = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->zeta), stages, FMT, dict_len);
+  const size_t smem = pipe_smem<RP>(cap, int(S->d), off_stride, int(S->ent_stride), stages, FMT, dict_len);
   RKMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t tiles = (A->n_rows + kTileRows - 1) / kTileRows;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * sms())));
   if (grid > red.max_blocks || S->d > red.max_len)
     param_error("internal: sketch reduction scratch too small");
   red.groups = det_groups(grid);
-  launch_maybe_pdl(fn, dim3(grid), dim3(kThreads), smem, st, A->n_rows,
-                   static_cast<const RP*>(A->row_ptr), A->col,
-                   FMT == 3 ? reinterpret_cast<const double*>(A->dtid) : FMT ? A->dval : A->val, x,
-                   xscale_dev, z, tiles, cap, int(S->d), int(S->zeta), off_stride, S->tile_off,
-                   S->tile_ent, S->scale, stop, step, stages, env_l2_hints(), env_debug(),
-                   A->doff, A->ndiag, A->n_cols, env_sync(), A->dstride, A->ddict, A->ntup, red);
+#define RKMF_PIPE_LAUNCH_ARGS                                                                  \
+  A->n_rows, static_cast<const RP*>(A->row_ptr), A->col,                                       \
+      FMT == 3 ? reinterpret_cast<const double*>(A->dtid) : FMT ? A->dval : A->val, x,         \
+      xscale_dev, z, tiles, cap, int(S->d), int(S->ent_stride), off_stride, S->tile_off,       \
+      S->tile_ent, S->scale, stop, step, stages, env_l2_hints(), env_debug(), A->doff,         \
+      A->ndiag, A->n_cols, env_sync(), A->dstride, A->ddict, A->ntup, red
+  if constexpr (FMT != 0) {
+    DictParam dp{};
+    if (dict_par && A->ddict_host)
+      for (int i = 0; i < A->ntup * ND; ++i) dp.v[i] = A->ddict_host[i];
+    launch_maybe_pdl(fn, dim3(grid), dim3(kThreads), smem, st, RKMF_PIPE_LAUNCH_ARGS, dp);
+  } else {
+    launch_maybe_pdl(fn, dim3(grid), dim3(kThreads), smem, st, RKMF_PIPE_LAUNCH_ARGS);
+  }
+#undef RKMF_PIPE_LAUNCH_ARGS
   return true;
 }
 

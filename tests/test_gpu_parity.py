@@ -47,6 +47,35 @@ def test_sketch_validation(rk):
 
 
 # ---------------- K2: SpMV + sketch ----------------
+# the sketch tile layout (quad words + tail bytes per 32-slot group, snake
+# passes of 128 slots) across its shapes: one and several passes, partial
+# groups, ragged last tile, long bins (zeta = d), zeta up to the device limit
+@pytest.mark.parametrize("d,n,z", [(40, 300, 5), (24, 24, 24), (30, 200, 1), (120, 65613, 8),
+                                   (200, 100003, 8), (800, 3600, 4), (300, 1000, 64),
+                                   (129, 5000, 16), (1, 129, 1)])
+def test_sketch_layout_shapes(rk, oracle, torch, d, n, z):
+    S = rk.make_sketch(d, n, z, 3)
+    OS = oracle.make_sketch(d, n, z, 3)
+    x = np.random.default_rng(d + n).standard_normal(n)
+    p = rk.sketch_apply(S, x)
+    assert rel(p, oracle.sketch_apply(OS, x)) <= 1e-13
+    # fused with an SpMV (identity-free: a 1D Laplacian, 3 diagonals)
+    rp = np.zeros(n + 1, np.int64)
+    cols, vals = [], []
+    for i in range(n):
+        for j, v in ((i - 1, -1.0), (i, 2.0), (i + 1, -1.0)):
+            if 0 <= j < n:
+                cols.append(j)
+                vals.append(v)
+        rp[i + 1] = len(cols)
+    ci, vv = np.array(cols, np.int32), np.array(vals)
+    A = rk.SparseMatrix.from_csr(rp, ci, vv)
+    zo = oracle.spmv((rp, ci, vv), x)
+    z2, p2 = rk.spmv_sketch(A, S, x)
+    assert rel(z2, zo) <= 1e-14
+    assert rel(p2, oracle.sketch_apply(OS, zo)) <= 1e-13
+
+
 @pytest.mark.parametrize("name,N", [("cfg1", 256), ("cfg2", 40), ("cfg4", 24), ("cfg3", 20)])
 def test_spmv_and_sketch(rk, oracle, torch, name, N):
     from paper_2503_22631_b200 import configs

@@ -31,7 +31,7 @@ x = torch.tensor(P.b, device="cuda")
 rp = 8 if P.nnz >= 2**31 else 4
 nb = 12 * P.nnz + rp * (P.n + 1) + 16 * P.n
 tiles = (P.n + 127) // 128
-sk = tiles * (2 * ((2 * P.d + 1 + 7) // 8 * 8) + 128 * P.zeta)  # sketch tile layout
+sk = tiles * sum(S.layout_bytes_per_tile())  # sketch tile layout
 nd, nt = A.ndiag, A.ntuples
 streams = []
 if nt:
