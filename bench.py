@@ -139,7 +139,7 @@ def class_bytes(n, nnz, m, total_m, cycles):
     final = cycles * (8 * n * m + 8 * n + 16 * n + 8 * n)
     start = (cycles + 1) * 8 * n
     return {"spmv_sketch": spmv, "basis_update": upd, "final_update": final,
-            "start_sketch_init": start}
+            "start_sketch_init": start, "fused_cycle": spmv + upd}
 
 
 def k2_streamed_bytes(n, nnz, ndiag, ntuples, layout):

@@ -119,10 +119,16 @@ int64_t rkmf_context_launch_count(const rkmf_context* ctx);
 /* Per-kernel-class device timing: CUDA events around every launch of the
  * solve (off by default; adds ~1 us gaps, so keep it out of headline runs).
  * Classes: 0 spmv_sketch (K2), 1 rgs_step (K3), 2 basis_update (K4),
- * 3 dense f (K6), 4 final_update (K5), 5 start sketch + init (K7). */
-#define RKMF_KCLASS_COUNT 6
+ * 3 dense f (K6), 4 final_update (K5), 5 start sketch + init (K7),
+ * 6 a cycle's steps fused into one kernel (small matrices, below). */
+#define RKMF_KCLASS_COUNT 7
 int rkmf_context_kernel_timing(rkmf_context* ctx, int enable);
-/* ms[6] accumulated device milliseconds, launches[6] counts; reset != 0 clears. */
+/* Matrices of at most 131072 rows (single rank, randomized builder, m <= 63)
+ * run each cycle's m steps as one cooperative kernel with grid barriers
+ * instead of three launches per step (enable != 0, the default); 0 keeps the
+ * per-step kernels (A/B runs, tests of both paths). */
+int rkmf_context_set_fused_cycle(rkmf_context* ctx, int enable);
+/* ms[7] accumulated device milliseconds, launches[7] counts; reset != 0 clears. */
 int rkmf_context_kernel_times(rkmf_context* ctx, double* ms, int64_t* launches, int reset);
 
 /* ---- CSR matrices (sparse.hpp:16-24). Columns int32; row pointers int64 on

@@ -128,6 +128,7 @@ SYMBOLS = [
     ("rkmf_context_launch_count", C.c_int64, [_P]),
     ("rkmf_context_kernel_timing", C.c_int, [_P, C.c_int]),
     ("rkmf_context_kernel_times", C.c_int, [_P, _P, _P, C.c_int]),
+    ("rkmf_context_set_fused_cycle", C.c_int, [_P, C.c_int]),
     ("rkmf_matrix_create_host", C.c_int, [_P, _I64, _I64, _P, _P, _P, _PP]),
     ("rkmf_matrix_create_device", C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _PP]),
     ("rkmf_matrix_destroy", C.c_int, [_P]),
@@ -206,6 +207,8 @@ def lib():
             pass
         L = C.CDLL(LIB_PATH)
         for name, res, args in SYMBOLS:
+            if os.environ.get("RKMF_LIB_PATH") and not hasattr(L, name):
+                continue  # an older build under A/B comparison (tools/)
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
@@ -268,15 +271,19 @@ class Context:
         return int(lib().rkmf_context_launch_count(self.h))
 
     KERNEL_CLASSES = ("spmv_sketch", "rgs_step", "basis_update", "dense_f", "final_update",
-                      "start_sketch_init")
+                      "start_sketch_init", "fused_cycle")
+
+    def set_fused_cycle(self, enable: bool) -> None:
+        """Small matrices: each cycle's steps as one cooperative kernel (default on)."""
+        self.check(lib().rkmf_context_set_fused_cycle(self.h, int(enable)))
 
     def kernel_timing(self, enable: bool) -> None:
         """Events around every solve launch (diagnostic runs only)."""
         self.check(lib().rkmf_context_kernel_timing(self.h, int(enable)))
 
     def kernel_times(self, reset: bool = True) -> dict:
-        ms = np.zeros(6)
-        cnt = np.zeros(6, np.int64)
+        ms = np.zeros(len(self.KERNEL_CLASSES))
+        cnt = np.zeros(len(self.KERNEL_CLASSES), np.int64)
         self.check(lib().rkmf_context_kernel_times(self.h, _ptr(ms), _ptr(cnt), int(reset)))
         return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(self.KERNEL_CLASSES)}
 

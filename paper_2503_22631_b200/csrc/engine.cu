@@ -177,6 +177,19 @@ SketchSum sketch_allreduce(rkmf_context* ctx, const DetRed& red, int64_t d, DevB
 void run_steps(rkmf_context* ctx, const rkmf_matrix* A, const rkmf_sketch* S,
                const SolveBuffers& b, double tol, bool fuse_last) {
   const SketchView sv = S->view();
+  if (ctx->fused_cycle && !(ctx->comm && ctx->nranks > 1) && !A->partitioned &&
+      cycle_small_applicable(&A->view, &sv, b.m_eff)) {
+    bool ok = false;
+    ctx->timed(6, [&] {
+      ok = launch_cycle_small(&A->view, &sv, int(b.m_eff), fuse_last, b.W, b.ldw, b.z, b.U,
+                              b.Rbar, b.ldr, b.G, tol, b.n_global, ctx->st_dev,
+                              ctx->red_sketch(b.d), ctx->stream);
+    });
+    if (ok) {
+      ctx->launches++;
+      return;
+    }
+  }
   const int grid = spmv_sketch_grid(&A->view, &sv, 1);
   int32_t* stop = &ctx->st_dev->stopped;
   DetRed& red = ctx->red_sketch(b.d);
@@ -442,6 +455,12 @@ int rkmf_context_set_stream(rkmf_context* ctx, void* s) {
 }
 
 int64_t rkmf_context_launch_count(const rkmf_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int rkmf_context_set_fused_cycle(rkmf_context* ctx, int enable) {
+  if (!ctx) return RKMF_PARAMETER_ERROR;
+  ctx->fused_cycle = enable != 0;
+  return RKMF_OK;
+}
 
 int rkmf_context_kernel_timing(rkmf_context* ctx, int enable) {
   return guarded(ctx, [&] {

@@ -184,6 +184,7 @@ struct rkmf_context {
   }
   // ---- optional per-kernel-class timing (rkmf_context_kernel_timing) ----
   bool ktime = false;
+  bool fused_cycle = true;  // small matrices: a cycle's steps in one kernel (cycle_small.cu)
   std::vector<cudaEvent_t> kpool;
   std::vector<std::pair<int, size_t>> kpend;  // (class, index of the start event)
   double kms[RKMF_KCLASS_COUNT] = {0};

@@ -280,6 +280,14 @@ void launch_fx_colmax(int64_t n, const unsigned long long* hi, const unsigned lo
                       const unsigned long long* vmax_bits, double* out, cudaStream_t st);
 void launch_matrix_check(const CsrView* A, int32_t* flags, bool require_sorted, cudaStream_t st);
 
+// cycle_small.cu: a whole cycle's steps in one cooperative kernel (small n)
+constexpr int64_t kCycleSmallMaxRows = 131072;
+bool cycle_small_applicable(const CsrView* A, const SketchView* S, int64_t m_eff);
+bool launch_cycle_small(const CsrView* A, const SketchView* S, int m_eff, bool fuse_last,
+                        double* W, int64_t ldw, double* z, double* U, double* Rbar, int64_t ldr,
+                        double* G, double tol, int64_t n_global, SolveState* st_dev,
+                        DetRed& red, cudaStream_t st);
+
 // krylov.cu
 // the start sketch arrives as ng group partials (detred.cuh)
 void launch_start_init_m(int64_t d, const double* sgpart, int ng, double* U, SolveState* st_dev,

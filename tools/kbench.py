@@ -23,6 +23,11 @@ if "--label" in sys.argv:
     label = sys.argv[sys.argv.index("--label") + 1]
 P = configs.build_device(name)
 A = P.A
+if os.environ.get("RKMF_FUSED") == "0":  # per-step kernels even for small matrices
+    A.ctx.set_fused_cycle(False)
+    label += "+steps"
+if "--no-solve" in sys.argv:
+    pass
 S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, A.ctx)
 x = P.b.clone()
 rk.kernel_bench(A, S, x, 1, 5)
