@@ -32,6 +32,9 @@ namespace {
 constexpr int kCyGroups = 4;                      // tiles in flight per block
 constexpr int kCyThreads = kCyGroups * kTileRows;  // 512
 constexpr int kCyMaxKK = 64;                      // k + 1 <= 64: register triangular solve
+#ifndef RKMF_CY_TWO_LEVEL
+#define RKMF_CY_TWO_LEVEL 1
+#endif
 
 __device__ __forceinline__ double cy_warp_sum(double v) {
 #pragma unroll
@@ -140,6 +143,23 @@ __global__ void __launch_bounds__(kCyThreads)
     }
     grid.sync();
     // ---- B: sketched Gram-Schmidt (K3's Gram form), every block ----
+#if RKMF_CY_TWO_LEVEL
+    // p: one warp per bin sums the blocks' partials (lane l takes blocks l,
+    // l + 32, ... in order, then a fixed butterfly) into red.gpart, a second
+    // barrier, and every block reads the d values
+    {
+      const int nb = int(gridDim.x);
+      for (int j = int(blockIdx.x) * kW + w; j < d; j += nb * kW) {
+        double v = 0.0;
+        for (int b = l; b < nb; b += 32) v += __ldcg(red.part + int64_t(b) * d + j);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (l == 0) red.gpart[j] = v;
+      }
+      grid.sync();
+      for (int jj = t; jj < d; jj += kCyThreads) ps[jj] = __ldcg(red.gpart + jj);
+    }
+#else
     // p = sum over the blocks' partials in a fixed order: nch chunks of
     // consecutive blocks per bin (independent loads in flight), then the
     // chunks in order
@@ -158,6 +178,7 @@ __global__ void __launch_bounds__(kCyThreads)
         ps[j] = s;
       }
     }
+#endif
     const int kk = k + 1;
     const int64_t g0 = int64_t(k) * (k - 1) / 2;  // packed row k starts here
     __syncthreads();

@@ -32,6 +32,11 @@ namespace {
 
 
 constexpr int kStages = 8;
+// diagonal kernels: block b takes chunks of RKMF_K2_CHUNK consecutive tiles,
+// chunk b, b + grid, ... (1 = plain round robin)
+#ifndef RKMF_K2_CHUNK
+#define RKMF_K2_CHUNK 1
+#endif
 // doubles per row-dictionary tuple in shared memory (ND rounded up to even)
 template <int ND>
 constexpr int kDictStride = (ND + 1) / 2 * 2;
@@ -143,6 +148,18 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
   double* dict_s = acc + (d + 1) / 2 * 2;
   const int t = threadIdx.x;
   const bool dict_par = ntup * ND <= kDictParam;
+  // this block's k-th tile and tile count (chunks of CH consecutive tiles)
+  constexpr int64_t CH = FMT ? RKMF_K2_CHUNK : 1;
+  auto tile_of = [&](int64_t k) -> int64_t {
+    return (int64_t(blockIdx.x) + (k / CH) * int64_t(gridDim.x)) * CH + k % CH;
+  };
+  int64_t tcount;
+  {
+    const int64_t nsup = (num_tiles + CH - 1) / CH, b = blockIdx.x;
+    const int64_t ns = nsup > b ? (nsup - b + gridDim.x - 1) / gridDim.x : 0;
+    tcount = ns * CH;
+    if (ns > 0) tcount -= max(int64_t(0), (b + (ns - 1) * int64_t(gridDim.x)) * CH + CH - num_tiles);
+  }
   if constexpr (FMT == 3)
     if (!dict_par)
     for (int i = t; i < ntup * kDictStride<ND>; i += block_threads<TPR, G>()) {
@@ -200,7 +217,8 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
     }
     int s = 0, it = 0;
     uint32_t eph = 0;  // parity of the empty barrier round being waited for
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (; it < tcount; ++it) {
+      const int64_t tile = tile_of(it);
       const long long rs = nrs, re = nre;
       const int64_t nt = tile + gridDim.x;
       if (!FMT && nt < num_tiles) {
@@ -255,7 +273,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
     const int u = t - kSpmv;
     int s = 0;
     uint32_t ph = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int64_t k = 0; k < tcount; ++k) {
       if (sync_mode & 1) {
         // named barrier 8 + s (the SpMV group bar.arrives on it): a hardware
         // barrier, so the waiting sketch warps take no issue slots
@@ -370,11 +388,12 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
     // tile's products consumed the buffer, so the loads are in flight while
     // the thread waits for the tile's stage (the same overlap as a double
     // buffer, half the registers: no spills at four blocks per SM).
+    static_assert(G == 1 || RKMF_K2_CHUNK == 1, "chunked tile runs take one SpMV group");
     double xc[ND];
-    int32_t tile = int32_t(blockIdx.x) + g * int32_t(gridDim.x);
-    const int32_t gstride = G * int32_t(gridDim.x);
-    if (tile < nt32) load_x(tile, xc);
-    for (; tile < nt32; tile += gstride) {
+    int64_t kk = g;
+    int32_t tile = kk < tcount ? int32_t(tile_of(kk)) : nt32;
+    if (kk < tcount) load_x(tile, xc);
+    for (; kk < tcount; kk += G, tile = kk < tcount ? int32_t(tile_of(kk)) : nt32) {
       mbar_wait(&full[s], ph);
       const unsigned char* st = smem + s * L.stride;
       if (!(debug & 4)) {
@@ -418,7 +437,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
       }
       handoff();
       advance();
-      if (tile + gstride < nt32) load_x(tile + gstride, xc);
+      if (kk + G < tcount) load_x(int32_t(tile_of(kk + G)), xc);
     }
     return;
   } else {

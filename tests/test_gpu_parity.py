@@ -21,6 +21,16 @@ def torch():
     return T
 
 
+@pytest.fixture(autouse=True, params=["fused", "steps"])
+def cycle_path(request, rk):
+    """Every test twice: small matrices through the fused cycle kernel
+    (cycle_small.cu, the default) and through the per-step K2/K3/K4 kernels."""
+    ctx = rk.Context.default()
+    ctx.set_fused_cycle(request.param == "fused")
+    yield request.param
+    ctx.set_fused_cycle(True)
+
+
 def rel(a, b):
     a = np.asarray(a.cpu() if hasattr(a, "cpu") else a)
     b = np.asarray(b.cpu() if hasattr(b, "cpu") else b)
@@ -123,28 +133,48 @@ def test_row_dictionary(rk, oracle, torch, name, N, ntup):
     """Constant-coefficient stencils: the diagonal copy's rows take few value
     tuples (3 x 3 boundary classes in 2D, 27 in 3D), so K2 streams one byte
     per row (dia.cu row dictionary). z is bit-identical to the copy without
-    the dictionary and to the CSR kernel; whole solves agree to rounding (the
-    sketch's cross-block sums follow the grid)."""
+    the dictionary and to the CSR kernel; whole solves (through the per-step
+    kernels: the fused small-matrix cycle reads CSR) agree to rounding (the
+    sketch's cross-block sums follow the grid). Dictionaries of at most 224
+    doubles travel as a kernel parameter, larger ones in shared memory: rows
+    scaled by 9 factors take the second path (up to 9 x the tuples)."""
     from paper_2503_22631_b200 import configs
     P = configs.build(name, N)
     A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
     assert A.ndiag > 0 and A.ntuples == ntup
     S = rk.make_sketch(P.d, P.n, P.zeta, 1)
-    z1, p1 = rk.spmv_sketch(A, S, P.b)
     f = rk.FunctionSpec.exp_neg(P.t)
     opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
     b = torch.tensor(P.b, device="cuda")
-    r1 = rk.restarted_krylov(A, b, f, opts, S)
-    assert A.set_row_dictionary(False) == 0 and A.ntuples == 0 and A.ndiag > 0
-    z0, p0 = rk.spmv_sketch(A, S, P.b)
-    r0 = rk.restarted_krylov(A, b, f, opts, S)
-    assert torch.equal(z1, z0) and rel(p1, p0) <= 1e-14
-    assert r1.cycles == r0.cycles and rel(r1.f_hat, r0.f_hat) <= 1e-12
-    assert A.set_diagonal_copy(False) == 0 and A.ntuples == 0
-    zc, _ = rk.spmv_sketch(A, S, P.b)
-    assert torch.equal(z1, zc)
-    assert rel(z1, oracle.spmv((P.row_ptr, P.col_idx, P.values), P.b)) <= 1e-14
-    assert A.set_diagonal_copy(True) > 0 and A.ntuples == ntup
+    A.ctx.set_fused_cycle(False)
+    try:
+        z1, p1 = rk.spmv_sketch(A, S, P.b)
+        r1 = rk.restarted_krylov(A, b, f, opts, S)
+        assert A.set_row_dictionary(False) == 0 and A.ntuples == 0 and A.ndiag > 0
+        z0, p0 = rk.spmv_sketch(A, S, P.b)
+        r0 = rk.restarted_krylov(A, b, f, opts, S)
+        assert torch.equal(z1, z0) and rel(p1, p0) <= 1e-14
+        assert r1.cycles == r0.cycles and rel(r1.f_hat, r0.f_hat) <= 1e-12
+        assert A.set_diagonal_copy(False) == 0 and A.ntuples == 0
+        zc, _ = rk.spmv_sketch(A, S, P.b)
+        assert torch.equal(z1, zc)
+        assert rel(z1, oracle.spmv((P.row_ptr, P.col_idx, P.values), P.b)) <= 1e-14
+        assert A.set_diagonal_copy(True) > 0 and A.ntuples == ntup
+        # up to 9 x the tuples: the shared-memory dictionary (ntup * ndiag > 224)
+        rows = np.repeat(np.arange(P.n), np.diff(P.row_ptr))
+        v8 = P.values * (1.0 + 1e-3 * (rows % 9))
+        B8 = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, v8)
+        assert B8.ndiag > 0 and ntup < B8.ntuples <= 256 and B8.ntuples * B8.ndiag > 224
+        zd, pd = rk.spmv_sketch(B8, S, P.b)
+        rd = rk.restarted_krylov(B8, b, f, opts, S)
+        assert B8.set_row_dictionary(False) == 0
+        zn, pn = rk.spmv_sketch(B8, S, P.b)
+        rn = rk.restarted_krylov(B8, b, f, opts, S)
+        assert torch.equal(zd, zn) and rel(pd, pn) <= 1e-14
+        assert rd.cycles == rn.cycles and rel(rd.f_hat, rn.f_hat) <= 1e-12
+        assert rel(zd, oracle.spmv((P.row_ptr, P.col_idx, v8), P.b)) <= 1e-14
+    finally:
+        A.ctx.set_fused_cycle(True)
     # values that vary per row (> 256 tuples): the copy stays, no dictionary
     v = P.values * (1.0 + 1e-3 * np.random.default_rng(3).random(P.values.size))
     B = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, v)
