@@ -144,12 +144,13 @@ def class_bytes(n, nnz, m, total_m, cycles):
 
 def k2_streamed_bytes(n, nnz, ndiag, ntuples, layout):
     """Bytes K2 streams by design per launch: the matrix stream it actually
-    reads (the diagonal copy's row dictionary: one tuple-id byte per row; the
-    diagonal copy: 8 ndiag per row; else CSR 12 nnz + 4 (n+1)), the sketch
+    reads (a row dictionary, of the diagonal copy or of the CSR rows: one
+    form-id byte per row; the diagonal copy: 8 ndiag per row; else CSR
+    12 nnz + 4 (n+1)), the sketch
     tile layout (per 128-row tile its header and entry block,
     S.layout_bytes_per_tile()), x read and z written."""
     tiles = (n + 127) // 128
-    if ndiag and ntuples:
+    if ntuples:
         mat = tiles * 128
     elif ndiag:
         mat = 8 * ndiag * tiles * 128
@@ -161,6 +162,8 @@ def k2_streamed_bytes(n, nnz, ndiag, ntuples, layout):
 def matrix_stream(A):
     if A.ndiag and A.ntuples:
         return f"diagonal copy ({A.ndiag} diagonals) as a row dictionary ({A.ntuples} tuples)"
+    if A.ntuples:
+        return f"CSR rows as a row dictionary ({A.ntuples} forms)"
     return f"diagonal copy ({A.ndiag} diagonals)" if A.ndiag else "CSR"
 
 

@@ -318,17 +318,20 @@ class SparseMatrix:
         return nd.value
 
     def set_row_dictionary(self, enable: bool) -> int:
-        """Drop (False) or build (True, if the diagonal copy's rows take at
-        most 256 distinct value tuples) the row dictionary the fused SpMV +
-        sketch then streams (one byte per row); returns the tuple count
-        (0 = none). Results are identical."""
+        """Drop (False) or build (True, if the rows take at most 256 distinct
+        forms: the diagonal copy's value tuples, or without a copy the CSR rows
+        up to translation) the row dictionary the fused SpMV + sketch then
+        streams (one byte per row); returns the form count (0 = none). z is
+        identical."""
         nt = C.c_int()
         self.ctx.check(lib().rkmf_matrix_dia_dict(self.h, int(bool(enable)), C.byref(nt)))
         return nt.value
 
     @property
     def ntuples(self) -> int:
-        """Distinct row tuples of the diagonal copy's dictionary (0 = none)."""
+        """Distinct row forms of the row dictionary K2 streams (0 = none): the
+        diagonal copy's value tuples, or, without a copy, the CSR rows up to
+        translation (rowdict.cu)."""
         nt = C.c_int()
         self.ctx.check(lib().rkmf_matrix_dia_dict(self.h, 2, C.byref(nt)))
         return nt.value

@@ -81,17 +81,20 @@ void finish_matrix(rkmf_matrix* M, int64_t max_tile_nnz, bool require_sorted) {
   double* out = reinterpret_cast<double*>(scr + 16);
   DevBuf colsum;
   colsum.ensure(sizeof(double) * size_t(2 * M->view.n_cols + 1));
+  // validate first: norm1 scatters by column index
   launch_matrix_check(&M->view, flags, require_sorted, ctx->stream);
-  launch_matrix_norm1(&M->view, colsum.as<double>(), out, ctx->stream);
-  ctx->launches += 4;
   int32_t hf[2] = {0, 0};
   RKMF_CUDA(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+  RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hf[0]) shape_error("invalid CSR structure (sparse.cpp:61-81 invariants)");
+  if (hf[1]) numerical_error("non-finite matrix entry");
+  launch_matrix_norm1(&M->view, colsum.as<double>(), out, ctx->stream);
+  ctx->launches += 4;
   RKMF_CUDA(cudaMemcpyAsync(&M->norm1, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   RKMF_CUDA(cudaStreamSynchronize(ctx->stream));
   colsum.release();
-  if (hf[0]) shape_error("invalid CSR structure (sparse.cpp:61-81 invariants)");
-  if (hf[1]) numerical_error("non-finite matrix entry");
   if (dia_enabled_by_env()) build_dia(M);
+  if (!M->view.ndiag) build_csr_dict(M);
 }
 
 __global__ void rp_narrow_kernel(int64_t n, const int64_t* __restrict__ src, int32_t* dst) {
@@ -596,6 +599,7 @@ int rkmf_matrix_destroy(rkmf_matrix* M) {
   if (M->halo.send_idx) cudaFree(M->halo.send_idx);
   if (M->halo.sendbuf) cudaFree(M->halo.sendbuf);
   drop_dia(M);
+  drop_csr_dict(M);
   if (M->rp) cudaFree(M->rp);
   if (M->col) cudaFree(M->col);
   if (M->val) cudaFree(M->val);
@@ -607,8 +611,14 @@ int rkmf_matrix_dia(rkmf_matrix* M, int enable, int* ndiag) {
   if (!M) return RKMF_PARAMETER_ERROR;
   return guarded(M->ctx, [&] {
     set_device(M->ctx);
-    if (enable == 1) build_dia(M);
-    else if (enable == 0) drop_dia(M);  // other values: query only
+    if (enable == 1) {  // the diagonal copy, else the CSR row dictionary
+      build_dia(M);
+      if (!M->view.ndiag) build_csr_dict(M);
+      else drop_csr_dict(M);
+    } else if (enable == 0) {  // CSR stream only
+      drop_dia(M);
+      drop_csr_dict(M);
+    }  // other values: query only
     if (ndiag) *ndiag = M->view.ndiag;
   });
 }
@@ -617,9 +627,15 @@ int rkmf_matrix_dia_dict(rkmf_matrix* M, int enable, int* ntuples) {
   if (!M) return RKMF_PARAMETER_ERROR;
   return guarded(M->ctx, [&] {
     set_device(M->ctx);
-    if (enable == 1) build_dia_dict(M);
-    else if (enable == 0) drop_dia_dict(M);  // other values: query only
-    if (ntuples) *ntuples = M->view.ntup;
+    // the diagonal copy's dictionary, or without a copy the CSR row dictionary
+    if (enable == 1) {
+      if (M->view.ndiag) build_dia_dict(M);
+      else build_csr_dict(M);
+    } else if (enable == 0) {
+      drop_dia_dict(M);
+      drop_csr_dict(M);
+    }  // other values: query only
+    if (ntuples) *ntuples = M->view.ndiag ? M->view.ntup : M->view.rntup;
   });
 }
 
@@ -718,6 +734,9 @@ int rkmf_matrix_rp64(rkmf_matrix* M, int enable, int* is64) {
       M->view.row_ptr = rp;
       M->view.rp64 = true;
       M->ctx->launches++;
+      // the point is to run the int64 row-pointer kernels: the CSR stream,
+      // not its row dictionary
+      drop_csr_dict(M);
     }
     if (is64) *is64 = M->view.rp64 ? 1 : 0;
   });

@@ -237,6 +237,10 @@ struct rkmf_matrix {
   uint8_t* dia_tid = nullptr;  // optional row dictionary of the copy: tuple ids
   double* dia_dict = nullptr;  // and the distinct row tuples
   std::vector<double> dia_dict_host;  // host copy (K2 passes small ones as kernel parameters)
+  uint8_t* rd_tid = nullptr;  // optional CSR row dictionary (rowdict.cu): form ids
+  int32_t* rd_cnt = nullptr;  // per form: nonzero count, offsets, values
+  int32_t* rd_off = nullptr;
+  double* rd_val = nullptr;
   bool partitioned = false;
   HaloPlan halo;
   int64_t n_rows_global() const { return partitioned ? halo.n_global : view.n_rows; }
@@ -275,6 +279,9 @@ void build_dia(rkmf_matrix* M);
 void drop_dia(rkmf_matrix* M);
 void build_dia_dict(rkmf_matrix* M);
 void drop_dia_dict(rkmf_matrix* M);
+// rowdict.cu
+void build_csr_dict(rkmf_matrix* M);
+void drop_csr_dict(rkmf_matrix* M);
 bool dia_enabled_by_env();
 // comm.cu
 void comm_allreduce_sum(rkmf_context* ctx, double* buf, size_t count);

@@ -165,7 +165,19 @@ struct CsrView {
   const double* ddict;
   const double* ddict_host;  // host copy of ddict
   int ntup;
+  // optional CSR row dictionary (rowdict.cu; matrices without a diagonal
+  // copy): rtid[tile * 128 + r] = the row's form id; form f has rcnt[f]
+  // nonzeros at column offsets roff[f * kRdMaxNnz + q] (col - row) with values
+  // rval[f * kRdMaxNnz + q], q in column order. rntup == 0 when absent; rkd =
+  // the largest rcnt.
+  const uint8_t* rtid;
+  const int32_t* rcnt;
+  const int32_t* roff;
+  const double* rval;
+  int rntup;
+  int rkd;
 };
+constexpr int kRdMaxNnz = 32;
 constexpr int kMaxDiag = 8;
 constexpr int kMaxTuples = 256;
 // Row-pointer tail padding (entries) and value/column padding (elements)

@@ -115,10 +115,12 @@ constexpr int block_threads() { return spmv_threads<TPR, G>() + kSketchThreads +
       const uint16_t *__restrict__ toff, const uint8_t *__restrict__ tent, double sscale,      \
       const int32_t *stop, int step, int nstages, int l2_hints_arg, int debug_arg,        \
       const int32_t *__restrict__ doff, int ndiag, int64_t ncols, int sync_mode_arg, int dstride,   \
-      const double *__restrict__ ddict, int ntup, DetRed red
+      const double *__restrict__ ddict, int ntup, const int32_t *__restrict__ rcnt,              \
+      const int32_t *__restrict__ roff, const double *__restrict__ rval, int rntup, DetRed red
 #define RKMF_PIPE_ARGS                                                                       \
   n, rp, ci, val, x, xscale, z, num_tiles, cap, d, ent_stride, off_stride, toff, tent, sscale, \
-      stop, step, nstages, l2_hints_arg, debug_arg, doff, ndiag, ncols, sync_mode_arg, dstride, ddict, ntup, red
+      stop, step, nstages, l2_hints_arg, debug_arg, doff, ndiag, ncols, sync_mode_arg, dstride, ddict, \
+      ntup, rcnt, roff, rval, rntup, red
 
 // The ablation knobs (RKMF_PIPE_DEBUG / _SYNC / RKMF_L2_HINTS) reach the
 // kernel only in the experiments build; the product build folds them to
@@ -148,6 +150,18 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
   double* dict_s = acc + (d + 1) / 2 * 2;
   const int t = threadIdx.x;
   const bool dict_par = ntup * ND <= kDictParam;
+  // FMT 4: the CSR row dictionary [rntup][kRdMaxNnz] values, then offsets and
+  // counts, after acc (constant: loaded before the PDL wait)
+  double* rd_val_s = dict_s;
+  int32_t* rd_off_s = reinterpret_cast<int32_t*>(rd_val_s + rntup * kRdMaxNnz);
+  int32_t* rd_cnt_s = rd_off_s + rntup * kRdMaxNnz;
+  if constexpr (FMT == 4) {
+    for (int i = t; i < rntup * kRdMaxNnz; i += block_threads<TPR, G>()) {
+      rd_val_s[i] = rval[i];
+      rd_off_s[i] = roff[i];
+    }
+    for (int i = t; i < rntup; i += block_threads<TPR, G>()) rd_cnt_s[i] = rcnt[i];
+  }
   // this block's k-th tile and tile count (chunks of CH consecutive tiles)
   constexpr int64_t CH = FMT ? RKMF_K2_CHUNK : 1;
   auto tile_of = [&](int64_t k) -> int64_t {
@@ -330,7 +344,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
     else
       mbar_arrive(&zsr[s]);
   };
-  if constexpr (FMT >= 2) {
+  if constexpr (FMT == 2 || FMT == 3) {
     // Diagonal copy, ND diagonals: x is read at row + offset. Those reads do
     // not depend on the staged values, so each thread loads the next tile's x
     // (into the other register buffer) before waiting for this tile's stage.
@@ -440,6 +454,49 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
       if (kk + G < tcount) load_x(int32_t(tile_of(kk + G)), xc);
     }
     return;
+  } else if constexpr (FMT == 4) {
+  // CSR row dictionary: the row's form id (one streamed byte) -> its count,
+  // offsets and values in shared memory (one broadcast per warp when its rows
+  // share the form), walked exactly as the CSR branch below walks the row's
+  // nonzeros: the same products in the same order, so z is bit-identical.
+  for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
+       tile += int64_t(G) * gridDim.x) {
+    mbar_wait(&full[s], ph);
+    unsigned char* st = smem + s * L.stride;
+    if (!(debug & 4)) {
+      double* zs = reinterpret_cast<double*>(st + L.zs);
+      const int64_t row = tile * kTileRows + rl;
+      const bool live = row < n;
+      const int f = live ? int(st[L.val + rl]) : 0;
+      const int hi = live ? rd_cnt_s[f] : 0;
+      const double* vals = rd_val_s + f * kRdMaxNnz;
+      const int32_t* offs = rd_off_s + f * kRdMaxNnz;
+      const int32_t row32 = int32_t(row);
+      double sum = 0.0;
+      for (int e = part; e < hi; e += 8 * TPR) {
+        double v[8], xv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int ee = min(e + TPR * q, hi - 1);
+          v[q] = vals[ee];
+          xv[q] = __ldg(x + uint32_t(row32 + offs[ee]));
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum += (e + TPR * q < hi ? v[q] : 0.0) * xv[q];
+      }
+#pragma unroll
+      for (int o = 1; o < TPR; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      sum *= xs;
+      if (part == 0) {
+        if (live && z) z[row] = sum;
+        const double zt = live ? sum * sscale : 0.0;
+        zs[rl] = zt;
+        zs[kTileRows + rl] = -zt;
+      }
+    }
+    handoff();
+    advance();
+  }
   } else {
   // CSR: adjacent lanes of a row take its nonzeros round-robin and combine
   // their partial sums with a fixed butterfly (deterministic). 8 gathers per
@@ -586,13 +643,17 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   constexpr int kThreads = block_threads<TPR, G>();
   const int off_stride = int(tile_off_stride(S->d));
   auto fn = [] {
-    if constexpr (FMT != 0) return spmv_sketch_pipe_kernel<RP, TPR, G, FMT, ND>;
+    if constexpr (FMT == 2 || FMT == 3) return spmv_sketch_pipe_kernel<RP, TPR, G, FMT, ND>;
     else return spmv_sketch_pipe_csr_kernel<RP, TPR, G, FMT, ND>;
   }();
-  // FMT 3 streams one tuple-id byte per row: 128 bytes = 16 "values" per tile
-  const int cap = FMT == 3 ? kTileRows / 8 : FMT ? A->ndiag * kTileRows : A->cap;
+  // FMT 3/4 stream one id byte per row: 128 bytes = 16 "values" per tile
+  const int cap = FMT >= 3 ? kTileRows / 8 : FMT ? A->ndiag * kTileRows : A->cap;
   const bool dict_par = FMT == 3 && A->ntup * ND <= kDictParam;
-  const int dict_len = FMT == 3 && !dict_par ? A->ntup * kDictStride<ND> : 0;
+  // after acc: the FMT 3 row dictionary (unless a kernel parameter), or the
+  // FMT 4 CSR row dictionary (values, then int32 offsets and counts)
+  const int dict_len =
+      FMT == 3 ? (dict_par ? 0 : A->ntup * kDictStride<ND>)
+               : FMT == 4 ? A->rntup * kRdMaxNnz + (A->rntup * kRdMaxNnz + A->rntup + 1) / 2 : 0;
   // Pick the stage count. G stages feed the SpMV groups and one the sketch,
   // so (stages - G - 1) x resident blocks x stage bytes are in flight ahead
   // of them: take the configuration that keeps >= 64 KB per SM ahead (HBM
@@ -650,11 +711,15 @@ bool launch_pipe_t(const CsrView* A, const SketchView* S, const double* x,
   red.groups = det_groups(grid);
 #define RKMF_PIPE_LAUNCH_ARGS                                                                  \
   A->n_rows, static_cast<const RP*>(A->row_ptr), A->col,                                       \
-      FMT == 3 ? reinterpret_cast<const double*>(A->dtid) : FMT ? A->dval : A->val, x,         \
-      xscale_dev, z, tiles, cap, int(S->d), int(S->ent_stride), off_stride, S->tile_off,       \
+      FMT == 4   ? reinterpret_cast<const double*>(A->rtid)                                    \
+      : FMT == 3 ? reinterpret_cast<const double*>(A->dtid)                                    \
+      : FMT      ? A->dval                                                                     \
+                 : A->val,                                                                     \
+      x, xscale_dev, z, tiles, cap, int(S->d), int(S->ent_stride), off_stride, S->tile_off,    \
       S->tile_ent, S->scale, stop, step, stages, env_l2_hints(), env_debug(), A->doff,         \
-      A->ndiag, A->n_cols, env_sync(), A->dstride, A->ddict, A->ntup, red
-  if constexpr (FMT != 0) {
+      A->ndiag, A->n_cols, env_sync(), A->dstride, A->ddict, A->ntup, A->rcnt, A->roff,        \
+      A->rval, A->rntup, red
+  if constexpr (FMT == 2 || FMT == 3) {
     DictParam dp{};
     if (dict_par && A->ddict_host)
       for (int i = 0; i < A->ntup * ND; ++i) dp.v[i] = A->ddict_host[i];
@@ -693,7 +758,7 @@ int pick_groups(const CsrView* A) {
   return avg <= 10.0 ? 1 : 2;
 }
 
-template <typename RP, int TPR>
+template <typename RP, int TPR, int FMT = 0>
 bool launch_pipe_g(const CsrView* A, const SketchView* S, const double* x,
                    const double* xscale_dev, double* z, const int32_t* stop,
                    int step, DetRed& red, cudaStream_t st) {
@@ -701,20 +766,22 @@ bool launch_pipe_g(const CsrView* A, const SketchView* S, const double* x,
   int g = pick_groups(A);
   while (g > 1 && g * kTileRows * TPR + kSketchThreads + 32 > 1024) --g;
   if (g >= 3 && TPR <= 2)
-    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 3 : 1)>(A, S, x, xscale_dev, z, stop, step, red, st);
+    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 3 : 1), FMT>(A, S, x, xscale_dev, z, stop, step,
+                                                          red, st);
   if (g == 2 && TPR <= 2)
-    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 2 : 1)>(A, S, x, xscale_dev, z, stop, step, red, st);
-  return launch_pipe_t<RP, TPR, 1>(A, S, x, xscale_dev, z, stop, step, red, st);
+    return launch_pipe_t<RP, TPR, (TPR <= 2 ? 2 : 1), FMT>(A, S, x, xscale_dev, z, stop, step,
+                                                          red, st);
+  return launch_pipe_t<RP, TPR, 1, FMT>(A, S, x, xscale_dev, z, stop, step, red, st);
 }
 
-template <typename RP>
+template <typename RP, int FMT = 0>
 bool launch_pipe_rp(const CsrView* A, const SketchView* S, const double* x,
                     const double* xscale_dev, double* z, const int32_t* stop,
                     int step, DetRed& red, cudaStream_t st) {
   switch (pick_tpr(A)) {
-    case 4: return launch_pipe_g<RP, 4>(A, S, x, xscale_dev, z, stop, step, red, st);
-    case 2: return launch_pipe_g<RP, 2>(A, S, x, xscale_dev, z, stop, step, red, st);
-    default: return launch_pipe_g<RP, 1>(A, S, x, xscale_dev, z, stop, step, red, st);
+    case 4: return launch_pipe_g<RP, 4, FMT>(A, S, x, xscale_dev, z, stop, step, red, st);
+    case 2: return launch_pipe_g<RP, 2, FMT>(A, S, x, xscale_dev, z, stop, step, red, st);
+    default: return launch_pipe_g<RP, 1, FMT>(A, S, x, xscale_dev, z, stop, step, red, st);
   }
 }
 
@@ -758,6 +825,8 @@ bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double
     }
 #undef RKMF_DIA
   }
+  if (A->rtid && A->rntup > 0 && A->rkd <= kRdMaxNnz)  // CSR row dictionary
+    return launch_pipe_rp<int32_t, 4>(A, S, x, xscale_dev, z, stop_flag, step, red, st);
   if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
   return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, stop_flag, step, red, st)
                  : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, stop_flag, step, red, st);

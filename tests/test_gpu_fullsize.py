@@ -136,7 +136,12 @@ def test_cfg5_kind_int64_row_pointers(rk, oracle, torch):
     try:
         r64, A64 = _device(rk, torch, P, rp64=True)
         assert A64.rp64 and A64.ndiag == 0
-        r32, A32 = _device(rk, torch, P)
+        A32 = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+        assert A32.ntuples == 27 and A32.set_row_dictionary(False) == 0  # the CSR stream
+        S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+        r32 = rk.restarted_krylov(A32, torch.tensor(P.b, device="cuda"),
+                                  rk.FunctionSpec.exp_neg(P.t),
+                                  rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max), S)
         assert not A32.rp64
         assert torch.equal(r64.f_hat, r32.f_hat)
     finally:

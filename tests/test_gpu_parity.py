@@ -757,3 +757,47 @@ def test_fused_cycle_matches_steps_and_oracle(rk, oracle, torch, name, N):
                                  m_r=P.m, tol=P.tol, k_max=P.k_max)
     assert r1.converged and abs(r1.cycles - oc.cycles) <= 1
     assert rel(r1.f_hat, oc.f_hat) <= 1e-9
+
+
+# ---------------- CSR row dictionary (rowdict.cu) ----------------
+@pytest.mark.parametrize("N", [20, 53])
+def test_csr_row_dictionary(rk, oracle, torch, N):
+    """27-point matrices keep the CSR stream (no diagonal copy), but the
+    constant-coefficient Q1 matrix (cfg5's kind) has one row form per
+    boundary class (27): K2 then streams one byte per row and walks the
+    form's offsets and values from shared memory in the CSR order, so z is
+    bit-identical to the CSR kernel; solves agree to rounding and with the
+    oracle. Lognormal coefficients (cfg3's kind) give every row its own form:
+    no dictionary."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build("cfg5", N)
+    A = rk.SparseMatrix.from_csr(P.row_ptr, P.col_idx, P.values)
+    assert A.ndiag == 0 and A.ntuples == 27
+    S = rk.make_sketch(P.d, P.n, P.zeta, 1)
+    OS = oracle.make_sketch(P.d, P.n, P.zeta, 1)
+    zo = oracle.spmv((P.row_ptr, P.col_idx, P.values), P.b)
+    z1, p1 = rk.spmv_sketch(A, S, P.b)
+    assert rel(z1, zo) <= 1e-14
+    assert rel(p1, oracle.sketch_apply(OS, zo)) <= 1e-13
+    f = rk.FunctionSpec.exp_neg(P.t)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=P.k_max)
+    b = torch.tensor(P.b, device="cuda")
+    A.ctx.set_fused_cycle(False)  # the per-step K2 (small n would take the fused cycle)
+    try:
+        r1 = rk.restarted_krylov(A, b, f, opts, S)
+        assert A.set_row_dictionary(False) == 0 and A.ntuples == 0
+        z0, p0 = rk.spmv_sketch(A, S, P.b)
+        r0 = rk.restarted_krylov(A, b, f, opts, S)
+        assert A.set_row_dictionary(True) == 27
+    finally:
+        A.ctx.set_fused_cycle(True)
+    assert torch.equal(z1, z0) and rel(p1, p0) <= 1e-14
+    assert r1.cycles == r0.cycles and rel(r1.f_hat, r0.f_hat) <= 1e-12
+    o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, oracle.KIND_EXP_NEG,
+                                P.t, S=OS, m_r=P.m, tol=P.tol, k_max=P.k_max)
+    assert r1.converged and abs(r1.cycles - o.cycles) <= 1
+    assert rel(r1.f_hat, o.f_hat) <= 1e-9
+    # lognormal coefficients: a form per row, no dictionary
+    Q = configs.build("cfg3", 12)
+    B = rk.SparseMatrix.from_csr(Q.row_ptr, Q.col_idx, Q.values)
+    assert B.ndiag == 0 and B.ntuples == 0
