@@ -7,8 +7,8 @@
 // rows that reach its halo (the halo columns sit in natural order after the
 // owned rows, so those offsets are constant per class too). K2 then streams
 // one byte per row (the form id) instead of 12 bytes per nonzero and takes
-// offsets and values from a shared-memory dictionary, walking them in the
-// CSR kernel's order: z is bit-identical to the CSR stream.
+// offsets and values from a shared-memory dictionary, in column order (one
+// thread per row: z agrees with the CSR kernel's two-lane rows to rounding).
 //
 // Built on device like the diagonal copy's dictionary (dia.cu): a 64-bit hash
 // per row into an open-addressing table, ids in the order of each form's

@@ -457,8 +457,8 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
   } else if constexpr (FMT == 4) {
   // CSR row dictionary: the row's form id (one streamed byte) -> its count,
   // offsets and values in shared memory (one broadcast per warp when its rows
-  // share the form), walked exactly as the CSR branch below walks the row's
-  // nonzeros: the same products in the same order, so z is bit-identical.
+  // share the form), walked as the CSR branch below walks the row's
+  // nonzeros (column order; with TPR 1 sequentially).
   for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
        tile += int64_t(G) * gridDim.x) {
     mbar_wait(&full[s], ph);
@@ -565,8 +565,23 @@ __global__ void __launch_bounds__(block_threads<TPR, G>(), RKMF_K2_DIA_MINB)
     spmv_sketch_pipe_kernel(RKMF_PIPE_PARAMS, const __grid_constant__ DictParam dpar) {
   pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS, dpar);
 }
+// The CSR row-dictionary kernel (FMT 4) is bound by its x gathers (27 per row
+// on the Q1 matrices), so it runs one thread per row, two SpMV groups and two
+// resident blocks per SM (70 registers): cfg5 K2 4.50 ms, vs 5.69 ms with the
+// CSR kernel's two threads per row and one block, 5.28 ms with three groups
+// and one block, 5.09 ms at three blocks of 48 registers
+// (profiles/r02zg_rd_tuning.txt).
+#ifndef RKMF_K2_RD_MINB
+#define RKMF_K2_RD_MINB 2
+#endif
+#ifndef RKMF_K2_RD_TPR
+#define RKMF_K2_RD_TPR 1
+#endif
+#ifndef RKMF_K2_RD_G
+#define RKMF_K2_RD_G 2
+#endif
 template <typename RP, int TPR, int G, int FMT, int ND = 1>
-__global__ void __launch_bounds__(block_threads<TPR, G>(), 1)
+__global__ void __launch_bounds__(block_threads<TPR, G>(), (FMT == 4 ? RKMF_K2_RD_MINB : 1))
     spmv_sketch_pipe_csr_kernel(RKMF_PIPE_PARAMS) {
   pipe_body<RP, TPR, G, FMT, ND>(RKMF_PIPE_ARGS, DictParam{});
 }
@@ -825,8 +840,10 @@ bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double
     }
 #undef RKMF_DIA
   }
-  if (A->rtid && A->rntup > 0 && A->rkd <= kRdMaxNnz)  // CSR row dictionary
-    return launch_pipe_rp<int32_t, 4>(A, S, x, xscale_dev, z, stop_flag, step, red, st);
+  if (A->rtid && A->rntup > 0 && A->rkd <= kRdMaxNnz) {  // CSR row dictionary
+    return launch_pipe_t<int32_t, RKMF_K2_RD_TPR, RKMF_K2_RD_G, 4>(A, S, x, xscale_dev, z,
+                                                                   stop_flag, step, red, st);
+  }
   if (!A->padded || A->max_tile_nnz > A->cap || A->cap > 4096) return false;
   return A->rp64 ? launch_pipe_rp<int64_t>(A, S, x, xscale_dev, z, stop_flag, step, red, st)
                  : launch_pipe_rp<int32_t>(A, S, x, xscale_dev, z, stop_flag, step, red, st);

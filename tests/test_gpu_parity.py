@@ -765,8 +765,9 @@ def test_csr_row_dictionary(rk, oracle, torch, N):
     """27-point matrices keep the CSR stream (no diagonal copy), but the
     constant-coefficient Q1 matrix (cfg5's kind) has one row form per
     boundary class (27): K2 then streams one byte per row and walks the
-    form's offsets and values from shared memory in the CSR order, so z is
-    bit-identical to the CSR kernel; solves agree to rounding and with the
+    form's offsets and values from shared memory in column order, one thread
+    per row (the CSR kernel interleaves two lanes per row), so z agrees with
+    the CSR kernel to rounding; solves agree to rounding and with the
     oracle. Lognormal coefficients (cfg3's kind) give every row its own form:
     no dictionary."""
     from paper_2503_22631_b200 import configs
@@ -791,7 +792,7 @@ def test_csr_row_dictionary(rk, oracle, torch, N):
         assert A.set_row_dictionary(True) == 27
     finally:
         A.ctx.set_fused_cycle(True)
-    assert torch.equal(z1, z0) and rel(p1, p0) <= 1e-14
+    assert rel(z1, z0) <= 1e-15 and rel(p1, p0) <= 1e-14
     assert r1.cycles == r0.cycles and rel(r1.f_hat, r0.f_hat) <= 1e-12
     o = oracle.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, oracle.KIND_EXP_NEG,
                                 P.t, S=OS, m_r=P.m, tol=P.tol, k_max=P.k_max)
