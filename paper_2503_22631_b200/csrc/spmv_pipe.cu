@@ -473,7 +473,18 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
       const int32_t* offs = rd_off_s + f * kRdMaxNnz;
       const int32_t row32 = int32_t(row);
       double sum = 0.0;
-      for (int e = part; e < hi; e += 8 * TPR) {
+      int e = part;
+      for (; e + TPR * 7 < hi; e += 8 * TPR) {  // full batches: no clamps
+        double v[8], xv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          v[q] = vals[e + TPR * q];
+          xv[q] = __ldg(x + uint32_t(row32 + offs[e + TPR * q]));
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum += v[q] * xv[q];
+      }
+      if (e < hi) {  // the last partial batch
         double v[8], xv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -521,7 +532,18 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
         hi = int((long long)rps[rl + 1] - meta.rs);
       }
       double sum = 0.0;
-      for (int e = lo + part; e < hi; e += 8 * TPR) {
+      int e = lo + part;
+      for (; e + TPR * 7 < hi; e += 8 * TPR) {  // full batches: no clamps
+        double v[8], xv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          v[q] = vals[e + TPR * q];
+          xv[q] = (debug & 2) ? double(cols[e + TPR * q]) : __ldg(x + cols[e + TPR * q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum += v[q] * xv[q];
+      }
+      if (e < hi) {  // the last partial batch
         double v[8], xv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
