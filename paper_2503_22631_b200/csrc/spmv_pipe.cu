@@ -142,6 +142,9 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
   const int ent_bytes = ent_stride;
   const StageLayout L = stage_layout(int(sizeof(RP)), cap, off_stride, ent_bytes, FMT);
   __shared__ __align__(8) uint64_t full[kStages], zsr[kStages], empty[kStages];
+  // shared-space addresses, converted once (not per barrier call)
+  const uint32_t full_u = su32(full), zsr_u = su32(zsr), empty_u = su32(empty);
+  const uint32_t smem_u = su32(smem);
   __shared__ int32_t doff_s[kMaxDiag];  // FMT 2 with one offset list (dstride 0)
   if (FMT && threadIdx.x < kMaxDiag) doff_s[threadIdx.x] = doff ? doff[threadIdx.x] : 0;
   double* acc = reinterpret_cast<double*>(smem + nstages * L.stride);  // [d], sketch threads
@@ -212,7 +215,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
       waited = true;
       asm volatile("griddepcontrol.wait;" ::: "memory");
       if (stop != nullptr && *stop <= step) {
-        for (int i = 0; i < issued; ++i) mbar_wait(&full[i], 0u);
+        for (int i = 0; i < issued; ++i) mbar_wait_u(full_u + 8u * (i), 0u);
         return true;
       }
       return false;
@@ -240,8 +243,9 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
         nre = (long long)rp[min(n, nt * kTileRows + kTileRows)];
       }
       if (it == nstages && !waited && wait_prev(it)) return;
-      if (it >= nstages) mbar_wait(&empty[s], eph);
+      if (it >= nstages) mbar_wait_u(empty_u + 8u * (s), eph);
       unsigned char* st = smem + s * L.stride;
+      const uint32_t st_u = smem_u + uint32_t(s) * L.stride;
       const int64_t r0 = tile * kTileRows;
       const long long vs0 = rs & ~1LL, cs0 = rs & ~3LL;
       const uint32_t vbytes = uint32_t(((re - vs0) * 8 + 15) & ~15LL);
@@ -251,10 +255,10 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
       const uint32_t ebytes = uint32_t(ent_bytes);
       if (FMT) {  // one contiguous block of ndiag x 128 values
         const uint32_t dbytes = val ? uint32_t(cap) * 8u : 0u;
-        mbar_expect_tx(&full[s], dbytes + obytes + ebytes);
-        if (val) bulk_g2s(st + L.val, val + tile * int64_t(cap), dbytes, &full[s], pol);
-        bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], mpol);
-        bulk_g2s(st + L.ent, tent + tile * int64_t(ent_bytes), ebytes, &full[s], mpol);
+        mbar_expect_tx_u(full_u + 8u * s, dbytes + obytes + ebytes);
+        if (val) bulk_g2s_u(st_u + L.val, val + tile * int64_t(cap), dbytes, full_u + 8u * s, pol);
+        bulk_g2s_u(st_u + L.off, toff + tile * off_stride, obytes, full_u + 8u * s, mpol);
+        bulk_g2s_u(st_u + L.ent, tent + tile * int64_t(ent_bytes), ebytes, full_u + 8u * s, mpol);
         if (++s == nstages) {
           s = 0;
           if (it >= nstages) eph ^= 1u;
@@ -266,14 +270,14 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
       meta->vshift = int(rs - vs0);
       meta->cshift = int(rs - cs0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&full[s], rbytes + (re > rs ? vbytes + cbytes : 0u) + obytes + ebytes);
-      bulk_g2s(st + L.rp, rp + r0, rbytes, &full[s], pol);
+      mbar_expect_tx_u(full_u + 8u * s, rbytes + (re > rs ? vbytes + cbytes : 0u) + obytes + ebytes);
+      bulk_g2s_u(st_u + L.rp, rp + r0, rbytes, full_u + 8u * s, pol);
       if (re > rs) {
-        bulk_g2s(st + L.val, val + vs0, vbytes, &full[s], pol);
-        bulk_g2s(st + L.col, ci + cs0, cbytes, &full[s], pol);
+        bulk_g2s_u(st_u + L.val, val + vs0, vbytes, full_u + 8u * s, pol);
+        bulk_g2s_u(st_u + L.col, ci + cs0, cbytes, full_u + 8u * s, pol);
       }
-      bulk_g2s(st + L.off, toff + tile * off_stride, obytes, &full[s], mpol);
-      bulk_g2s(st + L.ent, tent + tile * int64_t(ent_bytes), ebytes, &full[s], mpol);
+      bulk_g2s_u(st_u + L.off, toff + tile * off_stride, obytes, full_u + 8u * s, mpol);
+      bulk_g2s_u(st_u + L.ent, tent + tile * int64_t(ent_bytes), ebytes, full_u + 8u * s, mpol);
       if (++s == nstages) {
         s = 0;
         if (it >= nstages) eph ^= 1u;  // rounds 1, 2, ... of each stage
@@ -293,8 +297,8 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
         // barrier, so the waiting sketch warps take no issue slots
         asm volatile("bar.sync %0, %1;" ::"r"(8 + s), "n"(kGroup + kSketchThreads) : "memory");
       } else {
-        mbar_wait(&zsr[s], ph);
-        mbar_wait(&full[s], ph);  // completed already (the SpMV group waited on it)
+        mbar_wait_u(zsr_u + 8u * (s), ph);
+        mbar_wait_u(full_u + 8u * (s), ph);  // completed already (the SpMV group waited on it)
       }
       unsigned char* st = smem + s * L.stride;
       if (!(debug & 1))
@@ -304,7 +308,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
       // orders this tile's acc updates before the next tile's (slot -> bin
       // ownership changes per tile)
       asm volatile("bar.sync 2, %0;" ::"n"(kSketchThreads) : "memory");
-      if (!(sync_mode & 1) || u == 0) mbar_arrive(&empty[s]);
+      if (!(sync_mode & 1) || u == 0) mbar_arrive_u(empty_u + 8u * (s));
       if (++s == nstages) {
         s = 0;
         ph ^= 1u;
@@ -342,7 +346,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
     if (sync_mode & 1)
       asm volatile("bar.arrive %0, %1;" ::"r"(8 + s), "n"(kGroup + kSketchThreads) : "memory");
     else
-      mbar_arrive(&zsr[s]);
+      mbar_arrive_u(zsr_u + 8u * (s));
   };
   if constexpr (FMT == 2 || FMT == 3) {
     // Diagonal copy, ND diagonals: x is read at row + offset. Those reads do
@@ -408,7 +412,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
     int32_t tile = kk < tcount ? int32_t(tile_of(kk)) : nt32;
     if (kk < tcount) load_x(tile, xc);
     for (; kk < tcount; kk += G, tile = kk < tcount ? int32_t(tile_of(kk)) : nt32) {
-      mbar_wait(&full[s], ph);
+      mbar_wait_u(full_u + 8u * (s), ph);
       const unsigned char* st = smem + s * L.stride;
       if (!(debug & 4)) {
         const int32_t row = tile * kTileRows + rl;
@@ -461,7 +465,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
   // nonzeros (column order; with TPR 1 sequentially).
   for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
        tile += int64_t(G) * gridDim.x) {
-    mbar_wait(&full[s], ph);
+    mbar_wait_u(full_u + 8u * (s), ph);
     unsigned char* st = smem + s * L.stride;
     if (!(debug & 4)) {
       double* zs = reinterpret_cast<double*>(st + L.zs);
@@ -516,7 +520,7 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
   // a zero product.
   for (int64_t tile = blockIdx.x + int64_t(g) * gridDim.x; tile < num_tiles;
        tile += int64_t(G) * gridDim.x) {
-    mbar_wait(&full[s], ph);
+    mbar_wait_u(full_u + 8u * (s), ph);
     unsigned char* st = smem + s * L.stride;
     if (!(debug & 4)) {
       const RP* rps = reinterpret_cast<const RP*>(st + L.rp);
