@@ -26,8 +26,9 @@ A = P.A
 if os.environ.get("RKMF_FUSED") == "0":  # per-step kernels even for small matrices
     A.ctx.set_fused_cycle(False)
     label += "+steps"
-if "--no-solve" in sys.argv:
-    pass
+if "--csrdict" in sys.argv:  # the CSR row dictionary instead of the diagonal copy
+    A.set_diagonal_copy(False)
+    label += f"+csrdict({A.set_row_dictionary(True)})"
 S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, A.ctx)
 x = P.b.clone()
 rk.kernel_bench(A, S, x, 1, 5)
