@@ -586,6 +586,10 @@ __device__ __forceinline__ void pipe_body(RKMF_PIPE_PARAMS, const DictParam& dpa
 #ifndef RKMF_K2_DIA_MINB
 #define RKMF_K2_DIA_MINB 4
 #endif
+// SpMV groups of the diagonal-dictionary kernel (FMT 3)
+#ifndef RKMF_K2_DICT_G
+#define RKMF_K2_DICT_G 1
+#endif
 template <typename RP, int TPR, int G, int FMT, int ND = 1>
 __global__ void __launch_bounds__(block_threads<TPR, G>(), RKMF_K2_DIA_MINB)
     spmv_sketch_pipe_kernel(RKMF_PIPE_PARAMS, const __grid_constant__ DictParam dpar) {
@@ -848,7 +852,7 @@ bool launch_spmv_sketch_pipe(const CsrView* A, const SketchView* S, const double
                              const int32_t* stop_flag, int step, DetRed& red, cudaStream_t st) {
   if (A->ndiag > 0 && A->dtid && A->ntup > 0) {  // row dictionary of the diagonal copy
 #define RKMF_DIT(NDV) \
-  case NDV: return launch_pipe_t<int32_t, 1, 1, 3, NDV>(A, S, x, xscale_dev, z, stop_flag, step, red, st)
+  case NDV: return launch_pipe_t<int32_t, 1, RKMF_K2_DICT_G, 3, NDV>(A, S, x, xscale_dev, z, stop_flag, step, red, st)
     switch (A->ndiag) {
       RKMF_DIT(1); RKMF_DIT(2); RKMF_DIT(3); RKMF_DIT(4);
       RKMF_DIT(5); RKMF_DIT(6); RKMF_DIT(7); RKMF_DIT(8);
