@@ -58,8 +58,7 @@ __global__ void __launch_bounds__(kCyThreads)
   const int dd = (d + 1) / 2 * 2;
   double* zs2 = sm;                                 // [kCyGroups][256]
   double* acc = zs2 + kCyGroups * 2 * kTileRows;    // [kCyGroups][dd]
-  double* mine = acc + kCyGroups * dd;              // [dd]
-  double* ps = mine + dd;                           // [dd]
+  double* ps = acc + kCyGroups * dd;                // [dd]
   double* cs = ps + dd;                             // [kCyMaxKK]
   double* Gs = cs + kCyMaxKK;                       // packed Gram rows 1..k: [kCyMaxKK^2 / 2]
   // U[:,0..m] resident in every block: column 0 from start_init, column k+1
@@ -277,7 +276,7 @@ template <typename RP>
 size_t cycle_small_smem(int d, int m_eff, int64_t gstage) {
   const int dd = (d + 1) / 2 * 2;
   return sizeof(double) *
-             size_t(kCyGroups * 2 * kTileRows + kCyGroups * dd + 2 * dd + kCyMaxKK +
+             size_t(kCyGroups * 2 * kTileRows + kCyGroups * dd + dd + kCyMaxKK +
                     kCyMaxKK * kCyMaxKK / 2 + (m_eff + 1) * d + kCyThreads + 2) +
          size_t(kCyGroups) * size_t((gstage + 15) & ~15);
 }
