@@ -165,3 +165,19 @@ def test_device_generated_cfg4_equals_host(rk, torch):
     hr, hc, hv = rk.gen_convdiff_upwind(cfg["N"], cfg["peclet"], cfg["v"])
     assert np.array_equal(rp, hr) and np.array_equal(ci, hc) and np.array_equal(v, hv)
     assert A.ndiag == 7
+
+
+def test_cfg3_full_size_reaches_the_branch_cut(rk, torch):
+    """cfg3 at its BASELINE size (200^3 lognormal Q1, A^{-1/2}, m = 40, d = 160):
+    the sketched compression's Ritz values leave the positive spectrum of A
+    (a Petrov-Galerkin compression with a non-orthonormal basis); within the
+    first dozen cycles one lies on the branch cut (-inf, 0] of z^{-1/2} and
+    the solver stops with NumericalError instead of integrating through the
+    pole (profiles/r02za_cfg3_sketch_size.txt)."""
+    from paper_2503_22631_b200 import configs
+    P = configs.build_device("cfg3")
+    assert (P.n, P.m, P.d) == (200 ** 3, 40, 160)
+    S = rk.make_sketch(P.d, P.n, P.zeta, configs.SKETCH_SEED, P.A.ctx)
+    opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=12)
+    with pytest.raises(rk.NumericalError, match="branch cut"):
+        rk.restarted_krylov(P.A, P.b, rk.FunctionSpec.inv_sqrt(), opts, S)
