@@ -802,3 +802,38 @@ def test_csr_row_dictionary(rk, oracle, torch, N):
     Q = configs.build("cfg3", 12)
     B = rk.SparseMatrix.from_csr(Q.row_ptr, Q.col_idx, Q.values)
     assert B.ndiag == 0 and B.ntuples == 0
+
+
+@pytest.mark.parametrize("n,m,d,zeta", [(20000, 10, 600, 8), (9000, 63, 256, 4), (120001, 20, 96, 8)])
+def test_fused_cycle_edge_shapes(rk, oracle, torch, n, m, d, zeta):
+    """The fused cycle kernel's edges: a sketch wider than its 512 threads
+    (d = 600), the largest basis it takes (m = 63: k + 1 = 64 in the register
+    triangular solve), more tiles than one round of blocks (70,001 rows: the
+    CSR rows read from L2 instead of staged), ragged last tiles. Against the
+    per-step kernels and the oracle at forced equal cycle counts."""
+    A = H.random_sparse(n, 6.0 / n, n + m, shift=4.0)
+    b = H.random_vector(n, n + 1)
+    t = 1.0 / abs(oracle.norm1(A))
+    S = rk.make_sketch(d, n, zeta, 5)
+    OS = oracle.make_sketch(d, n, zeta, 5)
+    dA = rk.SparseMatrix.from_scipy(A)
+    bd = torch.tensor(b, device="cuda")
+    f = rk.FunctionSpec.exp_neg(t)
+    opts = rk.RestartOptions(m_r=m, tol=1e-30, k_max=2)
+    ctx = dA.ctx
+    ctx.kernel_timing(True)
+    ctx.kernel_times(reset=True)
+    ctx.set_fused_cycle(True)
+    rf = rk.restarted_krylov(dA, bd, f, opts, S)
+    kt = ctx.kernel_times(reset=True)
+    ctx.kernel_timing(False)
+    assert kt["fused_cycle"][1] == 2
+    ctx.set_fused_cycle(False)
+    try:
+        rs = rk.restarted_krylov(dA, bd, f, opts, S)
+    finally:
+        ctx.set_fused_cycle(True)
+    o = oracle.restarted_krylov(A, b, oracle.KIND_EXP_NEG, t, S=OS, m_r=m, tol=1e-30, k_max=2)
+    assert rf.cycles == rs.cycles == o.cycles == 2
+    assert rel(rf.f_hat, rs.f_hat) <= 1e-11
+    assert rel(rf.f_hat, o.f_hat) <= 1e-9
