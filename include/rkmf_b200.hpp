@@ -13,6 +13,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "rkmf_b200.h"
@@ -77,6 +78,8 @@ class Context {
     ctx_.reset(c);
   }
   rkmf_context* get() const { return ctx_.get(); }
+  // small matrices: a cycle's steps as one cooperative kernel (default on)
+  void set_fused_cycle(bool enable) { check(get(), rkmf_context_set_fused_cycle(get(), enable)); }
 
  private:
   struct Del {
@@ -164,6 +167,12 @@ class SketchOperator {
     s_.reset(s);
   }
   void set_scale(double scale) { rkmf_sketch_set_scale(s_.get(), scale); }
+  // bytes per 128-column tile of the layout the fused kernel streams
+  std::pair<int64_t, int64_t> layout_bytes_per_tile() const {
+    int64_t h = 0, e = 0;
+    rkmf_sketch_layout_info(s_.get(), &h, &e);
+    return {h, e};
+  }
   rkmf_sketch* get() const { return s_.get(); }
   const rkmf_context* context() const { return ctx_; }
 

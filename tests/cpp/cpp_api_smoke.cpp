@@ -43,6 +43,20 @@ int main() {
       nf += full.f_hat[i] * full.f_hat[i];
     }
     const double rel = std::sqrt(e / nf);
+    // the same solve through the per-step kernels (the matrix is small enough
+    // for the fused cycle kernel by default): equal to rounding
+    ctx.set_fused_cycle(false);
+    RestartResult steps = restarted_krylov(ctx, dA, b, FunctionSpec::exp_neg(t), o, S);
+    ctx.set_fused_cycle(true);
+    double es = 0;
+    for (size_t i = 0; i < b.size(); ++i)
+      es += (full.f_hat[i] - steps.f_hat[i]) * (full.f_hat[i] - steps.f_hat[i]);
+    const auto lb = S.layout_bytes_per_tile();
+    if (std::sqrt(es / nf) > 1e-11 || steps.cycles != full.cycles || lb.first <= 0 ||
+        lb.second <= 0) {
+      std::printf("cpp_api_smoke: fused vs per-step kernels differ (%.3e)\n", std::sqrt(es / nf));
+      return 1;
+    }
     std::printf("cpp_api_smoke: n=%lld cycles=%lld converged=%d semigroup_rel=%.3e R_accum=%zux\n",
                 (long long)n, (long long)full.cycles, int(full.converged), rel,
                 full.R_accum.size());
