@@ -409,25 +409,8 @@ __global__ void __launch_bounds__(kUpdThreads)
   const int ncol = next ? m_eff : mk;
   double yy = 0.0, ee = 0.0;
   bool bad = false;
-  for (int64_t i = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * kUpdThreads) {
-    double ay = 0.0, aw = 0.0;
-    int c = 0;
-    for (; c + 3 < ncol; c += 4) {
-      double v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = __ldcs(W + int64_t(c + q) * ldw + i);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        ay += v[q] * cg[c + q];
-        aw += v[q] * cr[c + q];
-      }
-    }
-    for (; c < ncol; ++c) {
-      const double v = __ldcs(W + int64_t(c) * ldw + i);
-      ay += v * cg[c];
-      aw += v * cr[c];
-    }
+  // one row of the pass: y_i, f_hat_i (+ error), the next start w_i
+  auto row_tail = [&](int64_t i, double ay, double aw, double zi) {
     const double y = alpha1 * ay;
     bad |= !isfinite(y);
     const double fn = f_hat[i] + y;
@@ -437,7 +420,48 @@ __global__ void __launch_bounds__(kUpdThreads)
       const double e = fn - ref[i];
       ee += e * e;
     }
-    if (next) W[i] = (__ldcs(z + i) - aw) / rkk;
+    if (next) W[i] = (zi - aw) / rkk;
+  };
+  // Two rows per thread with 16-byte last-use loads, four column streams in
+  // flight (the K4 access pattern); the sums run over the columns in order.
+  const int64_t n2 = n / 2;
+  for (int64_t j2 = int64_t(blockIdx.x) * kUpdThreads + threadIdx.x; j2 < n2;
+       j2 += int64_t(gridDim.x) * kUpdThreads) {
+    double ay0 = 0.0, ay1 = 0.0, aw0 = 0.0, aw1 = 0.0;
+    int c = 0;
+    for (; c + 3 < ncol; c += 4) {
+      double2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        v[q] = __ldlu(reinterpret_cast<const double2*>(W + int64_t(c + q) * ldw) + j2);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ay0 += v[q].x * cg[c + q];
+        ay1 += v[q].y * cg[c + q];
+        aw0 += v[q].x * cr[c + q];
+        aw1 += v[q].y * cr[c + q];
+      }
+    }
+    for (; c < ncol; ++c) {
+      const double2 v = __ldlu(reinterpret_cast<const double2*>(W + int64_t(c) * ldw) + j2);
+      ay0 += v.x * cg[c];
+      ay1 += v.y * cg[c];
+      aw0 += v.x * cr[c];
+      aw1 += v.y * cr[c];
+    }
+    const double2 zz = next ? __ldlu(reinterpret_cast<const double2*>(z) + j2) : make_double2(0.0, 0.0);
+    row_tail(2 * j2, ay0, aw0, zz.x);
+    row_tail(2 * j2 + 1, ay1, aw1, zz.y);
+  }
+  if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    const int64_t i = n - 1;
+    double ay = 0.0, aw = 0.0;
+    for (int c = 0; c < ncol; ++c) {
+      const double v = W[int64_t(c) * ldw + i];
+      ay += v * cg[c];
+      aw += v * cr[c];
+    }
+    row_tail(i, ay, aw, next ? z[i] : 0.0);
   }
   yy = block_sum<kUpdThreads>(yy, buf);
   if (ref) ee = block_sum<kUpdThreads>(ee, buf2);

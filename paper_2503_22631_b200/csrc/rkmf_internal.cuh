@@ -223,6 +223,8 @@ __host__ __device__ inline int64_t tile_off_stride(int64_t d) {
 // zs2[128 + r] = -z_r, so an entry byte (local row | sign << 7) indexes its
 // signed value directly. The warp runs the group's rounds in lockstep (trip
 // count = the group's longest slot), a lane's padding bytes predicated off.
+// Entry bytes are extracted with a byte permute (PRMT) so each entry's table
+// address is two instructions (PRMT, IMAD) rather than shift, mask and add.
 // Every lane of the warp executes this (slots past d have length 0).
 __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t* hdr,
                                                    const uint8_t* ent, const double* zs2,
@@ -242,21 +244,21 @@ __device__ __forceinline__ void sketch_tile_gather(int t, int d, const uint16_t*
 #pragma unroll 1
     for (; p + 4 < mx; p += 8, gw += 64) {  // two rounds per iteration
       const uint32_t e = gw[0], f = gw[32];
-      if (p < len) a0 += zs2[e & 0xffu];
-      if (p + 1 < len) a1 += zs2[(e >> 8) & 0xffu];
-      if (p + 2 < len) a2 += zs2[(e >> 16) & 0xffu];
-      if (p + 3 < len) a3 += zs2[e >> 24];
-      if (p + 4 < len) a0 += zs2[f & 0xffu];
-      if (p + 5 < len) a1 += zs2[(f >> 8) & 0xffu];
-      if (p + 6 < len) a2 += zs2[(f >> 16) & 0xffu];
-      if (p + 7 < len) a3 += zs2[f >> 24];
+      if (p < len) a0 += zs2[__byte_perm(e, 0, 0x4440)];
+      if (p + 1 < len) a1 += zs2[__byte_perm(e, 0, 0x4441)];
+      if (p + 2 < len) a2 += zs2[__byte_perm(e, 0, 0x4442)];
+      if (p + 3 < len) a3 += zs2[__byte_perm(e, 0, 0x4443)];
+      if (p + 4 < len) a0 += zs2[__byte_perm(f, 0, 0x4440)];
+      if (p + 5 < len) a1 += zs2[__byte_perm(f, 0, 0x4441)];
+      if (p + 6 < len) a2 += zs2[__byte_perm(f, 0, 0x4442)];
+      if (p + 7 < len) a3 += zs2[__byte_perm(f, 0, 0x4443)];
     }
     if (p < mx) {
       const uint32_t e = gw[0];
-      if (p < len) a0 += zs2[e & 0xffu];
-      if (p + 1 < len) a1 += zs2[(e >> 8) & 0xffu];
-      if (p + 2 < len) a2 += zs2[(e >> 16) & 0xffu];
-      if (p + 3 < len) a3 += zs2[e >> 24];
+      if (p < len) a0 += zs2[__byte_perm(e, 0, 0x4440)];
+      if (p + 1 < len) a1 += zs2[__byte_perm(e, 0, 0x4441)];
+      if (p + 2 < len) a2 += zs2[__byte_perm(e, 0, 0x4442)];
+      if (p + 3 < len) a3 += zs2[__byte_perm(e, 0, 0x4443)];
     }
     if (s < d) acc[bins[s]] += (a0 + a1) + (a2 + a3);
   }
