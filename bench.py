@@ -20,7 +20,8 @@ Workloads (BASELINE.json configs; --config overrides):
 `--gpus N` with N > 1 re-executes itself under torch.distributed.run (one rank
 per GPU) unless it already runs under a launcher. `--impl reference` times the
 reference's CPU solver path on the host cores (the Eigen-free restatement in
-oracle/: the reference itself is not buildable here) on the same
+oracle/, which reproduces the reference's own sources bit for bit, DESIGN.md §4;
+Eigen is absent, so an Eigen build of the reference cannot be timed) on the same
 config; that arm never loads the product library (its inputs come from the
 oracle's own generators, oracle/problems_oracle.cpp).
 """
@@ -246,8 +247,11 @@ def run_reference(args):
             "libraries_mapped": sorted({ln.split()[-1] for ln in maps.splitlines()
                                         if ln.endswith(".so") and ("oracle" in ln
                                                                    or ROOT in ln)}),
-            "note": "the reference (Eigen-based C++) is not buildable in this image; its CPU "
-                    "path is the Eigen-free restatement in oracle/ (DESIGN.md §4)"}
+            "note": "Eigen is absent from this image, so the reference's CPU path is timed as "
+                    "its Eigen-free restatement in oracle/, which reproduces the reference's "
+                    "own sources (oracle/_ref, compiled against an Eigen-API stand-in) bit for "
+                    "bit in a contraction-free build (DESIGN.md §4); oracle/_ref itself is "
+                    "single-threaded stand-in arithmetic, a correctness pin, not a baseline"}
     print(json.dumps(line), flush=True)
     return 0
 

@@ -78,6 +78,8 @@ def raw():
         L.ref_save_mtx.argtypes = [C.c_char_p, i64, i64, P, P, P, C.c_char_p]
         L.ref_load_vector.argtypes = [C.c_char_p, P, P, i64, C.c_char_p]
         L.ref_save_vector.argtypes = [C.c_char_p, P, i64, C.c_char_p]
+        L.ref_convergence_sweep.argtypes = [i64, P, P, P, P, d, P, P, i64, C.c_int, P, i64, P,
+                                            C.c_char_p]
         _raw = L
     return _raw
 
@@ -174,6 +176,45 @@ def save_vector(path: str, x) -> None:
     x = np.ascontiguousarray(x, np.float64)
     err = C.create_string_buffer(512)
     _check(raw().ref_save_vector(path.encode(), _p(x), len(x), err), err)
+
+
+class MethodSpecC(C.Structure):  # layout of rkmf_method_spec (include/rkmf_b200.h)
+    _fields_ = [("name", C.c_char * 32), ("m", C.c_int64), ("d", C.c_int64), ("zeta", C.c_int64),
+                ("tol", C.c_double), ("k_max", C.c_int64), ("seed", C.c_uint64)]
+
+
+class SweepRecordC(C.Structure):  # layout of rkmf_sweep_record
+    _fields_ = [("method", C.c_char * 32), ("n", C.c_int64), ("m_or_totalm", C.c_int64),
+                ("cycle", C.c_int64), ("matvecs", C.c_int64), ("rel_error", C.c_double),
+                ("update_norm", C.c_double), ("kappa_W", C.c_double),
+                ("leftmost_ritz_re", C.c_double), ("elapsed_ms", C.c_double),
+                ("note", C.c_char * 256), ("phase_build_ms", C.c_double),
+                ("phase_eval_ms", C.c_double)]
+
+
+def convergence_sweep(A, b, t: float, methods, reference=None, with_timing: bool = False):
+    """restart::convergence_sweep (restart.cpp:124-305) on {A, b, ExpNeg(t)};
+    methods: objects with name, m, d, zeta, tol, k_max, seed. Rows as dicts."""
+    O = front()
+    rp, ci, v, n, _ = O._csr(A)
+    b = np.ascontiguousarray(b, np.float64)
+    ref = None if reference is None else np.ascontiguousarray(reference, np.float64)
+    ms = (MethodSpecC * max(len(methods), 1))()
+    for i, m in enumerate(methods):
+        ms[i] = MethodSpecC(m.name.encode()[:31], m.m, m.d, m.zeta, m.tol, m.k_max, m.seed)
+    cap = 4096
+    recs = (SweepRecordC * cap)()
+    n_out = C.c_int64()
+    err = C.create_string_buffer(512)
+    _check(raw().ref_convergence_sweep(n, _p(rp), _p(ci), _p(v), _p(b), t, _p(ref),
+                                       C.cast(ms, C.c_void_p), len(methods), int(with_timing),
+                                       C.cast(recs, C.c_void_p), cap, C.byref(n_out), err), err)
+    rows = []
+    for i in range(min(n_out.value, cap)):
+        r = recs[i]
+        rows.append({k: (getattr(r, k).decode() if isinstance(getattr(r, k), bytes)
+                         else getattr(r, k)) for k, _ in SweepRecordC._fields_})
+    return rows
 
 
 _strict = None

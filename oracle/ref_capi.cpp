@@ -309,4 +309,70 @@ int ref_save_vector(const char* path, const double* x, int64_t n, char* err) {
   REF_TRY(sparse::save_vector(make_vec(x, n), path));
 }
 
+// restart::convergence_sweep (restart.cpp:124-305) on an external-kind
+// problem {L, b, f = ExpNeg(t)} (problems.hpp:32-39; no generator needed).
+// The two structs have the layout of the product ABI's rkmf_method_spec /
+// rkmf_sweep_record (include/rkmf_b200.h), so one ctypes definition serves both.
+struct ref_method_spec {
+  char name[32];
+  int64_t m, d, zeta;
+  double tol;
+  int64_t k_max;
+  uint64_t seed;
+};
+struct ref_sweep_record {
+  char method[32];
+  int64_t n, m_or_totalm, cycle, matvecs;
+  double rel_error, update_norm, kappa_W, leftmost_ritz_re, elapsed_ms;
+  char note[256];
+  double phase_build_ms, phase_eval_ms;
+};
+
+int ref_convergence_sweep(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                          const double* b, double t, const double* reference,
+                          const ref_method_spec* methods, int64_t n_methods, int with_timing,
+                          ref_sweep_record* out, int64_t cap, int64_t* n_out, char* err) {
+  REF_TRY({
+    problems::ProblemInstance prob;
+    prob.L = make_csr(n, n, rp, ci, v);
+    prob.b = make_vec(b, n);
+    prob.f = densefun::FunctionSpec::exp_neg(t);
+    std::vector<restart::MethodSpec> ms;
+    for (int64_t i = 0; i < n_methods; ++i) {
+      restart::MethodSpec m;
+      m.name = methods[i].name;
+      m.m = methods[i].m;
+      m.d = methods[i].d;
+      m.zeta = methods[i].zeta;
+      m.tol = methods[i].tol;
+      m.k_max = methods[i].k_max;
+      m.seed = methods[i].seed;
+      ms.push_back(m);
+    }
+    Vector ref;
+    if (reference) ref = make_vec(reference, n);
+    const std::vector<restart::SweepRecord> rows =
+        restart::convergence_sweep(prob, ms, ref, with_timing != 0, 1);
+    *n_out = int64_t(rows.size());
+    for (size_t i = 0; i < rows.size() && int64_t(i) < cap; ++i) {
+      const restart::SweepRecord& r = rows[i];
+      ref_sweep_record& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      std::snprintf(o.method, sizeof(o.method), "%s", r.method.c_str());
+      std::snprintf(o.note, sizeof(o.note), "%s", r.note.c_str());
+      o.n = r.n;
+      o.m_or_totalm = r.m_or_totalm;
+      o.cycle = r.cycle;
+      o.matvecs = r.matvecs;
+      o.rel_error = r.rel_error;
+      o.update_norm = r.update_norm;
+      o.kappa_W = r.kappa_W;
+      o.leftmost_ritz_re = r.leftmost_ritz_re;
+      o.elapsed_ms = r.elapsed_ms;
+      o.phase_build_ms = r.phase_build_ms;
+      o.phase_eval_ms = r.phase_eval_ms;
+    }
+  });
+}
+
 }  // extern "C"

@@ -6,12 +6,23 @@
 // `--impl reference` legs may load this library, and only as the checker or
 // the timed CPU baseline. The product (paper_2503_22631_b200) never links it.
 //
-// Why a restatement: the reference cannot be built here (Eigen3 and vendor/
-// are absent; proj/CMakeLists.txt:5,12), so every function below follows the
-// cited reference file:line and replaces Eigen calls by explicit loops whose
-// summation order is stated. Parity with the reference is therefore at the
-// tolerance level (Eigen's GEMV/GEMM blocking order is not reproducible),
-// bit-exact only for the integer sketch generation.
+// Why a restatement: the reference's own build cannot run here (Eigen3 and
+// vendor/ are absent; proj/CMakeLists.txt:5,12), so every function below
+// follows the cited reference file:line and replaces Eigen calls by explicit
+// loops whose summation order is stated.
+//
+// How it is pinned: `make ref` (oracle/Makefile) compiles the reference's own
+// solver-path sources, unmodified and where they lie, against an Eigen-API
+// stand-in (oracle/eigen_standin) into oracle/_ref/librkmf_ref.so. Compiled
+// contraction-free like that library (liboracle_strict.so), this file
+// reproduces it BIT FOR BIT — sketches, decompositions (W, U, Rbar),
+// restarted f(A)b with both builders (f_hat, R_accum, update norms, counters),
+// funm, breakdown and saturation cases, error classes and messages
+// (tests/test_ref_pin.py, live and through the frozen fixture
+// tests/golden/ref_pin.npz). What stays unpinned is the rounding order of
+// Eigen's own kernels (packet reductions, GEMV/GEMM blocking), which no build
+// without Eigen can reproduce: against an Eigen build of the reference, parity
+// is at the tolerance level, bit-exact only for the integer sketch generation.
 //
 // Function kinds: ExpNeg follows densefun.cpp:119-157 (Pade-13 scaling and
 // squaring). InvSqrt (f(z) = z^{-1/2}) is NOT in the reference

@@ -131,7 +131,7 @@ def test_solve_on_a_file_written_by_the_reference(rk, torch, ref, tmp_path):
     pa, pb = str(tmp_path / "A.mtx"), str(tmp_path / "b.vec")
     ref.save_mtx(pa, rp, ci, v, n)
     ref.save_vector(pb, P["b"])
-    A = rk.SparseMatrix.load_mtx(pa)
+    A = rk.SparseMatrix.from_mtx(pa)
     b = rk.load_vector(pb)
     assert np.array_equal(b, P["b"])
     S = rk.make_sketch(P["d"], n, P["zeta"], P["seed"])
@@ -142,3 +142,33 @@ def test_solve_on_a_file_written_by_the_reference(rk, torch, ref, tmp_path):
                             m_r=P["m"], tol=P["tol"], k_max=P["k_max"],
                             S=Rf.make_sketch(P["d"], n, P["zeta"], P["seed"]))
     assert r.cycles == q.cycles and _rel(r.f_hat.cpu().numpy(), q.f_hat) <= 1e-9
+
+
+def test_device_sweep_matches_reference_sweep(rk, torch, ref):
+    """restart::convergence_sweep (restart.cpp:124-305) row by row: restarted
+    methods on the device against the reference's own sweep on the same
+    {A, b, ExpNeg(t)}; error cells carry the reference's sanitised messages."""
+    P = ref_cases.build("lap3d_N20_cfg1shape")
+    rp, ci, v, n = P["A"]
+    ms = [rk.MethodSpec("restart-rand", m=P["m"], d=P["d"], zeta=P["zeta"], tol=P["tol"],
+                        k_max=P["k_max"], seed=P["seed"]),
+          rk.MethodSpec("restart-rand", m=12, tol=P["tol"], k_max=60, seed=9),  # d = 16 m, zeta 4
+          rk.MethodSpec("restart", m=P["m"], tol=P["tol"], k_max=P["k_max"]),
+          rk.MethodSpec("bogus"),
+          rk.MethodSpec("restart-rand", m=0),
+          rk.MethodSpec("restart", m=10, tol=0.0)]
+    exact = ref.front().restarted_krylov(P["A"], P["b"], 0, P["t"], m_r=40, tol=1e-13, S=None).f_hat
+    want = ref.convergence_sweep(P["A"], P["b"], P["t"], ms, reference=exact)
+    A = rk.SparseMatrix.from_csr(rp, ci, v)
+    got = rk.convergence_sweep(A, P["b"], rk.FunctionSpec.exp_neg(P["t"]), ms, reference=exact)
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        for k in ("method", "n", "m_or_totalm", "cycle", "matvecs", "note"):
+            assert g[k] == w[k], (k, g, w)
+        if w["note"]:
+            assert np.isnan(g["rel_error"]) and np.isnan(w["rel_error"])
+            continue
+        assert g["update_norm"] == pytest.approx(w["update_norm"], rel=1e-5, abs=1e-3 * P["tol"])
+        assert g["rel_error"] == pytest.approx(w["rel_error"], rel=1e-4, abs=1e-12)
+        assert g["kappa_W"] == pytest.approx(w["kappa_W"], rel=1e-6)
+        assert g["leftmost_ritz_re"] == pytest.approx(w["leftmost_ritz_re"], rel=1e-6)
