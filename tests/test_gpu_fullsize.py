@@ -181,3 +181,39 @@ def test_cfg3_full_size_reaches_the_branch_cut(rk, torch):
     opts = rk.RestartOptions(m_r=P.m, tol=P.tol, k_max=12)
     with pytest.raises(rk.NumericalError, match="branch cut"):
         rk.restarted_krylov(P.A, P.b, rk.FunctionSpec.inv_sqrt(), opts, S)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_fullsize_matches_reference_sources_digest(rk, oracle, torch, full_problems, name):
+    """The device solve at the full BASELINE size against the REFERENCE'S OWN
+    sources (oracle/_ref: restart.cpp etc. compiled unmodified against the
+    Eigen-API stand-in), through the digest frozen by
+    tests/golden/make_ref_fullsize.py: f_hat at 8,192 sample rows, and the
+    sparse-sign sketch S f_hat (d = 256; every row of f_hat enters eight
+    entries, E||S e||^2 = ||e||^2, so the digest's relative error estimates the
+    relative 2-norm error of the whole vector), both to BASELINE's 1e-9; equal
+    cycle counts; R_accum, update norms, kappa_W and Ritz values per cycle."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_fullsize.npz")
+    g = np.load(path)
+    P = full_problems[name]
+    n, cycles, total_m, converged = g[f"{name}/meta"].tolist()
+    assert n == P.n
+    r, _ = _device(rk, torch, P, diagnostics=True)
+    assert (r.cycles, r.total_m, int(r.converged)) == (cycles, total_m, converged)
+    f = r.f_hat.cpu().numpy()
+    rows = np.sort(np.random.default_rng(2503).choice(n, 8192, replace=False))
+    assert _rel(f[rows], g[f"{name}/f_samples"]) <= 1e-9
+    assert np.linalg.norm(f) == pytest.approx(g[f"{name}/f_norm"][0], rel=1e-10)
+    D = oracle.make_sketch(256, n, 8, 2503)
+    assert _rel(oracle.sketch_apply(D, f), g[f"{name}/f_digest"]) <= 1e-9
+    R = g[f"{name}/R_accum"]
+    assert np.abs(np.asarray(r.R_accum) - R).max() <= 1e-6 * np.abs(R).max()
+    assert r.alpha == pytest.approx(g[f"{name}/alpha"][0], rel=1e-12)
+    for h, un, kap, rz in zip(r.history, g[f"{name}/update_norm"], g[f"{name}/kappa_W"],
+                              g[f"{name}/ritz_left"]):
+        assert h.update_norm == pytest.approx(un, rel=1e-5, abs=1e-3 * P.tol)
+        assert h.kappa_W == pytest.approx(kap, rel=1e-6)
+        assert h.leftmost_ritz_re == pytest.approx(rz, rel=1e-6, abs=1e-9 * np.abs(R).max())
+    assert [r.counters[k] for k in ("matvecs", "dot_n", "dot_d", "basis_updates",
+                                    "peak_basis_cols")] == g[f"{name}/counters"].tolist()
