@@ -79,15 +79,35 @@ def workload_config(name: str, meta: dict, world: int) -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons during the timed region."""
+    """nvidia-smi clocks/throttle reasons during the timed region. The process
+    is started before the warm-up steps (its start-up and NVML initialisation
+    hold the driver for tens of milliseconds, which must not land in the timed
+    steps); only the samples stamped inside mark_start() .. mark_end() count."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.t0 = self.t1 = None
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def _inside(self, stamp: str) -> bool:
+        if self.t0 is None or self.t1 is None:
+            return True
+        try:
+            import datetime
+            ts = datetime.datetime.strptime(stamp, "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return True
+        return self.t0 - 0.05 <= ts <= self.t1 + 0.05
 
     def __enter__(self):
         try:
@@ -109,12 +129,14 @@ class ClockSampler:
                 self.p.kill()
 
     def summary(self):
+        lines = [[x.strip() for x in ln.split(",")] for ln in (self.out or "").splitlines()]
+        lines = [f for f in lines if len(f) >= 9]
+        inside = [f for f in lines if self._inside(f[0])]
+        if inside:  # (a timed region shorter than the sampling period: keep every sample)
+            lines = inside
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in (self.out or "").splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
+        for f in lines:
             try:
                 sm.append(float(f[1]))
                 mx.append(float(f[2]))
@@ -395,6 +417,8 @@ def run_ours(args):
     ctx.set_stream(stream)
     A, S, f, opts, b_dev = w.A, w.S, w.f, w.opts, w.b_dev
 
+    clk = ClockSampler(local)
+    clk.__enter__()  # before the warm-up: see ClockSampler
     for _ in range(args.warmup):
         res = rk.restarted_krylov(A, b_dev, f, opts, S)
 
@@ -406,9 +430,10 @@ def run_ours(args):
     launches0 = ctx.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     flush = l2_resident(int(w.meta["n"]), int(w.meta["nnz"]), w.m)
-    with ClockSampler(local) as clk:
+    try:
         barrier()
         torch.cuda.synchronize()
+        clk.mark_start()
         total_m = 0
         if flush:  # L2-resident working set: flush before each step, time the steps only
             junk = torch.empty(2 * L2_BYTES // 8, dtype=torch.float64, device=dev)
@@ -428,7 +453,10 @@ def run_ours(args):
                 total_m += res.total_m
             e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
         barrier()
+    finally:
+        clk.__exit__()
     gpu_launches = ctx.launch_count - launches0
     ms = sum(a.elapsed_time(c) for a, c in pairs) if flush else e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64)  # max over ranks (CPU tensor: gloo)
