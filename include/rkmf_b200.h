@@ -337,9 +337,11 @@ int rkmf_matrix_save_mtx(rkmf_context* ctx, const rkmf_matrix* A, const char* pa
  * SweepRecord (restart.hpp:81-129, restart.cpp:124-305) and the CLI's CSV
  * (rkmf_bench.cpp:172-186). Methods "restart" (classical builder) and
  * "restart-rand" (d = 16 m unless given) run on the device, one row per
- * cycle; a failing or unsupported cell (the one-shot approximants "arnoldi",
- * "incomplete", "rand", "rand-ls", "sfom" are not on the device path) becomes
- * one NaN row carrying the sanitised message. Rows keep the method order;
+ * cycle; the one-shot approximants "arnoldi" and "rand" (d = 4 m unless given)
+ * are the first cycle of those methods and become one row with cycle 0; a
+ * failing or unsupported cell (the one-shot approximants "incomplete",
+ * "rand-ls", "sfom" are not on the device path) becomes one NaN row carrying
+ * the sanitised message. Rows keep the method order;
  * without timing the CSV is byte-identical across reruns. ---- */
 typedef struct {
   char name[32];

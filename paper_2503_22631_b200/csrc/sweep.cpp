@@ -7,9 +7,10 @@
 // with d = 16 m_r unless given, restart.cpp:229-233) run through
 // rkmf_restarted_krylov and become one row per cycle; a failing cell becomes
 // a single NaN row carrying the sanitised error text and the sweep goes on
-// (restart.cpp:276-286). The one-shot approximants ("arnoldi", "incomplete",
-// "rand", "rand-ls", "sfom") are outside the device hot path:
-// their cells become such a note row. Rows keep the config order; with
+// (restart.cpp:276-286). Of the one-shot approximants, "arnoldi" and "rand"
+// are the first cycle of the restarted methods and run as such (one row,
+// cycle 0); "incomplete", "rand-ls" and "sfom" are outside the device hot path
+// (SURVEY.md §2): their cells become such a note row. Rows keep the config order; with
 // with_timing off the output is byte-deterministic (the device solves are
 // bitwise reproducible, detred.cuh), as acceptance criterion c14 asks
 // (proj/tests/acceptance.cpp:545-582). Cells run one after another on the
@@ -60,15 +61,25 @@ std::vector<rkmf_sweep_record> run_cell(rkmf_context* ctx, const rkmf_matrix* A,
                                         const double* ref, const rkmf_method_spec& ms,
                                         int with_timing) {
   const std::string name(ms.name);
-  if (one_shot(name))
+  // The one-shot approximants f_m = beta W_m f(R_m) e_1 on the classical
+  // basis ("arnoldi", approximants.cpp:49-60) and alpha W_m f(R_m) e_1 on the
+  // randomized one ("rand", approximants.cpp:62-70; d = 4 m unless given,
+  // restart.cpp:170-171) are exactly the first cycle of the corresponding
+  // restarted method, so they run as one cycle and become one row with
+  // cycle = 0 (restart.cpp:199-221; sampled m = {min(m, n)}, restart.cpp:132-142).
+  const bool shot = name == "arnoldi" || name == "rand";
+  if (one_shot(name) && !shot)
     throw CellError{"method '" + name + "' is a one-shot approximant: not on the device path"};
-  if (name != "restart" && name != "restart-rand")
+  if (!shot && name != "restart" && name != "restart-rand")
     throw CellError{"sweep: unknown method name '" + name + "'"};
+  const int64_t m_shot = std::min<int64_t>(ms.m, n);
+  if (shot && m_shot < 1) throw CellError{"sweep: sampled m values must be >= 1"};
   rkmf_restart_options o;
   rkmf_restart_options_default(&o);
-  o.m_r = ms.m;
-  o.tol = ms.tol;
-  o.k_max = ms.k_max;
+  o.m_r = shot ? m_shot : ms.m;
+  o.tol = shot ? std::numeric_limits<double>::min() : ms.tol;
+  o.k_max = shot ? 1 : ms.k_max;
+  if (shot) o.budget_total_m = std::max<int64_t>(o.budget_total_m, m_shot);
   o.diagnostics = 1;  // kappa_W and the leftmost Ritz value per cycle (restart.cpp:101,103)
   rkmf_sketch* S = nullptr;
   auto fail = [&](int code) {
@@ -78,8 +89,8 @@ std::vector<rkmf_sweep_record> run_cell(rkmf_context* ctx, const rkmf_matrix* A,
       throw CellError{msg};
     }
   };
-  if (name == "restart-rand") {
-    const int64_t d = ms.d > 0 ? ms.d : 16 * ms.m;
+  if (name == "restart-rand" || name == "rand") {
+    const int64_t d = ms.d > 0 ? ms.d : (shot ? 4 * m_shot : 16 * ms.m);
     fail(rkmf_sketch_create(ctx, d, n, ms.zeta, ms.seed, &S));
   }
   std::vector<double> f(static_cast<size_t>(n));
@@ -93,7 +104,7 @@ std::vector<rkmf_sweep_record> run_cell(rkmf_context* ctx, const rkmf_matrix* A,
     const rkmf_cycle_record& c = recs[static_cast<size_t>(i)];
     rkmf_sweep_record r = base_row(ms, n);
     r.m_or_totalm = c.total_m;
-    r.cycle = c.cycle;
+    r.cycle = shot ? 0 : c.cycle;
     r.matvecs = c.total_matvecs;
     if (ref && !std::isnan(c.error_vs_reference)) r.rel_error = c.error_vs_reference;
     r.update_norm = c.update_norm;

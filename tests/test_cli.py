@@ -66,6 +66,7 @@ def test_run_sweep_csv_is_deterministic(tmp_path):
                 "k_max": 6, "seed": 1},
                {"name": "restart", "m_r": 30, "tol": 1e-10, "k_max": 6},
                {"name": "rand", "m": 40},
+               {"name": "sfom", "m": 40},
                {"name": "restart-rand", "m_r": 30, "d": 10, "k_max": 2}]
     cfg = {"problem": {"kind": "baseline", "config": "cfg1", "N": 64},
            "methods": methods, "reference": {"mode": "restart-highm"}}
@@ -87,8 +88,12 @@ def test_run_sweep_csv_is_deterministic(tmp_path):
     assert float(rr[-1][5]) <= 1e-8 and float(rc[-1][5]) <= 1e-8
     # kappa_W and the leftmost Ritz value are filled (restart.cpp:101,103)
     assert all(float(r[7]) >= 1.0 for r in rr)
-    # the one-shot method and the failing cell: one NaN row each with a note
-    one = [r for r in rows if r[0] == "rand"]
+    # "rand" = the first cycle of restart-rand with d = 4 m: one row, cycle 0
+    shot = [r for r in rows if r[0] == "rand"]
+    assert len(shot) == 1 and shot[0][2] == "40" and shot[0][3] == "0" and shot[0][4] == "40"
+    assert shot[0][10] == "" and float(shot[0][5]) < 1.0 and float(shot[0][7]) >= 1.0
+    # the unsupported one-shot method and the failing cell: one NaN row each with a note
+    one = [r for r in rows if r[0] == "sfom"]
     assert len(one) == 1 and one[0][5] == "nan" and "one-shot" in one[0][10]
     bad = [r for r in rows if r[0] == "restart-rand" and r[3] == "0"]
     assert len(bad) == 1 and bad[0][10] != ""

@@ -154,6 +154,10 @@ def test_device_sweep_matches_reference_sweep(rk, torch, ref):
                         k_max=P["k_max"], seed=P["seed"]),
           rk.MethodSpec("restart-rand", m=12, tol=P["tol"], k_max=60, seed=9),  # d = 16 m, zeta 4
           rk.MethodSpec("restart", m=P["m"], tol=P["tol"], k_max=P["k_max"]),
+          rk.MethodSpec("rand", m=24, seed=5),                      # one-shot: d = 4 m, cycle 0
+          rk.MethodSpec("rand", m=P["m"], d=P["d"], zeta=P["zeta"], seed=P["seed"]),
+          rk.MethodSpec("arnoldi", m=18),
+          rk.MethodSpec("rand", m=0),
           rk.MethodSpec("bogus"),
           rk.MethodSpec("restart-rand", m=0),
           rk.MethodSpec("restart", m=10, tol=0.0)]
