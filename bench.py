@@ -251,6 +251,28 @@ def run_reference(args):
     tot_m = sum(v[0] for v in vals)
     tot_t = sum(v[1] for v in vals)
     value = tot_m / tot_t * scale
+    # the reference's OWN sources (oracle/_ref: compiled against the Eigen-API
+    # stand-in, single-threaded like the reference's solve) on a bounded sample:
+    # one 5-vector cycle. Reported beside the line, not as its value: the
+    # stand-in's index-order loops are not Eigen's vector kernels, and the
+    # 16-thread port above is the faster (more conservative) CPU number.
+    ref_src = None
+    try:
+        from oracle import ref as R
+        if world == 1 and P.fn == "exp_neg" and R.available():
+            Rf = R.front()
+            key = (P.d, P.n, P.zeta)
+            t0 = time.perf_counter()
+            rr = Rf.restarted_krylov((P.row_ptr, P.col_idx, P.values), P.b, 0, P.t, m_r=5,
+                                     tol=1e-300, k_max=1, S=_ORACLE_SKETCH[key])
+            dt = time.perf_counter() - t0
+            ref_src = {"value": rr.total_m / dt * scale, "unit": UNIT, "cores": 1,
+                       "kind": "reference",
+                       "sample": f"one 5-vector restart cycle of {what} through oracle/_ref "
+                                 f"(restart.cpp etc. compiled unmodified against the Eigen-API "
+                                 f"stand-in), {dt:.1f} s"}
+    except Exception as e:  # the pin library is optional here
+        ref_src = {"unavailable": str(e)[:200]}
     maps = open("/proc/self/maps").read()
     assert "librkmf_b200" not in maps, "the reference arm must not map the product library"
     sample = (f"one restart cycle (m={P.m} basis vectors, incl. the reference's per-cycle "
@@ -266,6 +288,7 @@ def run_reference(args):
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
+            "reference_sources": ref_src,
             "libraries_mapped": sorted({ln.split()[-1] for ln in maps.splitlines()
                                         if ln.endswith(".so") and ("oracle" in ln
                                                                    or ROOT in ln)}),
